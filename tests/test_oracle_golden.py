@@ -1,0 +1,117 @@
+"""Pin the CPU oracle (oracle/sfft_oracle.py) against the reference's own outputs
+stored by tests/golden/make_golden.py.  CPU only."""
+
+import numpy as np
+import pytest
+
+from conftest import (load_golden, oracle_cfg, regen_signal, runner_cases, sig_checksum,
+                      stage_signal)
+from oracle import sfft_oracle as O
+
+
+def test_filter_support_and_response():
+    z = load_golden("stage_filter")
+    for key in z.files:
+        if key.startswith("support_"):
+            _, n, b = key.split("_")
+            assert O.flat_support(int(n), int(b)) == int(z[key][0])
+    for n, b in [(2048, 16), (65536, 256), (3000, 24)]:
+        w = O.flat_window(n, b)
+        np.testing.assert_array_equal(w.taps, z[f"taps_{n}_{b}"])
+        resp = w.response if n < 10000 else w.response[::37]
+        np.testing.assert_array_equal(resp, z[f"resp_{n}_{b}"])
+
+
+def test_flat_bucketize_golden():
+    z = load_golden("stage_flat")
+    off = 0
+    for i, (n, b, sup, s, t, bp, te) in enumerate(z["meta"]):
+        x = stage_signal(20240901 + i, int(n))
+        np.testing.assert_array_equal(sig_checksum(x), z["checksum"][i])
+        acc = O.Access(x)
+        y = O.flat_buckets(acc, O.flat_window(int(n), int(b), int(sup)), int(s), int(t),
+                           int(bp), int(te))
+        np.testing.assert_array_equal(y, z["y"][off:off + b])
+        assert acc.count() == z["access"][i]
+        off += b
+
+
+def test_spike_bucketize_golden():
+    z = load_golden("stage_spike")
+    off = 0
+    for i, (n, b, t) in enumerate(z["meta"]):
+        x = stage_signal(20240902 + i, int(n))
+        acc = O.Access(x)
+        y = O.spike_buckets(acc, int(b), int(t))
+        np.testing.assert_array_equal(y, z["y"][off:off + b])
+        assert acc.count() == z["access"][i]
+        off += b
+
+
+def test_decode_stages_golden():
+    z = load_golden("stage_decode")
+    off = 0
+    for ln, want in zip(z["floor_lens"], z["floor_out"]):
+        assert O.noise_floor(z["floor_in"][off:off + ln]) == want
+        off += ln
+    n, k, b, R = (int(v) for v in z["vote_meta"])
+    win = O.flat_window(n, b)
+    acc = O.Access(z["vote_x"])
+    ys = []
+    for s, t in z["vote_perms"]:
+        ys.append(O.flat_buckets(acc, win, int(s), int(t)))
+    np.testing.assert_array_equal(np.vstack(ys), z["vote_y"])
+    thr = [O.noise_floor(y) for y in ys]
+    np.testing.assert_array_equal(thr, z["vote_thr"])
+    rounds = [(y, th, int(s), 0) for y, th, (s, t) in zip(ys, thr, z["vote_perms"])]
+    counts = O.vote_counts(rounds, 2 * k, n)
+    np.testing.assert_array_equal(counts, z["vote_counts"])
+    cands = O.pick_votes(counts, R, 2 * k, 0.5)
+    np.testing.assert_array_equal(cands, z["vote_cands"])
+    est = np.vstack([O.energy_est(y, win, int(s), int(t), np.array(cands))
+                     for y, (s, t) in zip(ys, z["vote_perms"])])
+    np.testing.assert_array_equal(est, z["vote_est"])
+    tm = O.robust_mean(est)
+    np.testing.assert_array_equal(tm, z["vote_tm"])
+    model = [(int(f), complex(c)) for f, c in zip(cands, np.where(np.isfinite(tm), tm, 0))]
+    (s0, t0), (s1, t1) = z["vote_perms"][0], z["vote_perms"][1]
+    np.testing.assert_array_equal(O.model_subtract(ys[0], win, int(s0), int(t0), 0, model),
+                                  z["vote_sub0"])
+    np.testing.assert_array_equal(O.model_subtract(ys[1], win, int(s1), int(t1), 3, model),
+                                  z["vote_sub1_t3"])
+    np.testing.assert_array_equal(O.robust_mean(z["tm_in"]), z["tm_out"])
+
+
+CASES = runner_cases()
+FAST = [c for c in CASES if not c[0]["name"].startswith(("C2", "C3", "C4"))]
+SLOW = [c for c in CASES if c[0]["name"].startswith(("C2", "C3", "C4"))]
+
+
+def _check_runner(rec, arr):
+    x = regen_signal(rec, arr)
+    np.testing.assert_allclose(sig_checksum(x), arr["checksum"], rtol=1e-12, atol=1e-9)
+    fwk, cfg = oracle_cfg(rec)
+    run = {"voting": O.voting, "iterative": O.iterative, "peeling": O.peeling}[fwk]
+    if rec["error"]:
+        with pytest.raises(O.OracleError) as ei:
+            run(O.Access(x), rec["k"], cfg)
+        assert ei.value.kind == rec["error"]
+        return
+    out = run(O.Access(x), rec["k"], cfg)
+    assert list(out.entries.keys()) == arr["pos"].tolist()
+    np.testing.assert_array_equal(np.array(list(out.entries.values()), dtype=complex),
+                                  arr["coef"])
+    assert out.samples_read == rec["samples_read"]
+    assert out.iterations == rec["iterations"]
+    assert out.converged == rec["converged"]
+
+
+@pytest.mark.parametrize("case", FAST, ids=[c[0]["name"] for c in FAST])
+def test_runner_golden(case):
+    _check_runner(*case)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", SLOW, ids=[c[0]["name"] for c in SLOW])
+def test_runner_golden_full_size(case):
+    _check_runner(*case)
