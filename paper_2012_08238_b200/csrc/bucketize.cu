@@ -1,0 +1,376 @@
+// Bucketization (the encode stage), sm_100a.
+//
+// Flat window (sfft/bucketize.py:142-161):
+//   y[j] = FFT_B( fold_B( g[i] * x[sigma*(i - tau_tot) mod N] * w_N^{b'sigma*i} ) )[j] / B
+// Spike train (sfft/bucketize.py:164-178):
+//   y[j] = FFT_B( x[(N/B)*i - tau mod N] )[j] / B
+// Response table (sfft/filters.py:146-149, transposed to [L][B]):
+//   T[rho][j] = G[rho + j*L] = FFT_B( fold_B( g[i] * w_N^{rho*i} ) )[j] / B
+//
+// One CTA owns one bucketization (item) when B <= kFusedMaxB: every thread
+// owns whole slots s and sums the ceil(Omega/B) rows of its slot in row
+// order (the reference's fold order, no atomics), the slots land in shared
+// memory, and the CTA runs the B-point FFT in place.  Larger B (config 5,
+// FFAST stages) use a four-step split B = B1*B2 whose column pass produces
+// the slots directly (no z round trip) and whose row pass writes y.
+#include "kernels.cuh"
+
+namespace sfft {
+
+struct ItemCtx {
+  const void* xs;
+  int64_t a, b, c;
+  int64_t step;    // flat: sigma*B mod n
+  int64_t estep;   // flat: bsig*B mod n
+  bool skip;
+};
+
+template <int MODE>
+__device__ __forceinline__ ItemCtx item_ctx(const Prod& p, int item, int elem_bytes) {
+  ItemCtx c;
+  const int sig = p.item_sig ? p.item_sig[item] : item;
+  c.skip = p.active && !p.active[sig];
+  c.xs = p.x ? (const char*)p.x + (int64_t)sig * p.xstride * elem_bytes : nullptr;
+  c.a = p.item_a ? p.item_a[item] : 0;
+  c.b = p.item_b ? p.item_b[item] : 0;
+  c.c = p.item_c ? p.item_c[item] : 0;
+  c.step = 0;
+  c.estep = 0;
+  if (MODE == PROD_FLAT) {
+    c.step = mulmod(c.a, p.B % p.n, p.n);
+    c.estep = mulmod(c.c, p.B % p.n, p.n);
+  }
+  return c;
+}
+
+template <typename Tin, int MODE>
+__device__ __forceinline__ double2 produce(const Prod& p, const ItemCtx& c, int item,
+                                           int64_t s) {
+  const int64_t n = p.n;
+  if (MODE == PROD_FLAT) {
+    const Tin* xs = (const Tin*)c.xs;
+    int64_t idx = mulmod(c.a, pmod(s - c.b, n), n);
+    double2 acc = cmk(0.0, 0.0);
+    if (c.c == 0) {
+      // rows in order, 4 gathers in flight per step
+      int64_t i = s;
+      for (; i + 3 * p.B < p.omega; i += 4 * p.B) {
+        int64_t i1 = idx + c.step; i1 -= (i1 >= n) ? n : 0;
+        int64_t i2 = i1 + c.step;  i2 -= (i2 >= n) ? n : 0;
+        int64_t i3 = i2 + c.step;  i3 -= (i3 >= n) ? n : 0;
+        const double2 v0 = Sample<Tin>::load(xs, idx);
+        const double2 v1 = Sample<Tin>::load(xs, i1);
+        const double2 v2 = Sample<Tin>::load(xs, i2);
+        const double2 v3 = Sample<Tin>::load(xs, i3);
+        const double g0 = __ldg(p.taps + i), g1 = __ldg(p.taps + i + p.B);
+        const double g2 = __ldg(p.taps + i + 2 * p.B), g3 = __ldg(p.taps + i + 3 * p.B);
+        acc = cadd_rn(acc, cmk(__dmul_rn(g0, v0.x), __dmul_rn(g0, v0.y)));
+        acc = cadd_rn(acc, cmk(__dmul_rn(g1, v1.x), __dmul_rn(g1, v1.y)));
+        acc = cadd_rn(acc, cmk(__dmul_rn(g2, v2.x), __dmul_rn(g2, v2.y)));
+        acc = cadd_rn(acc, cmk(__dmul_rn(g3, v3.x), __dmul_rn(g3, v3.y)));
+        idx = i3 + c.step;
+        idx -= (idx >= n) ? n : 0;
+      }
+      for (; i < p.omega; i += p.B) {
+        const double2 v = Sample<Tin>::load(xs, idx);
+        const double g = __ldg(p.taps + i);
+        acc = cadd_rn(acc, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
+        idx += c.step;
+        idx -= (idx >= n) ? n : 0;
+      }
+    } else {
+      int64_t e = mulmod(c.c, s % n, n);
+      for (int64_t i = s; i < p.omega; i += p.B) {
+        const double2 v = Sample<Tin>::load(xs, idx);
+        const double g = __ldg(p.taps + i);
+        const double2 z = cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y));
+        acc = cadd_rn(acc, cmul_rn(z, unit_root(n, e)));
+        idx += c.step;
+        idx -= (idx >= n) ? n : 0;
+        e += c.estep;
+        e -= (e >= n) ? n : 0;
+      }
+    }
+    return acc;
+  } else if (MODE == PROD_SPIKE) {
+    const Tin* xs = (const Tin*)c.xs;
+    const int64_t L = n / p.B;
+    return Sample<Tin>::load(xs, pmod(L * s - c.a, n));
+  } else if (MODE == PROD_GTAB) {
+    double2 acc = cmk(0.0, 0.0);
+    int64_t e = mulmod(c.a, s % n, n);
+    const int64_t estep = mulmod(c.a, p.B % n, n);
+    for (int64_t i = s; i < p.omega; i += p.B) {
+      const double g = __ldg(p.taps + i);
+      const double2 w = unit_root(n, e);
+      acc.x += g * w.x;
+      acc.y += g * w.y;
+      e += estep;
+      e -= (e >= n) ? n : 0;
+    }
+    return acc;
+  } else {
+    return p.z[(int64_t)item * p.B + s];
+  }
+}
+
+constexpr int kNT = 512;
+
+template <typename Tin, int MODE>
+__global__ void __launch_bounds__(kNT) k_fused(Prod p, FftPlan P, const double2* __restrict__ W,
+                                               double2* __restrict__ out) {
+  extern __shared__ double2 sm[];
+  const int item = blockIdx.x;
+  const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
+  if (c.skip) return;
+  const int B = (int)p.B;
+  for (int s = threadIdx.x; s < B; s += kNT) sm[s] = produce<Tin, MODE>(p, c, item, s);
+  __syncthreads();
+  fft_dif(sm, 1, B, P, W, B, threadIdx.x, kNT);
+  double2* o = out + (int64_t)item * B;
+  const double bd = (double)B;
+  for (int k = threadIdx.x; k < B; k += kNT) o[k] = cdivr(sm[fft_pos(k, P)], bd);
+}
+
+// Four-step column pass: DFT_B1 over n1 of z[n1*B2 + n2] for CG columns, times
+// w_B^{n2*k1}, stored at ws[k1*B2 + n2].
+template <typename Tin, int MODE>
+__global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2, int CG,
+                                              const double2* __restrict__ W,
+                                              double2* __restrict__ ws) {
+  extern __shared__ double2 sm[];
+  const int item = blockIdx.y;
+  const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
+  if (c.skip) return;
+  const int c0 = blockIdx.x * CG;
+  const int seg = B1 + 1;
+  const int B = (int)p.B;
+  for (int t = threadIdx.x; t < CG * B1; t += kNT) {
+    const int g = t % CG, n1 = t / CG;
+    const int n2 = c0 + g;
+    sm[g * seg + n1] = (n2 < B2) ? produce<Tin, MODE>(p, c, item, (int64_t)n1 * B2 + n2)
+                                 : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_dif(sm, CG, seg, P1, W, B, threadIdx.x, kNT);
+  double2* o = ws + (int64_t)item * B;
+  for (int t = threadIdx.x; t < CG * B1; t += kNT) {
+    const int g = t % CG, k1 = t / CG;
+    const int n2 = c0 + g;
+    if (n2 >= B2) continue;
+    const double2 v = sm[g * seg + fft_pos(k1, P1)];
+    const int64_t e = ((int64_t)n2 * k1) % B;
+    o[(int64_t)k1 * B2 + n2] = e ? cmul(v, __ldg(W + e)) : v;
+  }
+}
+
+// Four-step row pass: DFT_B2 over n2 of ws[k1*B2 + n2]; y[k1 + B1*k2] = . / B.
+__global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, FftPlan P2, int B1,
+                                              int B2, int RG, const double2* __restrict__ W,
+                                              const int32_t* item_sig, const int32_t* active,
+                                              double2* __restrict__ out) {
+  extern __shared__ double2 sm[];
+  const int item = blockIdx.y;
+  if (active) {
+    const int sig = item_sig ? item_sig[item] : item;
+    if (!active[sig]) return;
+  }
+  const int r0 = blockIdx.x * RG;
+  const int seg = B2 + 1;
+  const int B = B1 * B2;
+  const double2* in = ws + (int64_t)item * B;
+  for (int t = threadIdx.x; t < RG * B2; t += kNT) {
+    const int g = t / B2, n2 = t - g * B2;
+    const int k1 = r0 + g;
+    sm[g * seg + n2] = (k1 < B1) ? in[(int64_t)k1 * B2 + n2] : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_dif(sm, RG, seg, P2, W, B, threadIdx.x, kNT);
+  double2* o = out + (int64_t)item * B;
+  const double bd = (double)B;
+  for (int t = threadIdx.x; t < RG * B2; t += kNT) {
+    const int g = t % RG, k2 = t / RG;
+    const int k1 = r0 + g;
+    if (k1 >= B1) continue;
+    o[k1 + (int64_t)B1 * k2] = cdivr(sm[g * seg + fft_pos(k2, P2)], bd);
+  }
+}
+
+// Fallback for B with a prime factor above 13: slots to HBM, O(B^2) DFT.
+template <typename Tin, int MODE>
+__global__ void __launch_bounds__(256) k_slots(Prod p, double2* __restrict__ z) {
+  const int item = blockIdx.y;
+  const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
+  if (c.skip) return;
+  const int64_t s = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (s < p.B) z[(int64_t)item * p.B + s] = produce<Tin, MODE>(p, c, item, s);
+}
+
+__global__ void __launch_bounds__(256) k_dft_direct(const double2* __restrict__ z, int64_t B,
+                                                    const double2* __restrict__ W,
+                                                    const int32_t* item_sig,
+                                                    const int32_t* active,
+                                                    double2* __restrict__ out) {
+  const int item = blockIdx.y;
+  if (active) {
+    const int sig = item_sig ? item_sig[item] : item;
+    if (!active[sig]) return;
+  }
+  const int64_t k = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (k >= B) return;
+  const double2* zi = z + (int64_t)item * B;
+  double2 acc = cmk(0.0, 0.0);
+  int64_t e = 0;
+  for (int64_t s = 0; s < B; ++s) {
+    const double2 w = __ldg(W + e);
+    const double2 v = zi[s];
+    acc.x += v.x * w.x - v.y * w.y;
+    acc.y += v.x * w.y + v.y * w.x;
+    e += k;
+    if (e >= B) e -= B;
+  }
+  out[(int64_t)item * B + k] = cdivr(acc, (double)B);
+}
+
+__global__ void k_twiddle(double2* W, int64_t B) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= B) return;
+  double s, c;
+  sincospi(-2.0 * (double)e / (double)B, &s, &c);
+  W[e] = cmk(c, s);
+}
+
+// Flat-window taps (sfft/filters.py:125-151): sinc(u/B)/B-normalised times a
+// Gaussian, u = i - Omega/2, centre tap 1/B.
+__global__ void k_flat_taps(double* taps, int64_t omega, int64_t B, double gsig) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= omega) return;
+  const double u = (double)i - (double)omega / 2.0;
+  const double core = (u == 0.0) ? 1.0 / (double)B
+                                 : sin(3.141592653589793 * u / (double)B) /
+                                       (3.141592653589793 * u);
+  const double r = u / gsig;
+  taps[i] = core * exp(-0.5 * (r * r));
+}
+
+// max |T| over the response table (sfft/frameworks.py:331, :463).
+__global__ void k_absmax(const double2* __restrict__ v, int64_t count,
+                         unsigned long long* out_bits) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, cabs_(v[i]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, dbits(m));
+}
+
+// ----------------------------------------------------------------- host side
+
+template <typename K>
+static int ensure_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    SFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)bytes));
+  }
+  return 0;
+}
+
+// Choose B = B1*B2 for the four-step path: both plan-able and <= kFusedMaxB,
+// B2 the smallest such divisor >= sqrt(B).
+static bool split_plan(int64_t B, int64_t* B1, int64_t* B2) {
+  int64_t best = 0;
+  for (int64_t d = 1; d * d <= B; ++d) {
+    if (B % d) continue;
+    const int64_t a = d, b = B / d;
+    FftPlan pa, pb;
+    if (a <= kFusedMaxB && b <= kFusedMaxB && make_plan(a, &pa) && make_plan(b, &pb)) best = a;
+  }
+  if (!best) return false;
+  *B1 = best;
+  *B2 = B / best;
+  return true;
+}
+
+size_t bucketize_ws_bytes(int64_t B, int64_t nitems) {
+  FftPlan P;
+  if (B <= kFusedMaxB && make_plan(B, &P)) return 0;
+  return (size_t)nitems * (size_t)B * sizeof(double2);
+}
+
+template <typename Tin, int MODE>
+static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, double2* out,
+                           void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (nitems <= 0) return 0;
+  const int64_t B = p.B;
+  FftPlan P;
+  if (B <= kFusedMaxB && make_plan(B, &P)) {
+    const size_t sm = (size_t)B * sizeof(double2);
+    if (ensure_smem(k_fused<Tin, MODE>, sm)) return -3;
+    k_fused<Tin, MODE><<<(unsigned)nitems, kNT, sm, st>>>(p, P, W, out);
+    SFFT_CHECK_LAUNCH("k_fused");
+    return 0;
+  }
+  SFFT_REQUIRE(ws && ws_bytes >= bucketize_ws_bytes(B, nitems),
+               "bucketize: workspace too small for the four-step path");
+  double2* z = (double2*)ws;
+  int64_t B1, B2;
+  if (split_plan(B, &B1, &B2)) {
+    FftPlan P1, P2;
+    make_plan(B1, &P1);
+    make_plan(B2, &P2);
+    const int CG = (int)std::max<int64_t>(1, std::min<int64_t>(B2, kFusedMaxB / (B1 + 1)));
+    const int RG = (int)std::max<int64_t>(1, std::min<int64_t>(B1, kFusedMaxB / (B2 + 1)));
+    const size_t smc = (size_t)CG * (B1 + 1) * sizeof(double2);
+    const size_t smr = (size_t)RG * (B2 + 1) * sizeof(double2);
+    if (ensure_smem(k_cols<Tin, MODE>, smc)) return -3;
+    if (ensure_smem(k_rows, smr)) return -3;
+    dim3 gc((unsigned)cdiv_up(B2, CG), (unsigned)nitems);
+    k_cols<Tin, MODE><<<gc, kNT, smc, st>>>(p, P1, (int)B1, (int)B2, CG, W, z);
+    SFFT_CHECK_LAUNCH("k_cols");
+    dim3 gr((unsigned)cdiv_up(B1, RG), (unsigned)nitems);
+    k_rows<<<gr, kNT, smr, st>>>(z, P2, (int)B1, (int)B2, RG, W, p.item_sig, p.active, out);
+    SFFT_CHECK_LAUNCH("k_rows");
+    return 0;
+  }
+  dim3 g((unsigned)cdiv_up(B, 256), (unsigned)nitems);
+  k_slots<Tin, MODE><<<g, 256, 0, st>>>(p, z);
+  SFFT_CHECK_LAUNCH("k_slots");
+  k_dft_direct<<<g, 256, 0, st>>>(z, B, W, p.item_sig, p.active, out);
+  SFFT_CHECK_LAUNCH("k_dft_direct");
+  return 0;
+}
+
+int run_bucketize(int dtype, int mode, const Prod& p, int64_t nitems, const double2* W,
+                  double2* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (mode == PROD_FLAT)
+    return dtype == 0 ? run_bucketize_t<float2, PROD_FLAT>(p, nitems, W, out, ws, ws_bytes, st)
+                      : run_bucketize_t<double2, PROD_FLAT>(p, nitems, W, out, ws, ws_bytes, st);
+  if (mode == PROD_SPIKE)
+    return dtype == 0 ? run_bucketize_t<float2, PROD_SPIKE>(p, nitems, W, out, ws, ws_bytes, st)
+                      : run_bucketize_t<double2, PROD_SPIKE>(p, nitems, W, out, ws, ws_bytes, st);
+  if (mode == PROD_GTAB)
+    return run_bucketize_t<double2, PROD_GTAB>(p, nitems, W, out, ws, ws_bytes, st);
+  return run_bucketize_t<double2, PROD_LOAD>(p, nitems, W, out, ws, ws_bytes, st);
+}
+
+int run_twiddle(double2* W, int64_t B, cudaStream_t st) {
+  k_twiddle<<<(unsigned)cdiv_up(B, 256), 256, 0, st>>>(W, B);
+  SFFT_CHECK_LAUNCH("k_twiddle");
+  return 0;
+}
+
+int run_flat_taps(double* taps, int64_t omega, int64_t B, double gsig, cudaStream_t st) {
+  k_flat_taps<<<(unsigned)cdiv_up(omega, 256), 256, 0, st>>>(taps, omega, B, gsig);
+  SFFT_CHECK_LAUNCH("k_flat_taps");
+  return 0;
+}
+
+int run_absmax(const double2* v, int64_t count, double* out, cudaStream_t st) {
+  SFFT_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  const int blocks = (int)std::min<int64_t>(1184, cdiv_up(count, 256));
+  k_absmax<<<blocks, 256, 0, st>>>(v, count, (unsigned long long*)out);
+  SFFT_CHECK_LAUNCH("k_absmax");
+  return 0;
+}
+
+}  // namespace sfft

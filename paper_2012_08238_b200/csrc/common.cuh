@@ -1,0 +1,145 @@
+// Shared device/host helpers for the sm_100a sparse-FFT hot path.
+//
+// Complex values are double2 (re, im).  Every decision-relevant quantity is
+// fp64, in both the complex64 (input rounded to float2, fp64 accumulation) and
+// the complex128 mode (SURVEY.md §7 hard part 1).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#ifndef SFFT_HD
+#define SFFT_HD __host__ __device__ __forceinline__
+#endif
+
+namespace sfft {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+const char* last_error();
+
+#define SFFT_CHECK_LAUNCH(what)                                                  \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      ::sfft::set_error(std::string(what) + ": " + cudaGetErrorString(_e));     \
+      return -3;                                                                 \
+    }                                                                            \
+  } while (0)
+
+#define SFFT_CUDA(call)                                                          \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::sfft::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));    \
+      return -3;                                                                 \
+    }                                                                            \
+  } while (0)
+
+#define SFFT_REQUIRE(cond, msg)                                                  \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      ::sfft::set_error(msg);                                                    \
+      return -2;                                                                 \
+    }                                                                            \
+  } while (0)
+
+// ----------------------------------------------------------------- complex
+SFFT_HD double2 cmk(double r, double i) { return make_double2(r, i); }
+SFFT_HD double2 cadd(double2 a, double2 b) { return cmk(a.x + b.x, a.y + b.y); }
+SFFT_HD double2 csub(double2 a, double2 b) { return cmk(a.x - b.x, a.y - b.y); }
+SFFT_HD double2 cmul(double2 a, double2 b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+SFFT_HD double2 cconj(double2 a) { return cmk(a.x, -a.y); }
+SFFT_HD double2 cscale(double2 a, double s) { return cmk(a.x * s, a.y * s); }
+SFFT_HD double2 cdivr(double2 a, double s) { return cmk(a.x / s, a.y / s); }
+
+#ifdef __CUDACC__
+// Products/sums without FMA contraction, where the reference's rounding
+// sequence is cheap to reproduce exactly (elementwise numpy products).
+__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {
+  return cmk(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+             __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 csub_rn(double2 a, double2 b) {
+  return cmk(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 cadd_rn(double2 a, double2 b) {
+  return cmk(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+#endif
+
+// |z| as numpy's np.abs(complex128) (hypot).
+SFFT_HD double cabs_(double2 a) { return hypot(a.x, a.y); }
+
+// Complex division with Smith's scaling (numpy's complex128 divide).
+SFFT_HD double2 cdiv(double2 a, double2 b) {
+  const double br = b.x, bi = b.y;
+  const double abs_br = fabs(br), abs_bi = fabs(bi);
+  if (abs_br >= abs_bi) {
+    if (abs_br == 0.0 && abs_bi == 0.0) {
+      return cmk(a.x / abs_br, a.y / abs_br);
+    }
+    const double rat = bi / br;
+    const double scl = 1.0 / (br + bi * rat);
+    return cmk((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
+  }
+  const double rat = br / bi;
+  const double scl = 1.0 / (bi + br * rat);
+  return cmk((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+}
+
+// ----------------------------------------------------------------- modular
+SFFT_HD int64_t pmod(int64_t a, int64_t n) {
+  int64_t r = a % n;
+  return r < 0 ? r + n : r;
+}
+// (a*b) mod n for 0 <= a,b < n < 2^31 (products stay below 2^62).
+SFFT_HD int64_t mulmod(int64_t a, int64_t b, int64_t n) { return pmod(a * b, n); }
+
+// w_n^e = exp(-2*pi*i*(e mod n)/n), with the angle formed as the reference
+// forms it ((-2*pi*e)/n, sfft/signal.py:50-57).
+SFFT_HD double2 unit_root(int64_t n, int64_t e) {
+  const double th = (-6.283185307179586 * (double)pmod(e, n)) / (double)n;
+  double s, c;
+  sincos(th, &s, &c);
+  return cmk(c, s);
+}
+
+// ----------------------------------------------------------------- loads
+template <typename T>
+struct Sample;
+template <>
+struct Sample<float2> {
+  static __device__ __forceinline__ double2 load(const float2* p, int64_t i) {
+    float2 v = __ldg(p + i);
+    return cmk((double)v.x, (double)v.y);
+  }
+};
+template <>
+struct Sample<double2> {
+  static __device__ __forceinline__ double2 load(const double2* p, int64_t i) {
+    return __ldg(p + i);
+  }
+};
+
+// ----------------------------------------------------------------- misc
+SFFT_HD int64_t cdiv_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Non-negative doubles order like their bit patterns.
+SFFT_HD unsigned long long dbits(double v) {
+#ifdef __CUDA_ARCH__
+  return (unsigned long long)__double_as_longlong(v);
+#else
+  unsigned long long u;
+  memcpy(&u, &v, 8);
+  return u;
+#endif
+}
+
+}  // namespace sfft

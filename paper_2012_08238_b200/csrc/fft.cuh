@@ -1,0 +1,132 @@
+// Shared-memory mixed-radix FFT for one CTA (forward, w = exp(-2*pi*i/M)).
+//
+// In-place decimation-in-frequency over G independent segments of length M,
+// radices 2/3/4/5/7/11/13 (B = 2^8..2^17 for the flat
+// configs, 3^5*5^3 / 2^7*3^5 / 2^7*5^3 for the FFAST stages).  Output k of a
+// segment lands at smem position fft_pos(k) (mixed-radix digit reversal); the
+// caller gathers it back to natural order while writing to HBM, so no second
+// buffer is needed and B = 8192 complex128 fits in 128 KB of shared memory.
+//
+// Twiddles come from one table W[e] = w_Wn^e (complex128, L1/L2 resident);
+// a transform of length M | Wn reads W[e * (Wn / M)].
+#pragma once
+
+#include "common.cuh"
+
+namespace sfft {
+
+constexpr int kMaxStages = 28;
+constexpr int kFusedMaxB = 8192;   // one-CTA fold+FFT up to this many buckets
+
+struct FftPlan {
+  int n;
+  int nst;
+  int rad[kMaxStages];
+};
+
+// Host: factor n into supported radices (4s first).  false if a prime factor
+// above 13 remains (the caller then uses the direct-DFT path).
+inline bool make_plan(int64_t n, FftPlan* p) {
+  p->n = (int)n;
+  p->nst = 0;
+  int64_t m = n;
+  auto push = [&](int r) { p->rad[p->nst++] = r; m /= r; };
+  while (m % 4 == 0 && p->nst < kMaxStages) push(4);
+  while (m % 2 == 0 && p->nst < kMaxStages) push(2);
+  const int primes[] = {3, 5, 7, 11, 13};
+  for (int r : primes)
+    while (m % r == 0 && p->nst < kMaxStages) push(r);
+  return m == 1;
+}
+
+__device__ __forceinline__ int fft_pos(int k, const FftPlan& P) {
+  int pos = 0, span = P.n;
+#pragma unroll 1
+  for (int st = 0; st < P.nst; ++st) {
+    const int r = P.rad[st];
+    span /= r;
+    pos += (k % r) * span;
+    k /= r;
+  }
+  return pos;
+}
+
+template <int R>
+__device__ __forceinline__ void bfly(double2* __restrict__ s, int base, int Mp, int j,
+                                     const double2* __restrict__ W, int ws, int wsr) {
+  double2 a[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) a[p] = s[base + p * Mp];
+  if constexpr (R == 2) {
+    s[base] = cadd(a[0], a[1]);
+    const double2 d = csub(a[0], a[1]);
+    s[base + Mp] = j ? cmul(d, __ldg(W + j * ws)) : d;
+  } else if constexpr (R == 4) {
+    const double2 t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
+    const double2 t2 = cadd(a[1], a[3]), t3 = csub(a[1], a[3]);
+    s[base] = cadd(t0, t2);
+    const double2 b1 = cmk(t1.x + t3.y, t1.y - t3.x);
+    const double2 b2 = csub(t0, t2);
+    const double2 b3 = cmk(t1.x - t3.y, t1.y + t3.x);
+    if (j) {
+      s[base + Mp] = cmul(b1, __ldg(W + j * ws));
+      s[base + 2 * Mp] = cmul(b2, __ldg(W + 2 * j * ws));
+      s[base + 3 * Mp] = cmul(b3, __ldg(W + 3 * j * ws));
+    } else {
+      s[base + Mp] = b1;
+      s[base + 2 * Mp] = b2;
+      s[base + 3 * Mp] = b3;
+    }
+  } else {
+    // generic odd radix: all inputs are in registers, so each output can be
+    // formed and stored in turn (no second register array)
+#pragma unroll 1
+    for (int q = 0; q < R; ++q) {
+      double2 acc = a[0];
+#pragma unroll
+      for (int p = 1; p < R; ++p) {
+        const double2 w = __ldg(W + ((p * q) % R) * wsr);
+        acc.x = fma(a[p].x, w.x, fma(-a[p].y, w.y, acc.x));
+        acc.y = fma(a[p].x, w.y, fma(a[p].y, w.x, acc.y));
+      }
+      s[base + q * Mp] = (j && q) ? cmul(acc, __ldg(W + j * q * ws)) : acc;
+    }
+  }
+}
+
+// G segments of length P.n at s + g*seg.  Block-wide; ends with __syncthreads.
+__device__ __forceinline__ void fft_dif(double2* s, int G, int seg, const FftPlan& P,
+                                        const double2* __restrict__ W, int Wn, int tid,
+                                        int nt) {
+  const int M = P.n;
+  int Mb = M;
+#pragma unroll 1
+  for (int st = 0; st < P.nst; ++st) {
+    const int r = P.rad[st];
+    const int Mp = Mb / r;
+    const int nb = M / r;
+    const int ws = Wn / Mb;
+    const int wsr = Wn / r;
+#pragma unroll 1
+    for (int t = tid; t < G * nb; t += nt) {
+      const int g = t / nb;
+      const int tt = t - g * nb;
+      const int blk = tt / Mp;
+      const int j = tt - blk * Mp;
+      const int base = g * seg + blk * Mb + j;
+      switch (r) {
+        case 4: bfly<4>(s, base, Mp, j, W, ws, wsr); break;
+        case 2: bfly<2>(s, base, Mp, j, W, ws, wsr); break;
+        case 3: bfly<3>(s, base, Mp, j, W, ws, wsr); break;
+        case 5: bfly<5>(s, base, Mp, j, W, ws, wsr); break;
+        case 7: bfly<7>(s, base, Mp, j, W, ws, wsr); break;
+        case 11: bfly<11>(s, base, Mp, j, W, ws, wsr); break;
+        default: bfly<13>(s, base, Mp, j, W, ws, wsr); break;
+      }
+    }
+    __syncthreads();
+    Mb = Mp;
+  }
+}
+
+}  // namespace sfft
