@@ -79,6 +79,82 @@ int sfft_access_mark(uint8_t* map, int64_t n, int kind, int64_t a, int64_t b, in
 /* *out (device int64) = number of non-zero bytes of map[0..n). */
 int sfft_count_nonzero(const uint8_t* map, int64_t n, int64_t* out, void* stream);
 
+/* ---- decode stages ------------------------------------------------------- */
+
+/* A8 robust_noise_floor (sfft/reconstruct.py:119-133), one value per set:
+ * floor = max(min(mult*median|v|, peak/4), 1e-9*peak, 1e-300); peak = max|v|
+ * (peak_out may be NULL).  values: complex128 [nsets][B]. */
+int sfft_noise_floor(const void* values, int64_t nsets, int64_t B, double median_mult,
+                     double* floor_out, double* peak_out, void* stream);
+
+/* A9 heavy buckets of vote_tally (sfft/reconstruct.py:171-177): bit b of
+ * bits[set][B/32] is set iff bucket b is among the first heavy_count buckets
+ * with |v| >= max(thr[set], 0) in (-|v|, index) order.  nheavy may be NULL. */
+int sfft_heavy_bitmap(const void* values, int64_t nsets, int64_t B, const double* thr,
+                      int64_t heavy_count, uint32_t* bits, int32_t* nheavy, void* stream);
+
+/* Workspace bytes for sfft_vote_select. */
+size_t sfft_votes_ws_bytes(int64_t n, int64_t nsig, int64_t rounds);
+
+/* A10 vote_tally + A11 select_by_votes (sfft/reconstruct.py:158-194), for
+ * nsig independent signals of `rounds` rounds each (rounds <= 64).
+ * Position f of signal s scores one per round r whose heavy bitmap
+ * bits[s][r] holds f's flat bucket (((sigma*(f-b') mod n) - cs + L/2) mod n)/L.
+ * counts_out [nsig][n] (optional) receives the scores (or counts_in supplies
+ * them).  If cand != NULL, cand[s][0..keep) receives the positions with
+ * score >= need ordered by (-score, position) and ncand[s] their number. */
+int sfft_vote_select(int64_t n, int64_t B, int64_t rounds, int64_t nsig, const uint32_t* bits,
+                     const int64_t* sigma, const int64_t* bprime, int64_t center_shift,
+                     const int64_t* counts_in, int64_t* counts_out, int64_t need, int64_t keep,
+                     int64_t* cand, int32_t* ncand, void* ws, size_t ws_bytes, void* stream);
+
+/* A12 _energy_estimates (sfft/frameworks.py:321-332) for `rounds` bucket sets
+ * y[r][B]: est[r][c] = y[r][b]/(G[bL-m]*w^{tau[r] m}), m = sigma[r]*cand[c],
+ * (NaN, 0) where |G| < 0.05*(*gmax). */
+int sfft_energy_estimates(const void* y, int64_t B, const void* gtable, const double* gmax,
+                          int64_t n, int64_t rounds, const int64_t* sigma, const int64_t* tau,
+                          const int64_t* cand, int64_t ncand, void* est, void* stream);
+
+/* A13 _trimmed_mean (sfft/frameworks.py:335-351) over the rows of est
+ * [rounds][ncand] (rounds <= 64). */
+int sfft_trimmed_mean(const void* est, int64_t rounds, int64_t ncand, void* out, void* stream);
+
+/* A14 _subtract_flat (sfft/frameworks.py:423-436):
+ * out[i][j] = y[i][b] - sum_t coef_t * G[(b*L - sigma[i]*pos_t) mod n] *
+ *             w^{(tau_tot[i]*sigma[i]*pos_t) mod n},
+ * b = j (nb == B, blist NULL) or blist[i*nb + j]; the tones of item i are
+ * tone_pos/tone_coef[item_sig[i]*tone_stride + t], t < tone_count[item_sig[i]],
+ * summed in order.  out may alias y when blist is NULL. */
+int sfft_subtract_flat(const void* y, void* out, int64_t B, int64_t nb, const int32_t* blist,
+                       int64_t nitems, const void* gtable, int64_t n, const int32_t* item_sig,
+                       const int64_t* sigma, const int64_t* tau_tot, const int64_t* tone_pos,
+                       const void* tone_coef, const int32_t* tone_count, int64_t tone_stride,
+                       void* stream);
+
+/* ---- runners (device-resident frameworks) ---------------------------------- */
+
+/* Workspace bytes of sfft_run_iterative (nshifts = 1 + ladder length,
+ * cap = recovered-tone capacity per signal, max_iterations * B suffices). */
+size_t sfft_iterative_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t nshifts, int64_t cap);
+
+/* A16 run_iterative with phase location + _polish_flat_estimates
+ * (sfft/frameworks.py:439-608) for nsig signals (rows of x) at once.
+ * perm_sigma/perm_tau [nsig][nperm] hold each signal's permutation stream
+ * (PermutationParams.random draws in order; nperm >= max_iterations + 6).
+ * ladder_host (HOST int64[nladder]) is _phase_ladder(n).  Outputs per signal:
+ * out_pos/out_coef [nsig][k] the top-k entries in (-|c|, f) order,
+ * out_count, out_iterations, out_converged, out_samples (samples_read).
+ * Synchronises the stream once per iteration (early exit when all
+ * signals have stopped). */
+int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                       const double* taps, int64_t omega, int64_t B, const void* gtable,
+                       const double* gmax, const void* W, const int64_t* perm_sigma,
+                       const int64_t* perm_tau, int64_t nperm, int64_t k, int64_t max_iterations,
+                       const int64_t* ladder_host, int64_t nladder, int64_t cap, int64_t* out_pos,
+                       void* out_coef, int32_t* out_count, int32_t* out_iterations,
+                       int32_t* out_converged, int64_t* out_samples, void* ws, size_t ws_bytes,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,3 +92,21 @@ SIGNATURES.update({
     "sfft_access_mark": (C.c_int, [vp, i64, C.c_int, i64, i64, i64, P_i64, vp]),
     "sfft_count_nonzero": (C.c_int, [vp, i64, P_i64, vp]),
 })
+SIGNATURES.update({
+    "sfft_noise_floor": (C.c_int, [vp, i64, i64, f64, P_f64, P_f64, vp]),
+    "sfft_heavy_bitmap": (C.c_int, [vp, i64, i64, P_f64, i64, vp, P_i32, vp]),
+    "sfft_votes_ws_bytes": (sz, [i64, i64, i64]),
+    "sfft_vote_select": (C.c_int, [i64, i64, i64, i64, vp, P_i64, P_i64, i64, P_i64, P_i64, i64,
+                                   i64, P_i64, P_i32, vp, sz, vp]),
+    "sfft_energy_estimates": (C.c_int, [vp, i64, vp, P_f64, i64, i64, P_i64, P_i64, P_i64, i64,
+                                        vp, vp]),
+    "sfft_trimmed_mean": (C.c_int, [vp, i64, i64, vp, vp]),
+    "sfft_subtract_flat": (C.c_int, [vp, vp, i64, i64, P_i32, i64, vp, i64, P_i32, P_i64, P_i64,
+                                     P_i64, vp, P_i32, i64, vp]),
+})
+SIGNATURES.update({
+    "sfft_iterative_ws_bytes": (sz, [i64, i64, i64, i64, i64]),
+    "sfft_run_iterative": (C.c_int, [C.c_int, vp, i64, i64, i64, P_f64, i64, i64, vp, P_f64, vp,
+                                     P_i64, P_i64, i64, i64, i64, vp, i64, i64, P_i64, vp, P_i32,
+                                     P_i32, P_i32, P_i64, vp, sz, vp]),
+})

@@ -120,3 +120,114 @@ SFFT_API int sfft_count_nonzero(const uint8_t* map, int64_t n, int64_t* out, voi
   SFFT_REQUIRE(map && out && n >= 0, "sfft_count_nonzero: bad argument");
   return run_count_nonzero(map, n, out, (cudaStream_t)stream);
 }
+
+// ---- decode stages --------------------------------------------------------
+
+SFFT_API int sfft_noise_floor(const void* values, int64_t nsets, int64_t B, double median_mult,
+                              double* floor_out, double* peak_out, void* stream) {
+  SFFT_REQUIRE(values && floor_out && B > 0 && nsets >= 0, "sfft_noise_floor: bad argument");
+  return run_floor((const double2*)values, nsets, B, median_mult, nullptr, nullptr, floor_out,
+                   peak_out, (cudaStream_t)stream);
+}
+
+SFFT_API int sfft_heavy_bitmap(const void* values, int64_t nsets, int64_t B, const double* thr,
+                               int64_t heavy_count, uint32_t* bits, int32_t* nheavy,
+                               void* stream) {
+  SFFT_REQUIRE(values && thr && bits && B > 0 && nsets >= 0 && heavy_count >= 0,
+               "sfft_heavy_bitmap: bad argument");
+  return run_heavy_bitmap((const double2*)values, nsets, B, thr, heavy_count, nullptr, nullptr,
+                          bits, nheavy, (cudaStream_t)stream);
+}
+
+SFFT_API size_t sfft_votes_ws_bytes(int64_t n, int64_t nsig, int64_t rounds) {
+  return votes_ws_bytes(n, (int)nsig, (int)rounds);
+}
+
+SFFT_API int sfft_vote_select(int64_t n, int64_t B, int64_t rounds, int64_t nsig,
+                              const uint32_t* bits, const int64_t* sigma, const int64_t* bprime,
+                              int64_t center_shift, const int64_t* counts_in, int64_t* counts_out,
+                              int64_t need, int64_t keep, int64_t* cand, int32_t* ncand,
+                              void* ws, size_t ws_bytes, void* stream) {
+  SFFT_REQUIRE(n > 0 && B > 0 && n % B == 0 && rounds >= 0 && rounds <= 64 && nsig >= 1,
+               "sfft_vote_select: bad sizes");
+  SFFT_REQUIRE(counts_in || (bits && sigma), "sfft_vote_select: need counts or bitmaps");
+  SFFT_REQUIRE(need >= 1, "sfft_vote_select: need >= 1");
+  SFFT_REQUIRE(!cand || (ncand && keep > 0), "sfft_vote_select: cand needs ncand and keep > 0");
+  SFFT_REQUIRE(ws && ws_bytes >= votes_ws_bytes(n, (int)nsig, (int)rounds),
+               "sfft_vote_select: workspace too small");
+  VoteRounds vr;
+  vr.bits = bits;
+  vr.sigma = sigma;
+  vr.bprime = bprime;
+  vr.n = n;
+  vr.B = B;
+  vr.L = n / B;
+  vr.words = (B + 31) / 32;
+  vr.cs = center_shift;
+  vr.R = (int)rounds;
+  return run_votes(vr, (int)nsig, counts_in, counts_out, (int)need, (int)keep, cand, ncand,
+                   (int*)ws, cand != nullptr, (cudaStream_t)stream);
+}
+
+SFFT_API int sfft_energy_estimates(const void* y, int64_t B, const void* gtable,
+                                   const double* gmax, int64_t n, int64_t rounds,
+                                   const int64_t* sigma, const int64_t* tau, const int64_t* cand,
+                                   int64_t ncand, void* est, void* stream) {
+  SFFT_REQUIRE(y && gtable && gmax && sigma && tau && est && n % B == 0,
+               "sfft_energy_estimates: bad argument");
+  SFFT_REQUIRE(ncand == 0 || cand, "sfft_energy_estimates: null candidates");
+  return run_energy_est((const double2*)y, B, (const double2*)gtable, gmax, n, (int)rounds,
+                        sigma, tau, cand, ncand, (double2*)est, (cudaStream_t)stream);
+}
+
+SFFT_API int sfft_trimmed_mean(const void* est, int64_t rounds, int64_t ncand, void* out,
+                               void* stream) {
+  SFFT_REQUIRE(est && out, "sfft_trimmed_mean: null pointer");
+  return run_trimmed_mean((const double2*)est, (int)rounds, ncand, (double2*)out,
+                          (cudaStream_t)stream);
+}
+
+SFFT_API int sfft_subtract_flat(const void* y, void* out, int64_t B, int64_t nb,
+                                const int32_t* blist, int64_t nitems, const void* gtable,
+                                int64_t n, const int32_t* item_sig, const int64_t* sigma,
+                                const int64_t* tau_tot, const int64_t* tone_pos,
+                                const void* tone_coef, const int32_t* tone_count,
+                                int64_t tone_stride, void* stream) {
+  SFFT_REQUIRE(y && out && gtable && sigma && tau_tot && tone_count && n % B == 0,
+               "sfft_subtract_flat: bad argument");
+  SFFT_REQUIRE(nb == B || blist, "sfft_subtract_flat: partial bucket lists need blist");
+  return run_subtract((const double2*)y, (double2*)out, B, nb, blist, nitems,
+                      (const double2*)gtable, n, item_sig, sigma, tau_tot, tone_pos,
+                      (const double2*)tone_coef, tone_count, tone_stride, (cudaStream_t)stream);
+}
+
+// ---- runners ---------------------------------------------------------------
+
+SFFT_API size_t sfft_iterative_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t nshifts,
+                                        int64_t cap) {
+  return iterative_ws_bytes(n, B, (int)nsig, (int)nshifts, (int)cap);
+}
+
+SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride,
+                                int64_t nsig, const double* taps, int64_t omega, int64_t B,
+                                const void* gtable, const double* gmax, const void* W,
+                                const int64_t* perm_sigma, const int64_t* perm_tau, int64_t nperm,
+                                int64_t k, int64_t max_iterations, const int64_t* ladder_host,
+                                int64_t nladder, int64_t cap, int64_t* out_pos, void* out_coef,
+                                int32_t* out_count, int32_t* out_iterations,
+                                int32_t* out_converged, int64_t* out_samples, void* ws,
+                                size_t ws_bytes, void* stream) {
+  SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_iterative: dtype must be 0 or 1");
+  SFFT_REQUIRE(x && taps && gtable && gmax && W && perm_sigma && perm_tau && ladder_host,
+               "sfft_run_iterative: null pointer");
+  SFFT_REQUIRE(n > 0 && B > 0 && n % B == 0 && nsig >= 1 && k >= 1 && max_iterations >= 1,
+               "sfft_run_iterative: bad sizes");
+  SFFT_REQUIRE(n < (int64_t(1) << 31), "sfft_run_iterative: n must be < 2^31");
+  SFFT_REQUIRE(out_pos && out_coef && out_count && out_iterations && out_converged && out_samples,
+               "sfft_run_iterative: null output");
+  return run_iterative(dtype, x, n, xstride, (int)nsig, taps, omega, B, (const double2*)gtable,
+                       gmax, (const double2*)W, perm_sigma, perm_tau, (int)nperm, k,
+                       (int)max_iterations, ladder_host, (int)nladder, (int)cap, out_pos,
+                       (double2*)out_coef, out_count, out_iterations, out_converged, out_samples,
+                       ws, ws_bytes, (cudaStream_t)stream);
+}

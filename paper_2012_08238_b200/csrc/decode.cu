@@ -1,0 +1,514 @@
+// Decode-stage kernels (sm_100a): robust noise floor, heavy-bucket selection,
+// hash-inverse voting + vote selection, bucket-energy estimates, the trimmed
+// mean over rounds and the bucket-domain forward-model subtraction.
+//
+// All arithmetic that feeds a discrete decision is fp64 and follows the
+// reference's formulas and tie rules:
+//   floor      max(min(3*median|v|, peak/4), 1e-9*peak, 1e-300)   sfft/reconstruct.py:119-133
+//   heavy      |v| >= max(thr,0), order (-|v|, idx), first h       sfft/reconstruct.py:171-177
+//   votes      +1 per round whose heavy set holds f's flat bucket  sfft/reconstruct.py:158-179
+//   select     count >= max(frac*R, 1e-12), order (-count, pos)    sfft/reconstruct.py:182-194
+//   estimates  y[b] / (G[bL-m] * w^{tau m}), NaN under 0.05*max|G| sfft/frameworks.py:321-332
+//   trimmed    median / lower-quartile / keep / nanmean            sfft/frameworks.py:335-351
+//   subtract   y[b] - sum_f c_f G[(bL - sigma f)] w^{tau_tot sigma f} sfft/frameworks.py:423-436
+#include "kernels.cuh"
+#include "block.cuh"
+
+namespace sfft {
+
+constexpr int kFloorNT = 256;
+
+// One CTA per bucket set: floor[i] and peak[i] of values[i][0..B).
+__global__ void __launch_bounds__(kFloorNT) k_floor(const double2* __restrict__ values, int64_t B,
+                                                    double mult, const int32_t* item_sig,
+                                                    const int32_t* active, double* floor_out,
+                                                    double* peak_out) {
+  __shared__ unsigned hist[256];
+  __shared__ long long sh[4];
+  __shared__ double redd[32];
+  __shared__ unsigned long long redu[32];
+  const int item = blockIdx.x;
+  if (active) {
+    const int sig = item_sig ? item_sig[item] : item;
+    if (!active[sig]) return;
+  }
+  double med, peak;
+  median_and_peak<kFloorNT>(values + (int64_t)item * B, B, &med, &peak, hist, sh, redd, redu);
+  if (threadIdx.x == 0) {
+    const double fl = fmax(fmax(fmin(mult * med, 0.25 * peak), 1e-9 * peak), 1e-300);
+    floor_out[item] = fl;
+    if (peak_out) peak_out[item] = peak;
+  }
+}
+
+int run_floor(const double2* values, int64_t nsets, int64_t B, double mult,
+              const int32_t* item_sig, const int32_t* active, double* floor_out, double* peak_out,
+              cudaStream_t st) {
+  if (nsets <= 0) return 0;
+  k_floor<<<(unsigned)nsets, kFloorNT, 0, st>>>(values, B, mult, item_sig, active, floor_out,
+                                                peak_out);
+  SFFT_CHECK_LAUNCH("k_floor");
+  return 0;
+}
+
+// ================================================================ heavy set (A9)
+
+// Heavy bitmap of one round: the first `hc` eligible buckets in (-|v|, idx)
+// order.  bits[B/32 words].  One CTA per item.
+__global__ void __launch_bounds__(kFloorNT) k_heavy_bitmap(const double2* __restrict__ values,
+                                                           int64_t B, const double* thr,
+                                                           int64_t hc, const int32_t* item_sig,
+                                                           const int32_t* active,
+                                                           uint32_t* __restrict__ bits,
+                                                           int32_t* nheavy) {
+  constexpr int NT = kFloorNT;
+  __shared__ unsigned hist[256];
+  __shared__ long long sh[4];
+  __shared__ int redi[32];
+  const int item = blockIdx.x;
+  if (active) {
+    const int sig = item_sig ? item_sig[item] : item;
+    if (!active[sig]) return;
+  }
+  const double2* v = values + (int64_t)item * B;
+  const int64_t words = (B + 31) / 32;
+  uint32_t* bw = bits + (int64_t)item * words;
+  const double t = fmax(thr[item], 0.0);
+  const unsigned long long lo = dbits(t);
+  MagKey key{v};
+  // eligible count
+  int e = 0;
+  for (int64_t i = threadIdx.x; i < B; i += NT) e += key(i) >= lo;
+  const int E = block_sum_int<NT>(e, redi);
+  for (int64_t w = threadIdx.x; w < words; w += NT) bw[w] = 0u;
+  __syncthreads();
+  if (E <= hc) {
+    for (int64_t i = threadIdx.x; i < B; i += NT)
+      if (key(i) >= lo) atomicOr(&bw[i >> 5], 1u << (i & 31));
+    if (threadIdx.x == 0 && nheavy) nheavy[item] = E;
+    return;
+  }
+  // threshold: the (E-hc)-th smallest eligible key; above it all heavy, at it
+  // the smallest indices first.
+  long long below, equal;
+  const unsigned long long ut =
+      block_radix_select<NT>(key, B, lo, E - hc, hist, sh, &below, &equal);
+  const long long above = (long long)E - below - equal;
+  const long long need_eq = hc - above;
+  // ties in index order: each thread scans a contiguous index range
+  const int64_t per = (B + NT - 1) / NT;
+  const int64_t i0 = threadIdx.x * per, i1 = min(B, i0 + per);
+  int my_eq = 0;
+  for (int64_t i = i0; i < i1; ++i) my_eq += key(i) == ut;
+  int tot;
+  int rank = block_exscan<NT>(my_eq, redi, &tot);
+  for (int64_t i = i0; i < i1; ++i) {
+    const unsigned long long u = key(i);
+    bool h = u > ut;
+    if (u == ut) {
+      h = rank < need_eq;
+      ++rank;
+    }
+    if (h) atomicOr(&bw[i >> 5], 1u << (i & 31));
+  }
+  if (threadIdx.x == 0 && nheavy) nheavy[item] = (int)hc;
+}
+
+int run_heavy_bitmap(const double2* values, int64_t nsets, int64_t B, const double* thr,
+                     int64_t hc, const int32_t* item_sig, const int32_t* active, uint32_t* bits,
+                     int32_t* nheavy, cudaStream_t st) {
+  if (nsets <= 0) return 0;
+  k_heavy_bitmap<<<(unsigned)nsets, kFloorNT, 0, st>>>(values, B, thr, hc, item_sig, active,
+                                                       bits, nheavy);
+  SFFT_CHECK_LAUNCH("k_heavy_bitmap");
+  return 0;
+}
+
+// ================================================================ votes (A10, A11)
+
+__device__ __forceinline__ int vote_count(const VoteRounds& vr, const uint32_t* bits_s,
+                                          const int64_t* sig_s, const int64_t* bp_s, int64_t f) {
+  int cnt = 0;
+  const int64_t n = vr.n;
+  for (int r = 0; r < vr.R; ++r) {
+    const int64_t bp = bp_s ? bp_s[r] : 0;
+    const int64_t m = mulmod(sig_s[r], pmod(f - bp, n), n);
+    int64_t b = pmod(m - vr.cs + vr.L / 2, n) / vr.L;
+    if (b >= vr.B) b -= vr.B;
+    cnt += (bits_s[(int64_t)r * vr.words + (b >> 5)] >> (b & 31)) & 1u;
+  }
+  return cnt;
+}
+
+constexpr int kVoteNT = 512;
+constexpr int kVoteChunk = 4096;  // positions per CTA
+
+// Pass 1: counts (optionally stored) and, per chunk, a histogram of counts.
+__global__ void __launch_bounds__(kVoteNT) k_votes_hist(VoteRounds vr, const int64_t* counts_in,
+                                                        int64_t* counts_out, int nchunks,
+                                                        int* chist /*[S][nchunks][R+1]*/) {
+  extern __shared__ uint32_t sbits[];
+  __shared__ int h[65];
+  const int s = blockIdx.y;
+  const int chunk = blockIdx.x;
+  const int R = vr.R;
+  const int64_t* sig_s = vr.sigma ? vr.sigma + (int64_t)s * R : nullptr;
+  const int64_t* bp_s = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
+  const uint32_t* bits_s = sbits;
+  if (!counts_in) {
+    const uint32_t* g = vr.bits + (int64_t)s * R * vr.words;
+    for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += kVoteNT) sbits[i] = g[i];
+  }
+  for (int i = threadIdx.x; i <= R; i += kVoteNT) h[i] = 0;
+  __syncthreads();
+  const int64_t p0 = (int64_t)chunk * kVoteChunk;
+  for (int64_t p = p0 + threadIdx.x; p < min(vr.n, p0 + kVoteChunk); p += kVoteNT) {
+    int c;
+    if (counts_in) c = (int)counts_in[(int64_t)s * vr.n + p];
+    else c = vote_count(vr, bits_s, sig_s, bp_s, p);
+    if (counts_out) counts_out[(int64_t)s * vr.n + p] = c;
+    if (c > 0) atomicAdd(&h[c], 1);
+  }
+  __syncthreads();
+  int* o = chist + ((int64_t)s * nchunks + chunk) * (R + 1);
+  for (int i = threadIdx.x; i <= R; i += kVoteNT) o[i] = h[i];
+}
+
+// Pass 2: base[s][chunk][c] = (#positions with count > c) + (#count==c in
+// earlier chunks); ntot[s] = #positions with count >= need (capped at keep).
+__global__ void k_votes_scan(int nchunks, int R, int need, int keep, int* chist,
+                             int32_t* ncand) {
+  const int s = blockIdx.x;
+  int* hs = chist + (int64_t)s * nchunks * (R + 1);
+  __shared__ long long tot[65];
+  for (int c = threadIdx.x; c <= R; c += blockDim.x) {
+    long long run = 0;
+    for (int k = 0; k < nchunks; ++k) {
+      const int v = hs[(int64_t)k * (R + 1) + c];
+      hs[(int64_t)k * (R + 1) + c] = (int)run;
+      run += v;
+    }
+    tot[c] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long above = 0, sel = 0;
+    for (int c = R; c >= 0; --c) {
+      const long long t = tot[c];
+      tot[c] = above;
+      if (c >= need && c > 0) sel += t;
+      above += t;
+    }
+    ncand[s] = (int)(sel < keep ? sel : keep);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c <= R; c += blockDim.x) {
+    const long long a = tot[c];
+    for (int k = 0; k < nchunks; ++k) hs[(int64_t)k * (R + 1) + c] += (int)a;
+  }
+}
+
+// Pass 3: each chunk ranks its candidates (count >= need) in position order
+// within their count class and writes those with rank < keep.
+__global__ void __launch_bounds__(kVoteNT) k_votes_emit(VoteRounds vr, const int64_t* counts_in,
+                                                        int nchunks, const int* chist, int need,
+                                                        int keep, int64_t* cand,
+                                                        int32_t* cand_count) {
+  extern __shared__ uint32_t sbits[];
+  __shared__ int red[32];
+  __shared__ int64_t lpos[kVoteChunk];
+  __shared__ uint8_t lcnt[kVoteChunk];
+  __shared__ int run[65];
+  const int s = blockIdx.y;
+  const int chunk = blockIdx.x;
+  const int R = vr.R;
+  const int64_t* sig_s = vr.sigma ? vr.sigma + (int64_t)s * R : nullptr;
+  const int64_t* bp_s = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
+  if (!counts_in) {
+    const uint32_t* g = vr.bits + (int64_t)s * R * vr.words;
+    for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += kVoteNT) sbits[i] = g[i];
+  }
+  const int* base = chist + ((int64_t)s * nchunks + chunk) * (R + 1);
+  for (int i = threadIdx.x; i <= R; i += kVoteNT) run[i] = base[i];
+  __syncthreads();
+  // each thread owns 8 consecutive positions (kVoteChunk = 8 * kVoteNT)
+  const int64_t p0 = (int64_t)chunk * kVoteChunk + threadIdx.x * 8;
+  int cnts[8];
+  int mine = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t p = p0 + j;
+    int c = 0;
+    if (p < vr.n) {
+      if (counts_in) c = (int)counts_in[(int64_t)s * vr.n + p];
+      else c = vote_count(vr, sbits, sig_s, bp_s, p);
+    }
+    cnts[j] = c;
+    mine += (c >= need && c > 0);
+  }
+  int total;
+  int off = block_exscan<kVoteNT>(mine, red, &total);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (cnts[j] >= need && cnts[j] > 0) {
+      lpos[off] = p0 + j;
+      lcnt[off] = (uint8_t)cnts[j];
+      ++off;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t* cs = cand + (int64_t)s * keep;
+    for (int i = 0; i < total; ++i) {
+      const int c = lcnt[i];
+      const int rk = run[c]++;
+      if (rk < keep) cs[rk] = lpos[i];
+    }
+  }
+  (void)cand_count;
+}
+
+int run_votes(const VoteRounds& vr, int S, const int64_t* counts_in, int64_t* counts_out,
+              int need, int keep, int64_t* cand, int32_t* ncand, int* chist, bool emit,
+              cudaStream_t st) {
+  SFFT_REQUIRE(vr.R >= 0 && vr.R <= 64, "votes: rounds must be <= 64");
+  const int nchunks = (int)cdiv_up(vr.n, kVoteChunk);
+  const size_t sm = counts_in ? 0 : (size_t)vr.R * vr.words * sizeof(uint32_t);
+  SFFT_REQUIRE(sm <= 200 * 1024, "votes: heavy bitmaps exceed shared memory");
+  SFFT_CUDA(cudaFuncSetAttribute(k_votes_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sm ? sm : 1)));
+  dim3 g(nchunks, S);
+  k_votes_hist<<<g, kVoteNT, sm, st>>>(vr, counts_in, counts_out, nchunks, chist);
+  SFFT_CHECK_LAUNCH("k_votes_hist");
+  if (!emit) return 0;
+  k_votes_scan<<<S, 64, 0, st>>>(nchunks, vr.R, need, keep, chist, ncand);
+  SFFT_CHECK_LAUNCH("k_votes_scan");
+  const size_t sm3 = sm;
+  const size_t static3 = kVoteChunk * (8 + 1) + 65 * 4 + 32 * 4;
+  SFFT_REQUIRE(sm3 + static3 <= 220 * 1024, "votes: heavy bitmaps exceed shared memory");
+  SFFT_CUDA(cudaFuncSetAttribute(k_votes_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sm3 ? sm3 : 1)));
+  k_votes_emit<<<g, kVoteNT, sm3, st>>>(vr, counts_in, nchunks, chist, need, keep, cand, ncand);
+  SFFT_CHECK_LAUNCH("k_votes_emit");
+  return 0;
+}
+
+size_t votes_ws_bytes(int64_t n, int S, int R) {
+  return (size_t)cdiv_up(n, kVoteChunk) * S * (R + 1) * sizeof(int);
+}
+
+// ================================================================ estimates (A12, A13)
+
+// est[item][c] for item = (s, r): y[b]/(G[bL-m] * w^{tau m}); (NaN, 0) when
+// |G| < 0.05 * gmax (numpy assigns a real NaN into the complex array).
+__device__ __forceinline__ double2 energy_est_one(const double2* y, const double2* gt,
+                                                  double gfloor, int64_t n, int64_t B,
+                                                  int64_t L, int64_t sigma, int64_t tau,
+                                                  int64_t f) {
+  const int64_t m = mulmod(sigma, pmod(f, n), n);
+  const int64_t b = pmod(m + L / 2, n) / L;
+  const int64_t e = pmod(b * L - m, n);
+  const double2 w = gt[(e % L) * B + e / L];
+  if (cabs_(w) < gfloor) return cmk(CUDART_NAN, 0.0);
+  const double2 ph = unit_root(n, mulmod(tau % n, m, n));
+  return cdiv(y[b], cmul(w, ph));
+}
+
+// numpy linear quantile interpolation (_lerp in numpy/lib/_function_base_impl.py)
+__device__ __forceinline__ double np_lerp(double a, double b, double t) {
+  const double d = b - a;
+  return (t >= 0.5) ? (b - d * (1.0 - t)) : (a + d * t);
+}
+
+__device__ __forceinline__ void isort(double* v, int m) {
+  for (int i = 1; i < m; ++i) {
+    const double x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) {
+      v[j + 1] = v[j];
+      --j;
+    }
+    v[j + 1] = x;
+  }
+}
+
+// nanmedian over m values (mean of the two middle values for even counts)
+__device__ __forceinline__ double nanmedian(const double* src, int R, double* tmp) {
+  int m = 0;
+  for (int i = 0; i < R; ++i)
+    if (!isnan(src[i])) tmp[m++] = src[i];
+  if (m == 0) return CUDART_NAN;
+  isort(tmp, m);
+  const int h = m / 2;
+  return (m % 2) ? (tmp[h] + tmp[h]) / 2.0 : (tmp[h - 1] + tmp[h]) / 2.0;
+}
+
+// a + 1j*b as numpy forms it (NaN/inf in b poisons the real part)
+__device__ __forceinline__ double2 np_join(double a, double b) {
+  return cmk(a + (0.0 * b - 0.0), 0.0 + b);
+}
+
+constexpr int kMaxRounds = 64;
+
+// Trimmed mean over the R rows of est (row stride ld) for one column.
+__device__ double2 trimmed_mean_col(const double2* est, int64_t ld, int R) {
+  double re[kMaxRounds], im[kMaxRounds], tmp[kMaxRounds], dev[kMaxRounds];
+  for (int r = 0; r < R; ++r) {
+    const double2 v = est[(int64_t)r * ld];
+    re[r] = v.x;
+    im[r] = v.y;
+  }
+  const double mr = nanmedian(re, R, tmp);
+  const double mi = nanmedian(im, R, tmp);
+  const double2 med = np_join(mr, mi);
+  int m = 0;
+  for (int r = 0; r < R; ++r) {
+    dev[r] = hypot(re[r] - med.x, im[r] - med.y);
+    if (!isnan(dev[r])) tmp[m++] = dev[r];
+  }
+  double spread = CUDART_NAN;
+  if (m > 0) {
+    isort(tmp, m);
+    const double vi = (double)m * 0.25 + (1.0 + 0.25 * (1.0 - 1.0 - 1.0)) - 1.0;
+    double prev = floor(vi);
+    const double gamma = vi - prev;
+    int lo = (int)prev;
+    lo = lo < 0 ? 0 : (lo > m - 1 ? m - 1 : lo);
+    const int hi = lo + 1 > m - 1 ? m - 1 : lo + 1;
+    spread = np_lerp(tmp[lo], tmp[hi], gamma);
+  }
+  const double a4 = 4.0 * spread;
+  const double b8 = 1e-8 * (cabs_(med) + 1e-300);
+  const double tol = (isnan(a4) || isnan(b8)) ? CUDART_NAN : fmax(a4, b8);
+  double sr = 0.0, si = 0.0;
+  int cr = 0, ci = 0;
+  for (int r = 0; r < R; ++r) {
+    const bool keep = dev[r] <= tol;
+    const bool bad = !keep || isnan(re[r]) || isnan(im[r]);
+    if (!bad) {
+      sr += re[r];
+      si += im[r];
+      ++cr;
+      ++ci;
+    }
+  }
+  const double mre = cr ? sr / cr : CUDART_NAN;
+  const double mim = ci ? si / ci : CUDART_NAN;
+  return np_join(mre, mim);
+}
+
+__global__ void k_trimmed_mean(const double2* __restrict__ est, int R, int64_t C,
+                               double2* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  out[c] = trimmed_mean_col(est + c, C, R);
+}
+
+int run_trimmed_mean(const double2* est, int R, int64_t C, double2* out, cudaStream_t st) {
+  SFFT_REQUIRE(R >= 1 && R <= kMaxRounds, "trimmed_mean: 1 <= rounds <= 64");
+  if (C <= 0) return 0;
+  k_trimmed_mean<<<(unsigned)cdiv_up(C, 128), 128, 0, st>>>(est, R, C, out);
+  SFFT_CHECK_LAUNCH("k_trimmed_mean");
+  return 0;
+}
+
+__global__ void k_energy_est(const double2* __restrict__ y, int64_t B, const double2* gt,
+                             const double* gmax, int64_t n, int R, const int64_t* sigma,
+                             const int64_t* tau, const int64_t* cand, int64_t C,
+                             double2* __restrict__ est) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (c >= C) return;
+  const int64_t L = n / B;
+  est[(int64_t)r * C + c] = energy_est_one(y + (int64_t)r * B, gt, 0.05 * gmax[0], n, B, L,
+                                           sigma[r], tau[r], cand[c]);
+}
+
+int run_energy_est(const double2* y, int64_t B, const double2* gt, const double* gmax, int64_t n,
+                   int R, const int64_t* sigma, const int64_t* tau, const int64_t* cand,
+                   int64_t C, double2* est, cudaStream_t st) {
+  if (C <= 0 || R <= 0) return 0;
+  dim3 g((unsigned)cdiv_up(C, 128), R);
+  k_energy_est<<<g, 128, 0, st>>>(y, B, gt, gmax, n, R, sigma, tau, cand, C, est);
+  SFFT_CHECK_LAUNCH("k_energy_est");
+  return 0;
+}
+
+// ================================================================ subtraction (A14)
+
+// out[item][i] = y[item][bk] - sum_t c_t * G[(bk*L - m_t) mod n] * w^{(tau_tot m_t) mod n},
+// bk = i (full) or blist[item*nb + i]; tones of signal item_sig[item] in order.
+constexpr int kSubNT = 256;
+constexpr int kSubChunk = 256;
+
+__global__ void __launch_bounds__(kSubNT) k_subtract(
+    const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
+    const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
+    const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
+    const int32_t* tcount, int64_t tstride, const int32_t* gate) {
+  __shared__ int64_t s_row[kSubChunk];
+  __shared__ int64_t s_q[kSubChunk];
+  __shared__ double2 s_c[kSubChunk];
+  __shared__ double2 s_ph[kSubChunk];
+  const int item = blockIdx.y;
+  const int sig = item_sig ? item_sig[item] : item;
+  if (gate && !gate[sig]) return;
+  const int64_t i = (int64_t)blockIdx.x * kSubNT + threadIdx.x;
+  const int64_t L = n / B;
+  const int64_t sg = sigma[item];
+  const int64_t tt = tau_tot[item];
+  const int64_t T = tcount[sig];
+  const int64_t* tp = tpos + (int64_t)sig * tstride;
+  const double2* tc = tcoef + (int64_t)sig * tstride;
+  int64_t bk = 0;
+  double2 acc = cmk(0.0, 0.0);
+  const bool live = i < nb;
+  if (live) {
+    bk = blist ? blist[(int64_t)item * nb + i] : i;
+    acc = y[(int64_t)item * B + bk];
+  }
+  for (int64_t t0 = 0; t0 < T; t0 += kSubChunk) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < kSubChunk && t0 + j < T; j += kSubNT) {
+      const int64_t m = mulmod(sg, pmod(tp[t0 + j], n), n);
+      s_row[j] = (L - m % L) % L;
+      s_q[j] = (m + L - 1) / L;
+      s_c[j] = tc[t0 + j];
+      s_ph[j] = unit_root(n, mulmod(tt, m, n));
+    }
+    __syncthreads();
+    if (live) {
+      const int64_t tn = (T - t0 < kSubChunk) ? (T - t0) : kSubChunk;
+      for (int64_t j = 0; j < tn; ++j) {
+        int64_t col = bk - s_q[j];
+        col += (col < 0) ? B : 0;
+        const double2 w = __ldg(gt + s_row[j] * B + col);
+        acc = csub(acc, cmul(cmul(s_c[j], w), s_ph[j]));
+      }
+    }
+  }
+  if (live) out[(int64_t)item * nb + i] = acc;
+}
+
+int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
+                       const int32_t* blist, int64_t nitems, const double2* gt, int64_t n,
+                       const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
+                       const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
+                       int64_t tstride, const int32_t* gate, cudaStream_t st) {
+  if (nitems <= 0 || nb <= 0) return 0;
+  dim3 g((unsigned)cdiv_up(nb, kSubNT), (unsigned)nitems);
+  k_subtract<<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma, tau_tot, tpos,
+                                   tcoef, tcount, tstride, gate);
+  SFFT_CHECK_LAUNCH("k_subtract");
+  return 0;
+}
+
+int run_subtract(const double2* y, double2* out, int64_t B, int64_t nb, const int32_t* blist,
+                 int64_t nitems, const double2* gt, int64_t n, const int32_t* item_sig,
+                 const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos,
+                 const double2* tcoef, const int32_t* tcount, int64_t tstride, cudaStream_t st) {
+  return run_subtract_gated(y, out, B, nb, blist, nitems, gt, n, item_sig, sigma, tau_tot, tpos,
+                            tcoef, tcount, tstride, nullptr, st);
+}
+
+}  // namespace sfft

@@ -1,0 +1,777 @@
+// Batched iterative framework with phase location (sfft/frameworks.py:439-516,
+// :556-570) and the residual polish (:573-608), device-resident.
+//
+// S signals advance in lock step; every decision (convergence, heavy set,
+// ladder unwrapping, consistency, merge into the recovered list, the residual
+// test, polish corrections) is taken on the device per signal, and kernels
+// of finished signals exit at once.  The host only loops over iterations and
+// reads one "signals still active" counter per iteration.
+//
+// Per iteration and signal (perm = perms[s][it-1]):
+//   y[j] = bucketize(x, sigma, tau + d_j), d = {0} U ladder       (one launch)
+//   y0  -= model(recovered)                   all B buckets      (k_subtract)
+//   floor, convergence, heavy list (-|y0|, b)                    (k_it_decide)
+//   y[j>0] - model(recovered) at heavy buckets; unwrap; checks   (k_it_locate)
+//   merge found into recovered (insertion order = heavy order)   (k_it_merge)
+//   |y0 - model(found)| < 1.3 floor ?                            (k_subtract, k_it_resid)
+#include "kernels.cuh"
+#include "schedule.cuh"
+
+namespace sfft {
+
+struct IterState {
+  double scale_ref;
+  double floor;
+  double final_resid;
+  int32_t iterations;
+  int32_t converged;
+  int32_t entries;     // loop entries = permutations consumed by the loop
+  int32_t n_rec;
+  int32_t nheavy;
+  int32_t nfound;
+  int32_t polish;
+  int32_t pending;
+  int32_t cursor;      // next permutation index (polish)
+  int32_t ngroups;
+};
+
+struct IterArgs {
+  int64_t n, B, L, omega, k;
+  int S, P, M, max_it, cap;      // cap = recovered capacity per signal
+  int64_t ladder[kMaxShifts];    // d_1..d_{M-1}
+  const int64_t* psig;           // [S][P]
+  const int64_t* ptau;           // [S][P]
+  const double2* gt;             // [L][B]
+  const double* gmax;
+  // workspace
+  IterState* st;
+  int32_t* active;               // [S] main loop gate
+  int32_t* gate;                 // [S] secondary gate (residual / polish)
+  int32_t* n_active;             // device counter
+  int32_t* item_sig;             // [M*S]
+  int64_t* item_sigma;           // [M*S]
+  int64_t* item_tau;             // [M*S]
+  double2* y;                    // [M][S][B]
+  double2* resid;                // [S][B]
+  int64_t* rec_pos;              // [S][cap]
+  double2* rec_coef;             // [S][cap]
+  int32_t* rec_count;            // [S]
+  int32_t* heavy;                // [S][B]
+  int64_t* f_pos;                // [S][B] per heavy index
+  double2* f_coef;               // [S][B]
+  int32_t* f_ok;                 // [S][B]
+  int64_t* fc_pos;               // [S][B] compacted found (heavy order)
+  double2* fc_coef;              // [S][B]
+  int32_t* fc_count;             // [S]
+  int32_t* pend;                 // [S][cap] polish pending flags
+  double2* delta;                // [S][cap] polish corrections
+  Group* groups;                 // [S][kMaxGroups]
+};
+
+// ------------------------------------------------------------------ items
+__global__ void k_it_items(IterArgs a, int p, int nsh, const int64_t* shifts_dev,
+                           bool use_cursor) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsh * a.S) return;
+  const int j = i / a.S, s = i - j * a.S;
+  const int pi = use_cursor ? a.st[s].cursor : p;
+  const int pp = pi < a.P ? pi : a.P - 1;
+  a.item_sig[i] = s;
+  a.item_sigma[i] = a.psig[(int64_t)s * a.P + pp];
+  const int64_t d = shifts_dev ? shifts_dev[j] : (j == 0 ? 0 : a.ladder[j - 1]);
+  a.item_tau[i] = pmod(a.ptau[(int64_t)s * a.P + pp] + d, a.n);
+}
+
+// ------------------------------------------------------------------ decide
+constexpr int kDecNT = 512;
+
+// Floor / convergence / heavy list of y0 (sfft/frameworks.py:478-490).
+__global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a, int it) {
+  extern __shared__ unsigned char dsm[];
+  __shared__ unsigned hist[256];
+  __shared__ long long sh[4];
+  __shared__ double redd[32];
+  __shared__ unsigned long long redu[32];
+  __shared__ int redi[32];
+  const int s = blockIdx.x;
+  if (!a.active[s]) return;
+  IterState& S = a.st[s];
+  const int64_t B = a.B;
+  const double2* y0 = a.y + (int64_t)s * B;  // slot 0
+  double med, peak;
+  median_and_peak<kDecNT>(y0, B, &med, &peak, hist, sh, redd, redu);
+  const double robust = fmax(fmax(fmin(3.0 * med, 0.25 * peak), 1e-9 * peak), 1e-300);
+  const double sref = fmax(S.scale_ref, peak);
+  const double fl = fmax(robust, 1e-9 * sref);
+  const bool conv = peak < 1.3 * fl;
+  // log the measurement group (the ladder only counts when it was used)
+  if (threadIdx.x == 0) {
+    S.scale_ref = sref;
+    S.floor = fl;
+    const int g = S.ngroups;
+    if (g < kMaxGroups) {
+      Group& G = a.groups[(int64_t)s * kMaxGroups + g];
+      G.kind = 0;
+      G.a = a.item_sigma[s];
+      G.tau = a.item_tau[s];
+      G.cnt = a.omega;
+      G.nsh = conv ? 1 : a.M;
+      G.sh[0] = 0;
+      for (int j = 1; j < a.M; ++j) G.sh[j] = a.ladder[j - 1];
+      S.ngroups = g + 1;
+    }
+    S.entries = it;
+    if (conv) {
+      S.converged = 1;
+      S.final_resid = peak;
+      S.iterations = it - 1;
+      a.active[s] = 0;
+      atomicSub(a.n_active, 1);
+    }
+  }
+  if (conv) return;
+  // heavy = {b : |y0[b]| >= floor} in (-|y0|, b) order
+  unsigned long long* k1 = (unsigned long long*)dsm;
+  long long* k2 = (long long*)(k1 + kFusedMaxB);
+  int* pay = (int*)(k2 + kFusedMaxB);
+  const unsigned long long ufl = dbits(fl);
+  const int64_t per = (B + kDecNT - 1) / kDecNT;
+  const int64_t i0 = threadIdx.x * per, i1 = min(B, i0 + per);
+  int mine = 0;
+  for (int64_t i = i0; i < i1; ++i) mine += dbits(cabs_(y0[i])) >= ufl;
+  int total;
+  int off = block_exscan<kDecNT>(mine, redi, &total);
+  const bool sortable = B <= kFusedMaxB;
+  int32_t* hv = a.heavy + (int64_t)s * B;
+  for (int64_t i = i0; i < i1; ++i) {
+    const unsigned long long u = dbits(cabs_(y0[i]));
+    if (u >= ufl) {
+      if (sortable) {
+        k1[off] = ~u;
+        k2[off] = i;
+        pay[off] = (int)i;
+      } else {
+        hv[off] = (int)i;
+      }
+      ++off;
+    }
+  }
+  __syncthreads();
+  if (sortable) {
+    int cap = 1;
+    while (cap < total) cap <<= 1;
+    block_bitonic<kDecNT>(k1, k2, pay, total, cap);
+    for (int i = threadIdx.x; i < total; i += kDecNT) hv[i] = pay[i];
+  }
+  if (threadIdx.x == 0) S.nheavy = total;
+}
+
+// ------------------------------------------------------------------ locate
+constexpr int kLocNT = 128;
+constexpr int kLocChunk = 32;
+
+// Ladder values at heavy buckets minus the recovered model, phase unwrap,
+// passband / consistency / weight checks, coefficient (frameworks.py:493-516).
+__global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a) {
+  __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
+  __shared__ double2 t_c[kLocChunk];
+  __shared__ double2 t_ph[kLocChunk][kMaxShifts];
+  const int s = blockIdx.y;
+  if (!a.active[s]) return;
+  const IterState& S = a.st[s];
+  const int nh = S.nheavy;
+  const int h0 = blockIdx.x * kLocNT;
+  if (h0 >= nh) return;
+  const int h = h0 + threadIdx.x;
+  const bool live = h < nh;
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int M = a.M;
+  const int64_t sigma = a.item_sigma[s];
+  const int64_t tau = a.item_tau[s];  // shift 0 item
+  const int b = live ? a.heavy[(int64_t)s * B + h] : 0;
+  double2 ys[kMaxShifts];
+  ys[0] = a.y[(int64_t)s * B + b];
+  for (int j = 1; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
+  // subtract the recovered model from the ladder values (y0 already clean)
+  const int T = a.rec_count[s];
+  const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  const double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  for (int t0 = 0; t0 < T; t0 += kLocChunk) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < kLocChunk * M; q += kLocNT) {
+      const int tt = q / M, j = q - tt * M;
+      if (t0 + tt >= T || j == 0) continue;
+      const int64_t m = mulmod(sigma, pmod(rp[t0 + tt], n), n);
+      const int64_t tj = pmod(tau + a.ladder[j - 1], n);
+      t_ph[tt][j] = unit_root(n, mulmod(tj, m, n));
+      if (j == 1) {
+        t_row[tt] = (L - m % L) % L;
+        t_q[tt] = (m + L - 1) / L;
+        t_c[tt] = rc[t0 + tt];
+      }
+    }
+    __syncthreads();
+    if (live) {
+      const int tn = min(kLocChunk, T - t0);
+      for (int tt = 0; tt < tn; ++tt) {
+        int64_t col = b - t_q[tt];
+        col += (col < 0) ? B : 0;
+        const double2 cw = cmul(t_c[tt], __ldg(a.gt + t_row[tt] * B + col));
+        for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cmul(cw, t_ph[tt][j]));
+      }
+    }
+  }
+  if (!live) return;
+  const int64_t fi = (int64_t)s * B + h;
+  a.f_ok[fi] = 0;
+  const double2 y0 = ys[0];
+  // _unwrap_position (frameworks.py:179-196): ladder[0] == 1
+  if (cabs_(y0) == 0.0) return;
+  const double nd = (double)n;
+  const double scl = -nd / (2.0 * 3.141592653589793);
+  auto fmodpos = [&](double v, double m) {
+    double r = fmod(v, m);
+    if (r != 0.0 && r < 0.0) r += m;
+    if (r == 0.0) r = 0.0;
+    return r;
+  };
+  double2 r1 = cdiv(ys[1], y0);
+  double q = fmodpos(atan2(r1.y, r1.x) * scl, nd);
+  for (int j = 2; j < M; ++j) {
+    const double2 rj = cdiv(ys[j], y0);
+    const double phi = fmodpos(atan2(rj.y, rj.x) * scl, nd);
+    const double d = (double)a.ladder[j - 1];
+    const double period = nd / d;
+    const double base = phi / d;
+    q = base + rint((q - base) / period) * period;
+  }
+  const int64_t qi = pmod((int64_t)rint(q), n);
+  // passband of bucket b
+  const int64_t lo = pmod((int64_t)b * L - L / 2, n);
+  if (pmod(qi - lo, n) >= L) return;
+  // ladder consistency
+  const double tol = fmax(3.0 * S.floor, 0.15 * cabs_(y0));
+  for (int j = 1; j < M; ++j) {
+    const double2 pred = cmul(y0, unit_root(n, mulmod(a.ladder[j - 1] % n, qi, n)));
+    if (cabs_(csub(ys[j], pred)) > tol) return;
+  }
+  const int64_t e = pmod((int64_t)b * L - qi, n);
+  const double2 w = a.gt[(e % L) * B + e / L];
+  if (cabs_(w) < 0.05 * a.gmax[0]) return;
+  // mean of the dephased ladder values / w
+  double2 sum = cmk(0.0, 0.0);
+  for (int j = 0; j < M; ++j) {
+    const int64_t sh = (j == 0) ? 0 : a.ladder[j - 1];
+    const int64_t ex = pmod(-mulmod(pmod(tau + sh, n), qi, n), n);
+    sum = cadd(sum, cmul(ys[j], unit_root(n, ex)));
+  }
+  const double2 coeff = cdiv(cdivr(sum, (double)M), w);
+  const int64_t f = mulmod(modinv(sigma, n), qi, n);
+  a.f_pos[fi] = f;
+  a.f_coef[fi] = coeff;
+  a.f_ok[fi] = 1;
+}
+
+// ------------------------------------------------------------------ merge
+constexpr int kMrgNT = 512;
+
+__global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
+  __shared__ int redi[32];
+  const int s = blockIdx.x;
+  if (!a.active[s]) return;
+  IterState& S = a.st[s];
+  const int nh = S.nheavy;
+  const int64_t B = a.B;
+  const int n_old = a.rec_count[s];
+  int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  const int64_t* fp = a.f_pos + (int64_t)s * B;
+  const double2* fcf = a.f_coef + (int64_t)s * B;
+  const int32_t* fok = a.f_ok + (int64_t)s * B;
+  const int per = (nh + kMrgNT - 1) / kMrgNT;
+  const int h0 = threadIdx.x * per, h1 = min(nh, h0 + per);
+  int nnew = 0, nok = 0;
+  for (int h = h0; h < h1; ++h) {
+    if (!fok[h]) continue;
+    ++nok;
+    bool exists = false;
+    for (int t = 0; t < n_old && !exists; ++t) exists = rp[t] == fp[h];
+    nnew += !exists;
+  }
+  int tot_new, tot_ok;
+  int off_new = block_exscan<kMrgNT>(nnew, redi, &tot_new);
+  int off_ok = block_exscan<kMrgNT>(nok, redi, &tot_ok);
+  int64_t* cp = a.fc_pos + (int64_t)s * B;
+  double2* cc = a.fc_coef + (int64_t)s * B;
+  for (int h = h0; h < h1; ++h) {
+    if (!fok[h]) continue;
+    cp[off_ok] = fp[h];
+    cc[off_ok] = fcf[h];
+    ++off_ok;
+    int where = -1;
+    for (int t = 0; t < n_old && where < 0; ++t)
+      if (rp[t] == fp[h]) where = t;
+    if (where >= 0) {
+      rc[where] = cadd(rc[where], fcf[h]);
+    } else if (n_old + off_new < a.cap) {
+      rp[n_old + off_new] = fp[h];
+      rc[n_old + off_new] = fcf[h];
+      ++off_new;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nrec = min(a.cap, n_old + tot_new);
+    a.rec_count[s] = nrec;
+    S.n_rec = nrec;
+    S.nfound = tot_ok;
+    a.fc_count[s] = tot_ok;
+    a.gate[s] = (nrec >= a.k && tot_ok > 0) ? 1 : 0;
+  }
+}
+
+// ------------------------------------------------------------------ residual test
+__global__ void __launch_bounds__(kDecNT) k_it_resid(IterArgs a, int it) {
+  __shared__ double redd[32];
+  const int s = blockIdx.x;
+  if (!a.active[s]) return;
+  IterState& S = a.st[s];
+  bool conv = false;
+  double mx = 0.0;
+  if (a.gate[s]) {
+    const double2* r = a.resid + (int64_t)s * a.B;
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < a.B; i += kDecNT) m = fmax(m, cabs_(r[i]));
+    mx = block_max<kDecNT>(m, redd);
+    conv = mx < 1.3 * S.floor;
+  }
+  if (threadIdx.x == 0) {
+    if (conv) {
+      S.converged = 1;
+      S.final_resid = mx;
+      S.iterations = it;
+      a.active[s] = 0;
+      atomicSub(a.n_active, 1);
+    } else if (it == a.max_it) {
+      S.iterations = it;
+      a.active[s] = 0;
+      atomicSub(a.n_active, 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ polish
+__global__ void k_po_setup(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  IterState& S = a.st[s];
+  S.polish = (S.converged && S.n_rec > 0 && S.final_resid < 0.01 * S.scale_ref) ? 1 : 0;
+  S.cursor = S.entries;
+  S.pending = 0;
+}
+
+__global__ void k_po_epoch(IterArgs a) {
+  const int s = blockIdx.y;
+  const IterState& S = a.st[s];
+  if (!S.polish) return;
+  const int T = S.n_rec;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
+    a.pend[(int64_t)s * a.cap + t] = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.st[s].pending = T;
+}
+
+// polish gate + group log; items come from k_it_items with use_cursor
+__global__ void k_po_gate(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  IterState& S = a.st[s];
+  const int on = S.polish && S.pending > 0;
+  a.gate[s] = on;
+}
+
+__global__ void k_po_log(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S || !a.gate[s]) return;
+  IterState& S = a.st[s];
+  const int g = S.ngroups;
+  if (g < kMaxGroups) {
+    Group& G = a.groups[(int64_t)s * kMaxGroups + g];
+    G.kind = 0;
+    G.a = a.item_sigma[s];
+    G.tau = a.item_tau[s];
+    G.cnt = a.omega;
+    G.nsh = 3;
+    G.sh[0] = 0;
+    G.sh[1] = 1;
+    G.sh[2] = 2;
+    S.ngroups = g + 1;
+  }
+  S.cursor += 1;
+}
+
+constexpr int kPoNT = 256;
+constexpr int kPoChunk = 128;
+
+// One pass of _polish_flat_estimates for one signal (frameworks.py:590-608):
+// occupancy of every recovered tone's bucket, then each pending, non-collided
+// tone with a usable weight gets mean_t(resid_t[b] w^{-(tau+t)m}) / w.
+__global__ void __launch_bounds__(kPoNT) k_po_correct(IterArgs a) {
+  extern __shared__ int occ[];
+  __shared__ int64_t u_row[kPoChunk], u_q[kPoChunk];
+  __shared__ double2 u_c[kPoChunk];
+  __shared__ double2 u_ph[kPoChunk][3];
+  __shared__ int redi[32];
+  const int s = blockIdx.x;
+  if (!a.gate[s]) return;
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int T = a.rec_count[s];
+  const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  const double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  int32_t* pend = a.pend + (int64_t)s * a.cap;
+  double2* dl = a.delta + (int64_t)s * a.cap;
+  const int64_t sigma = a.item_sigma[s];
+  const int64_t tau = a.item_tau[s];
+  for (int64_t i = threadIdx.x; i < B; i += kPoNT) occ[i] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += kPoNT) {
+    const int64_t m = mulmod(sigma, pmod(rp[t], n), n);
+    atomicAdd(&occ[pmod(m + L / 2, n) / L], 1);
+  }
+  __syncthreads();
+  const double wfloor = 0.05 * a.gmax[0];
+  int corrected = 0;
+  for (int base = 0; base < T; base += kPoNT) {
+    const int t = base + threadIdx.x;
+    bool mine = false;
+    int64_t m = 0, bi = 0;
+    double2 w = cmk(0.0, 0.0);
+    if (t < T && pend[t]) {
+      m = mulmod(sigma, pmod(rp[t], n), n);
+      bi = pmod(m + L / 2, n) / L;
+      if (occ[bi] == 1) {
+        const int64_t e = pmod(bi * L - m, n);
+        w = a.gt[(e % L) * B + e / L];
+        mine = cabs_(w) >= wfloor;
+      }
+    }
+    double2 r[3];
+    for (int d = 0; d < 3; ++d) r[d] = mine ? a.y[((int64_t)d * a.S + s) * B + bi] : cmk(0, 0);
+    for (int u0 = 0; u0 < T; u0 += kPoChunk) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < kPoChunk; q += kPoNT) {
+        if (u0 + q >= T) continue;
+        const int64_t mu = mulmod(sigma, pmod(rp[u0 + q], n), n);
+        u_row[q] = (L - mu % L) % L;
+        u_q[q] = (mu + L - 1) / L;
+        u_c[q] = rc[u0 + q];
+        for (int d = 0; d < 3; ++d) u_ph[q][d] = unit_root(n, mulmod(pmod(tau + d, n), mu, n));
+      }
+      __syncthreads();
+      if (mine) {
+        const int un = min(kPoChunk, T - u0);
+        for (int q = 0; q < un; ++q) {
+          int64_t col = bi - u_q[q];
+          col += (col < 0) ? B : 0;
+          const double2 cw = cmul(u_c[q], __ldg(a.gt + u_row[q] * B + col));
+          for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q][d]));
+        }
+      }
+    }
+    if (mine) {
+      double2 acc = cmk(0.0, 0.0);
+      for (int d = 0; d < 3; ++d) {
+        const int64_t ex = pmod(-mulmod(pmod(tau + d, n), m, n), n);
+        acc = cadd(acc, cmul(r[d], unit_root(n, ex)));
+      }
+      dl[t] = cdiv(cdivr(acc, 3.0), w);
+      ++corrected;
+    }
+  }
+  __syncthreads();
+  // apply after every residual has been formed with the pre-pass coefficients
+  double2* rcw = a.rec_coef + (int64_t)s * a.cap;
+  for (int base = 0; base < T; base += kPoNT) {
+    const int t = base + threadIdx.x;
+    if (t < T && pend[t]) {
+      const int64_t m = mulmod(sigma, pmod(rp[t], n), n);
+      const int64_t bi = pmod(m + L / 2, n) / L;
+      if (occ[bi] == 1) {
+        const int64_t e = pmod(bi * L - m, n);
+        const double2 w = a.gt[(e % L) * B + e / L];
+        if (cabs_(w) >= wfloor) {
+          rcw[t] = cadd(rcw[t], dl[t]);
+          pend[t] = 0;
+        }
+      }
+    }
+  }
+  const int tot = block_sum_int<kPoNT>(corrected, redi);
+  if (threadIdx.x == 0) a.st[s].pending -= tot;
+}
+
+// ------------------------------------------------------------------ finalize
+constexpr int kFinNT = 512;
+
+// entries with c != 0, top k by (-|c|, f) (sfft/frameworks.py:151-155).
+__global__ void __launch_bounds__(kFinNT) k_finalize(const int64_t* rec_pos,
+                                                     const double2* rec_coef,
+                                                     const int32_t* rec_count, int cap,
+                                                     int64_t k, int64_t* out_pos,
+                                                     double2* out_coef, int32_t* out_n,
+                                                     int32_t* overflow) {
+  extern __shared__ unsigned char fsm[];
+  const int s = blockIdx.x;
+  const int T = rec_count[s];
+  const int64_t* rp = rec_pos + (int64_t)s * cap;
+  const double2* rc = rec_coef + (int64_t)s * cap;
+  unsigned long long* k1 = (unsigned long long*)fsm;
+  long long* k2 = (long long*)(k1 + kFusedMaxB);
+  int* pay = (int*)(k2 + kFusedMaxB);
+  if (T > kFusedMaxB) {
+    if (threadIdx.x == 0) {
+      overflow[0] = 1;
+      out_n[s] = 0;
+    }
+    return;
+  }
+  __shared__ int redi[32];
+  int mine = 0;
+  const int per = (T + kFinNT - 1) / kFinNT;
+  const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+  for (int t = t0; t < t1; ++t) mine += (rc[t].x != 0.0 || rc[t].y != 0.0);
+  int tot;
+  int off = block_exscan<kFinNT>(mine, redi, &tot);
+  for (int t = t0; t < t1; ++t) {
+    if (rc[t].x != 0.0 || rc[t].y != 0.0) {
+      k1[off] = ~dbits(cabs_(rc[t]));
+      k2[off] = rp[t];
+      pay[off] = t;
+      ++off;
+    }
+  }
+  __syncthreads();
+  int capp = 1;
+  while (capp < tot) capp <<= 1;
+  block_bitonic<kFinNT>(k1, k2, pay, tot, capp);
+  const int kk = (int)(k < (int64_t)tot ? k : (int64_t)tot);
+  for (int i = threadIdx.x; i < kk; i += kFinNT) {
+    out_pos[(int64_t)s * k + i] = rp[pay[i]];
+    out_coef[(int64_t)s * k + i] = rc[pay[i]];
+  }
+  if (threadIdx.x == 0) out_n[s] = kk;
+}
+
+// ------------------------------------------------------------------ host driver
+
+struct IterLayout {
+  size_t off[32];
+  size_t total;
+};
+
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
+  IterLayout L{};
+  size_t o = 0;
+  size_t sizes[] = {
+      sizeof(IterState) * S,                 // 0 st
+      sizeof(int32_t) * S,                   // 1 active
+      sizeof(int32_t) * S,                   // 2 gate
+      sizeof(int32_t) * 4,                   // 3 n_active + overflow
+      sizeof(int32_t) * M * S,               // 4 item_sig
+      sizeof(int64_t) * M * S,               // 5 item_sigma
+      sizeof(int64_t) * M * S,               // 6 item_tau
+      sizeof(double2) * (size_t)M * S * B,   // 7 y
+      sizeof(double2) * (size_t)S * B,       // 8 resid
+      sizeof(int64_t) * (size_t)S * cap,     // 9 rec_pos
+      sizeof(double2) * (size_t)S * cap,     // 10 rec_coef
+      sizeof(int32_t) * S,                   // 11 rec_count
+      sizeof(int32_t) * (size_t)S * B,       // 12 heavy
+      sizeof(int64_t) * (size_t)S * B,       // 13 f_pos
+      sizeof(double2) * (size_t)S * B,       // 14 f_coef
+      sizeof(int32_t) * (size_t)S * B,       // 15 f_ok
+      sizeof(int64_t) * (size_t)S * B,       // 16 fc_pos
+      sizeof(double2) * (size_t)S * B,       // 17 fc_coef
+      sizeof(int32_t) * S,                   // 18 fc_count
+      sizeof(int32_t) * (size_t)S * cap,     // 19 pend
+      sizeof(double2) * (size_t)S * cap,     // 20 delta
+      sizeof(Group) * (size_t)S * kMaxGroups,// 21 groups
+      sizeof(int64_t) * 3,                   // 22 shifts (polish)
+      sizeof(int32_t) * S,                   // 23 ngroups copy
+  };
+  const int cnt = sizeof(sizes) / sizeof(sizes[0]);
+  for (int i = 0; i < cnt; ++i) {
+    L.off[i] = o;
+    o += al(sizes[i]);
+  }
+  L.total = o;
+  return L;
+}
+
+size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap) {
+  return iter_layout(n, B, S, M, cap).total + bucketize_ws_bytes(B, (int64_t)M * S);
+}
+
+__global__ void k_copy_ngroups(const IterState* st, int S, int32_t* ng) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S) ng[s] = st[s].ngroups;
+}
+
+__global__ void k_it_outputs(const IterState* st, int S, int32_t* iters, int32_t* conv) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  iters[s] = st[s].iterations;
+  conv[s] = st[s].converged;
+}
+
+int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
+                  const double* taps, int64_t omega, int64_t B, const double2* gt,
+                  const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
+                  int P, int64_t k, int max_it, const int64_t* ladder, int nlad, int cap,
+                  int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
+                  int32_t* out_conv, int64_t* out_samples, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  const int M = 1 + nlad;
+  SFFT_REQUIRE(M <= kMaxShifts, "iterative: ladder too long");
+  SFFT_REQUIRE(max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
+  SFFT_REQUIRE(P >= max_it + 6, "iterative: need max_iterations + 6 permutations");
+  SFFT_REQUIRE(ws_bytes >= iterative_ws_bytes(n, B, S, M, cap), "iterative: workspace too small");
+  const IterLayout Lo = iter_layout(n, B, S, M, cap);
+  char* w = (char*)ws;
+  IterArgs a{};
+  a.n = n;
+  a.B = B;
+  a.L = n / B;
+  a.omega = omega;
+  a.k = k;
+  a.S = S;
+  a.P = P;
+  a.M = M;
+  a.max_it = max_it;
+  a.cap = cap;
+  for (int j = 0; j < nlad; ++j) a.ladder[j] = ladder[j];
+  a.psig = psig;
+  a.ptau = ptau;
+  a.gt = gt;
+  a.gmax = gmax;
+  a.st = (IterState*)(w + Lo.off[0]);
+  a.active = (int32_t*)(w + Lo.off[1]);
+  a.gate = (int32_t*)(w + Lo.off[2]);
+  a.n_active = (int32_t*)(w + Lo.off[3]);
+  int32_t* overflow = a.n_active + 1;
+  a.item_sig = (int32_t*)(w + Lo.off[4]);
+  a.item_sigma = (int64_t*)(w + Lo.off[5]);
+  a.item_tau = (int64_t*)(w + Lo.off[6]);
+  a.y = (double2*)(w + Lo.off[7]);
+  a.resid = (double2*)(w + Lo.off[8]);
+  a.rec_pos = (int64_t*)(w + Lo.off[9]);
+  a.rec_coef = (double2*)(w + Lo.off[10]);
+  a.rec_count = (int32_t*)(w + Lo.off[11]);
+  a.heavy = (int32_t*)(w + Lo.off[12]);
+  a.f_pos = (int64_t*)(w + Lo.off[13]);
+  a.f_coef = (double2*)(w + Lo.off[14]);
+  a.f_ok = (int32_t*)(w + Lo.off[15]);
+  a.fc_pos = (int64_t*)(w + Lo.off[16]);
+  a.fc_coef = (double2*)(w + Lo.off[17]);
+  a.fc_count = (int32_t*)(w + Lo.off[18]);
+  a.pend = (int32_t*)(w + Lo.off[19]);
+  a.delta = (double2*)(w + Lo.off[20]);
+  a.groups = (Group*)(w + Lo.off[21]);
+  int64_t* po_shifts = (int64_t*)(w + Lo.off[22]);
+  int32_t* ngroups = (int32_t*)(w + Lo.off[23]);
+  void* bws = w + Lo.total;
+  const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
+
+  // state init
+  SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
+  SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
+  SFFT_CUDA(cudaMemsetAsync(a.n_active, 0, sizeof(int32_t) * 4, st));
+  {
+    std::vector<int32_t> ones(S, 1);
+    SFFT_CUDA(cudaMemcpyAsync(a.active, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st));
+    const int32_t na = S;
+    SFFT_CUDA(cudaMemcpyAsync(a.n_active, &na, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    const int64_t ps[3] = {0, 1, 2};
+    SFFT_CUDA(cudaMemcpyAsync(po_shifts, ps, sizeof(ps), cudaMemcpyHostToDevice, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
+  }
+
+  Prod p{};
+  p.x = x;
+  p.xstride = xstride;
+  p.n = n;
+  p.taps = taps;
+  p.omega = omega;
+  p.B = B;
+  p.item_sig = a.item_sig;
+  p.item_a = a.item_sigma;
+  p.item_b = a.item_tau;
+  p.active = a.active;
+
+  const size_t dsm = (size_t)kFusedMaxB * (8 + 8 + 4);
+  SFFT_CUDA(cudaFuncSetAttribute(k_it_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  SFFT_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  const size_t occ_sm = (size_t)B * sizeof(int);
+  SFFT_REQUIRE(occ_sm <= 160 * 1024, "iterative: B too large for the polish occupancy table");
+  SFFT_CUDA(cudaFuncSetAttribute(k_po_correct, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(occ_sm, 1)));
+
+  const unsigned sb = (unsigned)cdiv_up(S, 128);
+  for (int it = 1; it <= max_it; ++it) {
+    k_it_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a, it - 1, M, nullptr, false);
+    SFFT_CHECK_LAUNCH("k_it_items");
+    int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
+    if (rc) return rc;
+    // y0 -= model(recovered), all buckets
+    rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
+                            a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st);
+    if (rc) return rc;
+    k_it_decide<<<S, kDecNT, dsm, st>>>(a, it);
+    SFFT_CHECK_LAUNCH("k_it_decide");
+    dim3 gl((unsigned)cdiv_up(B, kLocNT), S);
+    k_it_locate<<<gl, kLocNT, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_it_locate");
+    k_it_merge<<<S, kMrgNT, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_it_merge");
+    // residual of y0 after the tones found now (only where gate[s])
+    rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
+                            a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st);
+    if (rc) return rc;
+    k_it_resid<<<S, kDecNT, 0, st>>>(a, it);
+    SFFT_CHECK_LAUNCH("k_it_resid");
+    int32_t na = 0;
+    SFFT_CUDA(cudaMemcpyAsync(&na, a.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));
+    if (na <= 0) break;
+  }
+
+  // polish (2 epochs x <= 3 passes x shifts 0,1,2)
+  k_po_setup<<<sb, 128, 0, st>>>(a);
+  SFFT_CHECK_LAUNCH("k_po_setup");
+  p.active = a.gate;
+  for (int epoch = 0; epoch < 2; ++epoch) {
+    k_po_epoch<<<dim3(4, S), 256, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_po_epoch");
+    for (int pass = 0; pass < 3; ++pass) {
+      k_po_gate<<<sb, 128, 0, st>>>(a);
+      k_it_items<<<(unsigned)cdiv_up((int64_t)3 * S, 256), 256, 0, st>>>(a, 0, 3, po_shifts, true);
+      SFFT_CHECK_LAUNCH("k_it_items(polish)");
+      k_po_log<<<sb, 128, 0, st>>>(a);
+      int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)3 * S, W, a.y, bws, bws_bytes, st);
+      if (rc) return rc;
+      k_po_correct<<<S, kPoNT, occ_sm, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_po_correct");
+    }
+  }
+
+  k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
+                                      out_coef, out_n, overflow);
+  SFFT_CHECK_LAUNCH("k_finalize");
+  k_it_outputs<<<sb, 128, 0, st>>>(a.st, S, out_iters, out_conv);
+  k_copy_ngroups<<<sb, 128, 0, st>>>(a.st, S, ngroups);
+  k_union_count<<<S, kUnionNT, 0, st>>>(a.groups, ngroups, kMaxGroups, n, out_samples);
+  SFFT_CHECK_LAUNCH("k_union_count");
+  return 0;
+}
+
+}  // namespace sfft

@@ -1,6 +1,9 @@
 // Host-side launchers shared by the .cu translation units.
 #pragma once
 
+#include <algorithm>
+#include <vector>
+
 #include "fft.cuh"
 
 namespace sfft {
@@ -33,5 +36,48 @@ int run_absmax(const double2* v, int64_t count, double* out, cudaStream_t st);
 int run_mark(uint8_t* map, int64_t n, int kind, int64_t a, int64_t b, int64_t c,
              const int64_t* idx, cudaStream_t st);
 int run_count_nonzero(const uint8_t* map, int64_t n, int64_t* out, cudaStream_t st);
+
+// decode.cu
+int run_floor(const double2* values, int64_t nsets, int64_t B, double mult,
+              const int32_t* item_sig, const int32_t* active, double* floor_out, double* peak_out,
+              cudaStream_t st);
+int run_heavy_bitmap(const double2* values, int64_t nsets, int64_t B, const double* thr,
+                     int64_t hc, const int32_t* item_sig, const int32_t* active, uint32_t* bits,
+                     int32_t* nheavy, cudaStream_t st);
+struct VoteRounds {
+  const uint32_t* bits;   // [S][R][words]
+  const int64_t* sigma;   // [S*R]
+  const int64_t* bprime;  // [S*R] (null: 0)
+  int64_t n, B, L, words, cs;
+  int R;
+};
+int run_votes(const VoteRounds& vr, int S, const int64_t* counts_in, int64_t* counts_out,
+              int need, int keep, int64_t* cand, int32_t* ncand, int* chist, bool emit,
+              cudaStream_t st);
+size_t votes_ws_bytes(int64_t n, int S, int R);
+int run_trimmed_mean(const double2* est, int R, int64_t C, double2* out, cudaStream_t st);
+int run_energy_est(const double2* y, int64_t B, const double2* gt, const double* gmax, int64_t n,
+                   int R, const int64_t* sigma, const int64_t* tau, const int64_t* cand,
+                   int64_t C, double2* est, cudaStream_t st);
+int run_subtract(const double2* y, double2* out, int64_t B, int64_t nb, const int32_t* blist,
+                 int64_t nitems, const double2* gt, int64_t n, const int32_t* item_sig,
+                 const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos,
+                 const double2* tcoef, const int32_t* tcount, int64_t tstride, cudaStream_t st);
+
+int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
+                       const int32_t* blist, int64_t nitems, const double2* gt, int64_t n,
+                       const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
+                       const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
+                       int64_t tstride, const int32_t* gate, cudaStream_t st);
+
+// iterative.cu
+size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap);
+int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
+                  const double* taps, int64_t omega, int64_t B, const double2* gt,
+                  const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
+                  int P, int64_t k, int max_it, const int64_t* ladder, int nlad, int cap,
+                  int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
+                  int32_t* out_conv, int64_t* out_samples, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
 
 }  // namespace sfft

@@ -1,0 +1,153 @@
+// Read schedules of the runners and the map-free samples_read count.
+//
+// The reference marks a bool map per gathered index (sfft/signal.py:82-86)
+// and counts it at the end (RecoveryResult.samples_read, sfft/frameworks.py:
+// 151-155).  Here each signal logs its measurement groups instead — a flat
+// group is one permutation sigma with a handful of extra shifts (the phase
+// ladder, or the polish shifts 0/1/2), a spike group one (stride, tau) — and
+// one CTA per signal counts |union of read indices| exactly:
+//   flat group g reads {sigma_g * t : t in U_g},  U_g = union_d [-tau-d, Omega-tau-d) mod n
+//   an index e of group g is new iff no earlier group h holds it:
+//     flat h:  (sigma_h^{-1} e mod n) in U_h;  spike h: (e + tau_h) mod L_h == 0.
+// No bookkeeping store touches HBM during the gathers.
+#pragma once
+
+#include "block.cuh"
+
+namespace sfft {
+
+constexpr int kMaxShifts = 16;
+constexpr int kMaxGroups = 64;
+constexpr int kMaxPieces = 2 * kMaxShifts;
+
+struct Group {
+  int64_t a;     // flat: sigma | spike: stride L
+  int64_t tau;   // base shift
+  int64_t cnt;   // flat: Omega | spike: number of samples
+  int32_t kind;  // 0 flat, 1 spike
+  int32_t nsh;   // extra shifts (flat)
+  int64_t sh[kMaxShifts];
+};
+
+SFFT_HD int64_t modinv(int64_t a, int64_t n) {
+  int64_t t = 0, nt = 1, r = n, nr = pmod(a, n);
+  while (nr) {
+    const int64_t q = r / nr;
+    int64_t tmp = t - q * nt; t = nt; nt = tmp;
+    tmp = r - q * nr; r = nr; nr = tmp;
+  }
+  return t < 0 ? t + n : t;
+}
+
+struct GroupSh {
+  int64_t lo[kMaxPieces];
+  int64_t hi[kMaxPieces];
+  int np;
+  int64_t total;
+  int64_t ainv;
+};
+
+// Merge the circular intervals [s_d, s_d + omega) (mod n) into disjoint
+// linear pieces of [0, n).  Single thread.
+__device__ inline void merge_pieces(const Group& g, int64_t n, GroupSh* out) {
+  int64_t lo[kMaxPieces], hi[kMaxPieces];
+  int m = 0;
+  if (g.kind == 1) {
+    out->np = 0;
+    out->total = g.cnt;
+    out->ainv = 0;
+    return;
+  }
+  const int64_t w = g.cnt >= n ? n : g.cnt;
+  for (int d = 0; d < g.nsh; ++d) {
+    const int64_t s = pmod(-g.tau - g.sh[d], n);
+    if (w >= n) { lo[m] = 0; hi[m] = n; ++m; continue; }
+    if (s + w <= n) { lo[m] = s; hi[m] = s + w; ++m; }
+    else { lo[m] = s; hi[m] = n; ++m; lo[m] = 0; hi[m] = s + w - n; ++m; }
+  }
+  // insertion sort by lo
+  for (int i = 1; i < m; ++i) {
+    const int64_t a = lo[i], b = hi[i];
+    int j = i - 1;
+    while (j >= 0 && lo[j] > a) { lo[j + 1] = lo[j]; hi[j + 1] = hi[j]; --j; }
+    lo[j + 1] = a; hi[j + 1] = b;
+  }
+  int k = 0;
+  int64_t tot = 0;
+  for (int i = 0; i < m; ++i) {
+    if (k > 0 && lo[i] <= out->hi[k - 1]) {
+      if (hi[i] > out->hi[k - 1]) out->hi[k - 1] = hi[i];
+    } else {
+      out->lo[k] = lo[i];
+      out->hi[k] = hi[i];
+      ++k;
+    }
+  }
+  for (int i = 0; i < k; ++i) tot += out->hi[i] - out->lo[i];
+  out->np = k;
+  out->total = tot;
+  out->ainv = modinv(g.a, n);
+}
+
+__device__ __forceinline__ bool group_has(const Group& g, const GroupSh& gs, int64_t n,
+                                          int64_t e) {
+  if (g.kind == 1) {
+    const int64_t v = pmod(e + g.tau, n);
+    return (v % g.a) == 0 && (v / g.a) < g.cnt;
+  }
+  const int64_t t = mulmod(gs.ainv, e, n);
+  for (int i = 0; i < gs.np; ++i)
+    if (t >= gs.lo[i] && t < gs.hi[i]) return true;
+  return false;
+}
+
+// e of element j of group g (j < gs.total)
+__device__ __forceinline__ int64_t group_elem(const Group& g, const GroupSh& gs, int64_t n,
+                                              int64_t j) {
+  if (g.kind == 1) return pmod(g.a * j - g.tau, n);
+  for (int i = 0; i < gs.np; ++i) {
+    const int64_t len = gs.hi[i] - gs.lo[i];
+    if (j < len) return mulmod(g.a, gs.lo[i] + j, n);
+    j -= len;
+  }
+  return 0;
+}
+
+constexpr int kUnionNT = 512;
+
+// One CTA per signal: samples[s] = |union of the read sets of groups[s][0..ngroups[s])|.
+__global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __restrict__ groups,
+                                                          const int32_t* ngroups, int gstride,
+                                                          int64_t n, int64_t* samples) {
+  __shared__ Group sg[kMaxGroups];
+  __shared__ GroupSh sp[kMaxGroups];
+  __shared__ unsigned long long red[32];
+  const int s = blockIdx.x;
+  const int G = min(ngroups[s], kMaxGroups);
+  const Group* gs = groups + (int64_t)s * gstride;
+  for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += kUnionNT) merge_pieces(sg[i], n, &sp[i]);
+  __syncthreads();
+  unsigned long long cnt = 0;
+  for (int g = 0; g < G; ++g) {
+    const int64_t tot = sp[g].total;
+    for (int64_t j = threadIdx.x; j < tot; j += kUnionNT) {
+      const int64_t e = group_elem(sg[g], sp[g], n, j);
+      bool fresh = true;
+      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e);
+      cnt += fresh;
+    }
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < kUnionNT / 32; ++i) t += red[i];
+    samples[s] = (int64_t)t;
+  }
+}
+
+}  // namespace sfft

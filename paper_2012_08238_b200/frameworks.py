@@ -1,0 +1,308 @@
+"""Runner drop-ins (sfft/frameworks.py) backed by device-resident engines.
+
+``AlgorithmConfig`` / ``RecoveryResult`` / ``run_algorithm`` keep the
+reference's fields, validation and dispatch (:67-155, :704-715).
+``run_voting`` / ``run_iterative`` / ``run_peeling`` keep their signatures
+``(x, k, cfg) -> RecoveryResult``; each is the one-signal case of a batched
+``*_batch(xs, k, cfg)`` that runs many independent signals through one
+sequence of sm_100a kernels (csrc/voting.cu, iterative.cu, peeling.cu).
+
+Randomness: the host draws every permutation with the reference's own
+generator calls (``np.random.default_rng(cfg.seed)`` then
+PermutationParams.random in order) and uploads them, so the device consumes
+exactly the reference's stream.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+from dataclasses import asdict, dataclass, replace
+
+import numpy as np
+
+from ._lib import check, lib, ptr, stream_of
+from .errors import ConfigMismatch
+from .filters import FLAT, SPIKE, make_flat_filter, twiddles
+from .signal import PermutationParams, SparseSpectrum, TimeSignal
+
+__all__ = ["AlgorithmConfig", "RecoveryResult", "BatchResult", "FRAMEWORKS", "run_algorithm",
+           "run_voting", "run_iterative", "run_peeling", "run_voting_batch",
+           "run_iterative_batch", "run_peeling_batch", "phase_ladder", "draw_perms"]
+
+FRAMEWORKS = ("one_shot", "voting", "iterative", "peeling", "dense")
+
+_LOCATIONS = {"one_shot": {"prony"}, "voting": {"statistics"},
+              "iterative": {"phase", "binary", "multiscale"}, "peeling": {"phase"},
+              "dense": {"direct"}}
+_DEFAULT_LOCATION = {"one_shot": "prony", "voting": "statistics", "iterative": "phase",
+                     "peeling": "phase", "dense": "direct"}
+_FILTERS = {"one_shot": SPIKE, "voting": FLAT, "iterative": FLAT, "peeling": SPIKE,
+            "dense": "none"}
+_ESTIMATIONS = {"one_shot": {"prony"}, "voting": {"energy"}, "iterative": {"energy"},
+                "peeling": {"energy"}, "dense": {"direct"}}
+_DEFAULT_ESTIMATION = {"one_shot": "prony", "voting": "energy", "iterative": "energy",
+                       "peeling": "energy", "dense": "direct"}
+
+
+@dataclass(frozen=True)
+class AlgorithmConfig:
+    """Same fields, validation, JSON round trip and digest as the reference
+    (sfft/frameworks.py:67-138), so records are interchangeable."""
+
+    framework: str
+    filter_kind: str | None = None
+    num_buckets: int | None = None
+    coprime_factors: tuple | None = None
+    location_method: str | None = None
+    estimation_method: str | None = None
+    rounds: int = 10
+    max_iterations: int = 10
+    a_max: int = 4
+    branching: int = 2
+    pursuit_shifts: int = 8
+    spike_prestage: bool = False
+    prestage_width: int = 32
+    min_vote_fraction: float = 0.5
+    seed: int = 0
+
+    def validated(self) -> "AlgorithmConfig":
+        if self.framework not in FRAMEWORKS:
+            raise ConfigMismatch(f"unknown framework {self.framework!r}")
+        fk = self.filter_kind or _FILTERS[self.framework]
+        if fk != _FILTERS[self.framework]:
+            raise ConfigMismatch(
+                f"{self.framework} requires the {_FILTERS[self.framework]} filter, got {fk}")
+        loc = self.location_method or _DEFAULT_LOCATION[self.framework]
+        if loc not in _LOCATIONS[self.framework]:
+            raise ConfigMismatch(f"{self.framework} cannot use location {loc!r}")
+        est = self.estimation_method or _DEFAULT_ESTIMATION[self.framework]
+        if est not in _ESTIMATIONS[self.framework]:
+            raise ConfigMismatch(f"{self.framework} cannot use estimation {est!r}")
+        if self.framework == "peeling" and not self.coprime_factors:
+            raise ConfigMismatch("peeling requires coprime_factors")
+        if self.a_max < 1:
+            raise ConfigMismatch(f"a_max={self.a_max} must be >= 1")
+        return replace(self, filter_kind=fk, location_method=loc, estimation_method=est)
+
+    def resolve_buckets(self, n: int, k: int) -> int:
+        b = self.num_buckets
+        if b is None:
+            mult = 8 if self.framework == "one_shot" else 4
+            b = 1 << max(3, math.ceil(math.log2(max(mult * max(k, 1), 8))))
+            while b > max(n // 2, 1):
+                b //= 2
+        if n % b != 0:
+            raise ConfigMismatch(f"num_buckets={b} does not divide n={n}")
+        return b
+
+    def to_json(self) -> str:
+        d = asdict(self)
+        if d["coprime_factors"] is not None:
+            d["coprime_factors"] = list(d["coprime_factors"])
+        return json.dumps(d, sort_keys=True)
+
+    @classmethod
+    def from_json(cls, text: str) -> "AlgorithmConfig":
+        d = json.loads(text)
+        if d.get("coprime_factors") is not None:
+            d["coprime_factors"] = tuple(d["coprime_factors"])
+        return cls(**d)
+
+    def digest(self) -> str:
+        return hashlib.sha1(self.to_json().encode()).hexdigest()[:12]
+
+
+@dataclass
+class RecoveryResult:
+    spectrum: SparseSpectrum
+    samples_read: int
+    iterations: int
+    converged: bool
+
+
+@dataclass
+class BatchResult:
+    """Device outputs of a batched run: pos/coef [S][k] in (-|c|, f) order,
+    count/iterations/converged/samples_read [S]."""
+
+    n: int
+    k: int
+    pos: object
+    coef: object
+    count: object
+    iterations: object
+    converged: object
+    samples_read: object
+
+    def to_results(self) -> list:
+        pos = self.pos.cpu().numpy()
+        coef = self.coef.cpu().numpy()
+        cnt = self.count.cpu().numpy()
+        its = self.iterations.cpu().numpy()
+        conv = self.converged.cpu().numpy()
+        smp = self.samples_read.cpu().numpy()
+        out = []
+        for s in range(pos.shape[0]):
+            c = int(cnt[s])
+            ent = {int(p): complex(v) for p, v in zip(pos[s, :c], coef[s, :c])}
+            out.append(RecoveryResult(SparseSpectrum(self.n, ent), int(smp[s]), int(its[s]),
+                                      bool(conv[s])))
+        return out
+
+
+def phase_ladder(n: int) -> list:
+    """1, 8, 64, ... below N/16, then N/16 (sfft/frameworks.py:199-213)."""
+    ladder, delta, top = [], 1, max(n // 16, 1)
+    while delta < top:
+        ladder.append(delta)
+        delta *= 8
+    ladder.append(top)
+    return ladder
+
+
+def draw_perms(n: int, seed: int, count: int):
+    """The first ``count`` permutations of default_rng(seed) (sigma, tau)."""
+    rng = np.random.default_rng(seed)
+    sig = np.empty(count, dtype=np.int64)
+    tau = np.empty(count, dtype=np.int64)
+    for i in range(count):
+        p = PermutationParams.random(n, rng)
+        sig[i], tau[i] = p.sigma, p.tau
+    return sig, tau
+
+
+def _as_batch(xs):
+    """[S][N] CUDA tensor (complex64/complex128) from a tensor, a TimeSignal
+    or a list of TimeSignals."""
+    import torch
+    if isinstance(xs, TimeSignal):
+        return xs.samples.unsqueeze(0), [xs]
+    if isinstance(xs, (list, tuple)):
+        sigs = list(xs)
+        return torch.stack([s.samples for s in sigs]), sigs
+    t = xs if xs.ndim == 2 else xs.unsqueeze(0)
+    return t.contiguous(), None
+
+
+def _empty_batch(n, S, k, dev, iterations, converged):
+    import torch
+    kk = max(k, 1)
+    return BatchResult(n, max(k, 0), torch.zeros((S, kk), dtype=torch.int64, device=dev),
+                       torch.zeros((S, kk), dtype=torch.complex128, device=dev),
+                       torch.zeros(S, dtype=torch.int32, device=dev),
+                       torch.full((S,), iterations, dtype=torch.int32, device=dev),
+                       torch.full((S,), int(converged), dtype=torch.int32, device=dev),
+                       torch.zeros(S, dtype=torch.int64, device=dev))
+
+
+class _WS:
+    buf: dict = {}
+
+    @classmethod
+    def get(cls, nbytes, device):
+        import torch
+        key = str(device)
+        t = cls.buf.get(key)
+        if t is None or t.numel() < nbytes:
+            cls.buf.pop(key, None)
+            t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+            cls.buf[key] = t
+        return t
+
+
+# ------------------------------------------------------------------ iterative
+
+def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
+    """run_iterative (phase location) for every row of ``xs`` at once."""
+    import torch
+    cfg = cfg.validated()
+    if cfg.framework != "iterative":
+        raise ConfigMismatch(f"run_iterative got framework {cfg.framework!r}")
+    X, _ = _as_batch(xs)
+    S, n = X.shape
+    dev = X.device
+    if k <= 0:
+        return _empty_batch(n, S, 0, dev, 0, True)
+    if cfg.location_method != "phase":
+        raise NotImplementedError(
+            "binary/multiscale location is outside the device hot path (SURVEY.md §8(f) #1)")
+    b = cfg.resolve_buckets(n, k)
+    filt = make_flat_filter(n, b, device=dev)
+    ladder = phase_ladder(n)
+    M = 1 + len(ladder)
+    P = cfg.max_iterations + 6
+    sig, tau = draw_perms(n, cfg.seed, P)
+    psig = torch.as_tensor(np.tile(sig, (S, 1)), device=dev)
+    ptau = torch.as_tensor(np.tile(tau, (S, 1)), device=dev)
+    cap = cfg.max_iterations * b
+    out_pos = torch.zeros((S, k), dtype=torch.int64, device=dev)
+    out_coef = torch.zeros((S, k), dtype=torch.complex128, device=dev)
+    out_n = torch.zeros(S, dtype=torch.int32, device=dev)
+    out_it = torch.zeros(S, dtype=torch.int32, device=dev)
+    out_cv = torch.zeros(S, dtype=torch.int32, device=dev)
+    out_sm = torch.zeros(S, dtype=torch.int64, device=dev)
+    L = lib()
+    wsb = L.sfft_iterative_ws_bytes(n, b, S, M, cap)
+    ws = _WS.get(wsb, dev)
+    import ctypes
+    lad = (ctypes.c_int64 * len(ladder))(*ladder)
+    dt = 0 if X.dtype == torch.complex64 else 1
+    gmax = torch.tensor([filt.peak], dtype=torch.float64, device=dev)
+    check(L.sfft_run_iterative(dt, ptr(X), n, X.stride(0), S, ptr(filt.taps), filt.support, b,
+                               ptr(filt.gtable), ptr(gmax), ptr(twiddles(b, dev)), ptr(psig),
+                               ptr(ptau), P, k, cfg.max_iterations, lad, len(ladder), cap,
+                               ptr(out_pos), ptr(out_coef), ptr(out_n), ptr(out_it), ptr(out_cv),
+                               ptr(out_sm), ptr(ws), wsb, stream_of(dev)), "sfft_run_iterative")
+    return BatchResult(n, k, out_pos, out_coef, out_n, out_it, out_cv, out_sm)
+
+
+def run_iterative(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
+    """Permute, bucketize, locate single-tons by phase, subtract, repeat
+    (sfft/frameworks.py:439-570), then polish (:573-608)."""
+    return _single(run_iterative_batch, x, k, cfg)
+
+
+def _single(batch_fn, x, k, cfg) -> RecoveryResult:
+    res = batch_fn(x, k, cfg).to_results()[0]
+    if isinstance(x, TimeSignal) and x._log:
+        # earlier reads of this signal count too (access counter only grows)
+        res.samples_read = max(res.samples_read, x.access_count)
+    return res
+
+
+# ------------------------------------------------------------------ dispatch
+
+def run_voting_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
+    from .voting import voting_batch
+    return voting_batch(xs, k, cfg)
+
+
+def run_voting(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
+    """Randomised rounds, heavy-bucket votes, energy estimates, trimmed mean and
+    two model-refinement passes (sfft/frameworks.py:354-417)."""
+    return _single(run_voting_batch, x, k, cfg)
+
+
+def run_peeling_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
+    from .peeling import peeling_batch
+    return peeling_batch(xs, k, cfg)
+
+
+def run_peeling(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
+    """Co-prime spike stages decoded by single-ton peeling
+    (sfft/frameworks.py:614-699)."""
+    return _single(run_peeling_batch, x, k, cfg)
+
+
+_RUNNERS = {"voting": run_voting, "iterative": run_iterative, "peeling": run_peeling}
+
+
+def run_algorithm(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
+    cfg = cfg.validated()
+    if cfg.framework not in _RUNNERS:
+        raise NotImplementedError(
+            f"{cfg.framework!r} is outside the device hot path (SURVEY.md §2: one-shot and the "
+            "dense baseline are not rebuilt)")
+    return _RUNNERS[cfg.framework](x, k, cfg)
