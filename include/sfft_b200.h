@@ -30,6 +30,22 @@ extern "C" {
 int sfft_version(void);
 const char* sfft_last_error(void);
 
+/* Read-schedule export of the runners: per signal max_groups records of
+ * words_per_group int64 = {kind (0 flat, 1 spike, -1 unused), a (sigma or
+ * stride), tau, cnt (Omega or samples), nshift, shift[0..]}.  Host pointers. */
+int sfft_schedule_layout(int32_t* max_groups, int32_t* words_per_group);
+
+/* Number of kernels this library has launched in this process. */
+int64_t sfft_launch_count(void);
+
+/* Measurement aid: with profiling on, every flat/spike bucketization launch
+ * is bracketed by CUDA events recorded on its stream (no synchronisation;
+ * read back by sfft_prof_read), and the items it processed are counted on
+ * the device.  sfft_prof_read returns the
+ * summed kernel milliseconds, launch count and item count since enable. */
+int sfft_prof_enable(int on);
+int sfft_prof_read(double* ms, int64_t* launches, int64_t* items);
+
 /* ---- setup ------------------------------------------------------------ */
 
 /* W[e] = exp(-2*pi*i*e/B), e < B (complex128).  FFT twiddle table. */
@@ -143,7 +159,8 @@ size_t sfft_iterative_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t nshif
  * (PermutationParams.random draws in order; nperm >= max_iterations + 6).
  * ladder_host (HOST int64[nladder]) is _phase_ladder(n).  Outputs per signal:
  * out_pos/out_coef [nsig][k] the top-k entries in (-|c|, f) order,
- * out_count, out_iterations, out_converged, out_samples (samples_read).
+ * out_count, out_iterations, out_converged, out_samples (samples_read);
+ * out_sched (optional) receives the read schedule, see sfft_schedule_layout.
  * Synchronises the stream once per iteration (early exit when all
  * signals have stopped). */
 int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
@@ -152,8 +169,8 @@ int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int
                        const int64_t* perm_tau, int64_t nperm, int64_t k, int64_t max_iterations,
                        const int64_t* ladder_host, int64_t nladder, int64_t cap, int64_t* out_pos,
                        void* out_coef, int32_t* out_count, int32_t* out_iterations,
-                       int32_t* out_converged, int64_t* out_samples, void* ws, size_t ws_bytes,
-                       void* stream);
+                       int32_t* out_converged, int64_t* out_samples, int64_t* out_sched, void* ws,
+                       size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

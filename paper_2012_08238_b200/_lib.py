@@ -108,5 +108,11 @@ SIGNATURES.update({
     "sfft_iterative_ws_bytes": (sz, [i64, i64, i64, i64, i64]),
     "sfft_run_iterative": (C.c_int, [C.c_int, vp, i64, i64, i64, P_f64, i64, i64, vp, P_f64, vp,
                                      P_i64, P_i64, i64, i64, i64, vp, i64, i64, P_i64, vp, P_i32,
-                                     P_i32, P_i32, P_i64, vp, sz, vp]),
+                                     P_i32, P_i32, P_i64, P_i64, vp, sz, vp]),
+    "sfft_schedule_layout": (C.c_int, [vp, vp]),
+})
+SIGNATURES.update({
+    "sfft_launch_count": (i64, []),
+    "sfft_prof_enable": (C.c_int, [C.c_int]),
+    "sfft_prof_read": (C.c_int, [vp, vp, vp]),
 })

@@ -7,11 +7,16 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "schedule.cuh"
+
+#include <atomic>
 
 namespace sfft {
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
 void set_error(const std::string& msg) { g_err = msg; }
 const char* last_error() { return g_err.c_str(); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace sfft
 
 using namespace sfft;
@@ -19,6 +24,41 @@ using namespace sfft;
 #define SFFT_API extern "C" __attribute__((visibility("default")))
 
 SFFT_API int sfft_version(void) { return 1; }
+
+// Number of kernels this library has launched in this process.
+SFFT_API int64_t sfft_launch_count(void) { return g_launches.load(); }
+
+// Bucketization profiling: CUDA events around every flat/spike bucketization
+// launch (synchronising after each, so only for measurement runs) and a
+// device count of the items each launch actually processed.
+SFFT_API int sfft_prof_enable(int on) {
+  BucketProf& p = bucket_prof();
+  if (on && !p.d_items) SFFT_CUDA(cudaMalloc(&p.d_items, sizeof(unsigned long long)));
+  if (p.d_items) SFFT_CUDA(cudaMemset(p.d_items, 0, sizeof(unsigned long long)));
+  if (int rc = prof_collect()) return rc;
+  p.on = on != 0;
+  p.ms = 0.0;
+  p.launches = 0;
+  return 0;
+}
+
+SFFT_API int sfft_prof_read(double* ms, int64_t* launches, int64_t* items) {
+  BucketProf& p = bucket_prof();
+  if (int rc = prof_collect()) return rc;
+  unsigned long long it = 0;
+  if (p.d_items) SFFT_CUDA(cudaMemcpy(&it, p.d_items, sizeof(it), cudaMemcpyDeviceToHost));
+  *ms = p.ms;
+  *launches = p.launches;
+  *items = (int64_t)it;
+  return 0;
+}
+
+// Layout of the optional read-schedule export of the runners.
+SFFT_API int sfft_schedule_layout(int32_t* max_groups, int32_t* words_per_group) {
+  *max_groups = kMaxGroups;
+  *words_per_group = kSchedWords;
+  return 0;
+}
 
 SFFT_API const char* sfft_last_error(void) { return last_error(); }
 
@@ -215,8 +255,8 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
                                 int64_t k, int64_t max_iterations, const int64_t* ladder_host,
                                 int64_t nladder, int64_t cap, int64_t* out_pos, void* out_coef,
                                 int32_t* out_count, int32_t* out_iterations,
-                                int32_t* out_converged, int64_t* out_samples, void* ws,
-                                size_t ws_bytes, void* stream) {
+                                int32_t* out_converged, int64_t* out_samples, int64_t* out_sched,
+                                void* ws, size_t ws_bytes, void* stream) {
   SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_iterative: dtype must be 0 or 1");
   SFFT_REQUIRE(x && taps && gtable && gmax && W && perm_sigma && perm_tau && ladder_host,
                "sfft_run_iterative: null pointer");
@@ -229,5 +269,5 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
                        gmax, (const double2*)W, perm_sigma, perm_tau, (int)nperm, k,
                        (int)max_iterations, ladder_host, (int)nladder, (int)cap, out_pos,
                        (double2*)out_coef, out_count, out_iterations, out_converged, out_samples,
-                       ws, ws_bytes, (cudaStream_t)stream);
+                       out_sched, ws, ws_bytes, (cudaStream_t)stream);
 }

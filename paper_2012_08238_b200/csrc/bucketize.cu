@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kNT) k_fused(Prod p, FftPlan P, const double2*
   const int item = blockIdx.x;
   const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
   if (c.skip) return;
+  if (p.prof_items && threadIdx.x == 0) atomicAdd(p.prof_items, 1ull);
   const int B = (int)p.B;
   for (int s = threadIdx.x; s < B; s += kNT) sm[s] = produce<Tin, MODE>(p, c, item, s);
   __syncthreads();
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2
   const int item = blockIdx.y;
   const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
   if (c.skip) return;
+  if (p.prof_items && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(p.prof_items, 1ull);
   const int c0 = blockIdx.x * CG;
   const int seg = B1 + 1;
   const int B = (int)p.B;
@@ -340,8 +342,9 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
   return 0;
 }
 
-int run_bucketize(int dtype, int mode, const Prod& p, int64_t nitems, const double2* W,
-                  double2* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+static int run_bucketize_inner(int dtype, int mode, const Prod& p, int64_t nitems,
+                               const double2* W, double2* out, void* ws, size_t ws_bytes,
+                               cudaStream_t st) {
   if (mode == PROD_FLAT)
     return dtype == 0 ? run_bucketize_t<float2, PROD_FLAT>(p, nitems, W, out, ws, ws_bytes, st)
                       : run_bucketize_t<double2, PROD_FLAT>(p, nitems, W, out, ws, ws_bytes, st);
@@ -351,6 +354,57 @@ int run_bucketize(int dtype, int mode, const Prod& p, int64_t nitems, const doub
   if (mode == PROD_GTAB)
     return run_bucketize_t<double2, PROD_GTAB>(p, nitems, W, out, ws, ws_bytes, st);
   return run_bucketize_t<double2, PROD_LOAD>(p, nitems, W, out, ws, ws_bytes, st);
+}
+
+BucketProf& bucket_prof() {
+  static BucketProf p;
+  return p;
+}
+
+int prof_begin(cudaStream_t st, cudaEvent_t* ev0) {
+  SFFT_CUDA(cudaEventCreate(ev0));
+  SFFT_CUDA(cudaEventRecord(*ev0, st));
+  return 0;
+}
+
+int prof_end(cudaStream_t st, cudaEvent_t ev0) {
+  cudaEvent_t ev1;
+  SFFT_CUDA(cudaEventCreate(&ev1));
+  SFFT_CUDA(cudaEventRecord(ev1, st));
+  bucket_prof().pending.push_back({ev0, ev1});
+  bucket_prof().launches += 1;
+  return 0;
+}
+
+int prof_collect() {
+  BucketProf& p = bucket_prof();
+  for (auto& e : p.pending) {
+    SFFT_CUDA(cudaEventSynchronize(e.second));
+    float ms = 0.f;
+    SFFT_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+    p.ms += ms;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  p.pending.clear();
+  return 0;
+}
+
+// Flat and spike bucketizations of the runners and the C ABI go through here;
+// with profiling on, each launch is bracketed by CUDA events on its stream.
+int run_bucketize(int dtype, int mode, const Prod& p0, int64_t nitems, const double2* W,
+                  double2* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  BucketProf& bp = bucket_prof();
+  if (!bp.on || (mode != PROD_FLAT && mode != PROD_SPIKE))
+    return run_bucketize_inner(dtype, mode, p0, nitems, W, out, ws, ws_bytes, st);
+  Prod p = p0;
+  p.prof_items = bp.d_items;
+  cudaEvent_t ev0;
+  int rc = prof_begin(st, &ev0);
+  if (rc) return rc;
+  rc = run_bucketize_inner(dtype, mode, p, nitems, W, out, ws, ws_bytes, st);
+  if (rc) return rc;
+  return prof_end(st, ev0);
 }
 
 int run_twiddle(double2* W, int64_t B, cudaStream_t st) {

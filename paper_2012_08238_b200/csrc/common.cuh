@@ -22,9 +22,11 @@ namespace sfft {
 // ----------------------------------------------------------------- errors
 void set_error(const std::string& msg);
 const char* last_error();
+void count_launch();   // running total of this library's kernel launches
 
 #define SFFT_CHECK_LAUNCH(what)                                                  \
   do {                                                                           \
+    ::sfft::count_launch();                                                      \
     cudaError_t _e = cudaGetLastError();                                         \
     if (_e != cudaSuccess) {                                                     \
       ::sfft::set_error(std::string(what) + ": " + cudaGetErrorString(_e));     \
@@ -75,8 +77,56 @@ __device__ __forceinline__ double2 cadd_rn(double2 a, double2 b) {
 }
 #endif
 
-// |z| as numpy's np.abs(complex128) (hypot).
-SFFT_HD double cabs_(double2 a) { return hypot(a.x, a.y); }
+// |z| as numpy's vectorised np.abs(complex128 array): larger*sqrt(fma(r,r,1)),
+// r = smaller/larger (numpy universal-intrinsics loop; bit-exact with it).
+// Used wherever the reference takes np.abs of an array.
+#ifdef __CUDA_ARCH__
+__device__ __forceinline__ double cabs_(double2 a) {
+  double re = fabs(a.x), im = fabs(a.y);
+  if (isinf(re) || isinf(im)) return CUDART_INF;
+  if (isnan(re) || isnan(im)) return CUDART_NAN;
+  const double lg = fmax(re, im), sm = fmin(re, im);
+  if (lg == 0.0) return 0.0;
+  const double r = __ddiv_rn(sm, lg);
+  return __dmul_rn(__dsqrt_rn(__fma_rn(r, r, 1.0)), lg);
+}
+// glibc 2.35+ hypot (dbl-64 e_hypot.c, non-FMA kernel): what abs() of a
+// numpy complex128 scalar and of a Python complex return.
+__device__ __forceinline__ double hypot_glibc_kernel(double ax, double ay) {
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= __dmul_rn(2.0, ay)) {
+    const double d = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, d), ax));
+    t2 = __dmul_rn(__dsub_rn(d, __dmul_rn(2.0, __dsub_rn(ax, ay))), d);
+  } else {
+    const double d = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, d), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, d), ay), ay), __dmul_rn(d, d));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+__device__ __forceinline__ double cabs_scalar(double2 a) {
+  double x = fabs(a.x), y = fabs(a.y);
+  if (isinf(x) || isinf(y)) return CUDART_INF;
+  if (isnan(x) || isnan(y)) return CUDART_NAN;
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  const double SCALE = 0x1p-600, LARGE = 0x1p+511, TINY = 0x1p-511, EPS = 0x1p-54;
+  if (ax > LARGE) {
+    if (ay <= __dmul_rn(ax, EPS)) return __dadd_rn(ax, ay);
+    return __ddiv_rn(hypot_glibc_kernel(__dmul_rn(ax, SCALE), __dmul_rn(ay, SCALE)), SCALE);
+  }
+  if (ay < TINY) {
+    if (ax >= __ddiv_rn(ay, EPS)) return __dadd_rn(ax, ay);
+    return __dmul_rn(hypot_glibc_kernel(__ddiv_rn(ax, SCALE), __ddiv_rn(ay, SCALE)), SCALE);
+  }
+  if (ay <= __dmul_rn(ax, EPS)) return __dadd_rn(ax, ay);
+  return hypot_glibc_kernel(ax, ay);
+}
+#else
+inline double cabs_(double2 a) { return std::hypot(a.x, a.y); }
+inline double cabs_scalar(double2 a) { return std::hypot(a.x, a.y); }
+#endif
 
 // Complex division with Smith's scaling (numpy's complex128 divide).
 SFFT_HD double2 cdiv(double2 a, double2 b) {

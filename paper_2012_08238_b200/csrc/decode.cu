@@ -363,7 +363,7 @@ __device__ double2 trimmed_mean_col(const double2* est, int64_t ld, int R) {
   const double2 med = np_join(mr, mi);
   int m = 0;
   for (int r = 0; r < R; ++r) {
-    dev[r] = hypot(re[r] - med.x, im[r] - med.y);
+    dev[r] = cabs_(cmk(re[r] - med.x, im[r] - med.y));
     if (!isnan(dev[r])) tmp[m++] = dev[r];
   }
   double spread = CUDART_NAN;

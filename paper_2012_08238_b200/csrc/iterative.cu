@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a) {
   a.f_ok[fi] = 0;
   const double2 y0 = ys[0];
   // _unwrap_position (frameworks.py:179-196): ladder[0] == 1
-  if (cabs_(y0) == 0.0) return;
+  if (cabs_scalar(y0) == 0.0) return;
   const double nd = (double)n;
   const double scl = -nd / (2.0 * 3.141592653589793);
   auto fmodpos = [&](double v, double m) {
@@ -250,14 +250,14 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a) {
   const int64_t lo = pmod((int64_t)b * L - L / 2, n);
   if (pmod(qi - lo, n) >= L) return;
   // ladder consistency
-  const double tol = fmax(3.0 * S.floor, 0.15 * cabs_(y0));
+  const double tol = fmax(3.0 * S.floor, 0.15 * cabs_scalar(y0));
   for (int j = 1; j < M; ++j) {
     const double2 pred = cmul(y0, unit_root(n, mulmod(a.ladder[j - 1] % n, qi, n)));
-    if (cabs_(csub(ys[j], pred)) > tol) return;
+    if (cabs_scalar(csub(ys[j], pred)) > tol) return;
   }
   const int64_t e = pmod((int64_t)b * L - qi, n);
   const double2 w = a.gt[(e % L) * B + e / L];
-  if (cabs_(w) < 0.05 * a.gmax[0]) return;
+  if (cabs_scalar(w) < 0.05 * a.gmax[0]) return;
   // mean of the dephased ladder values / w
   double2 sum = cmk(0.0, 0.0);
   for (int j = 0; j < M; ++j) {
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_correct(IterArgs a) {
       if (occ[bi] == 1) {
         const int64_t e = pmod(bi * L - m, n);
         w = a.gt[(e % L) * B + e / L];
-        mine = cabs_(w) >= wfloor;
+        mine = cabs_scalar(w) >= wfloor;
       }
     }
     double2 r[3];
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_correct(IterArgs a) {
       if (occ[bi] == 1) {
         const int64_t e = pmod(bi * L - m, n);
         const double2 w = a.gt[(e % L) * B + e / L];
-        if (cabs_(w) >= wfloor) {
+        if (cabs_scalar(w) >= wfloor) {
           rcw[t] = cadd(rcw[t], dl[t]);
           pend[t] = 0;
         }
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kFinNT) k_finalize(const int64_t* rec_pos,
   int off = block_exscan<kFinNT>(mine, redi, &tot);
   for (int t = t0; t < t1; ++t) {
     if (rc[t].x != 0.0 || rc[t].y != 0.0) {
-      k1[off] = ~dbits(cabs_(rc[t]));
+      k1[off] = ~dbits(cabs_scalar(rc[t]));
       k2[off] = rp[t];
       pay[off] = t;
       ++off;
@@ -629,8 +629,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
                   int P, int64_t k, int max_it, const int64_t* ladder, int nlad, int cap,
                   int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
-                  int32_t* out_conv, int64_t* out_samples, void* ws, size_t ws_bytes,
-                  cudaStream_t st) {
+                  int32_t* out_conv, int64_t* out_samples, int64_t* out_sched, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
   const int M = 1 + nlad;
   SFFT_REQUIRE(M <= kMaxShifts, "iterative: ladder too long");
   SFFT_REQUIRE(max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
@@ -771,6 +771,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   k_copy_ngroups<<<sb, 128, 0, st>>>(a.st, S, ngroups);
   k_union_count<<<S, kUnionNT, 0, st>>>(a.groups, ngroups, kMaxGroups, n, out_samples);
   SFFT_CHECK_LAUNCH("k_union_count");
+  if (out_sched) {
+    k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched);
+    SFFT_CHECK_LAUNCH("k_export_groups");
+  }
   return 0;
 }
 

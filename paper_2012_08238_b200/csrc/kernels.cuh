@@ -23,7 +23,22 @@ struct Prod {
   const int64_t* item_c;     // flat: b'*sigma mod n (null: 0)
   const int32_t* active;     // per-signal gate (null: all active)
   const double2* z;          // PROD_LOAD source [nitems][B]
+  unsigned long long* prof_items;  // profiling: count of non-skipped items (null: off)
 };
+
+// Profiling of the bucketization (gather-fold-FFT) launches: CUDA events on
+// the launching stream around every launch, items counted on the device.
+struct BucketProf {
+  bool on = false;
+  unsigned long long* d_items = nullptr;  // device counter
+  double ms = 0.0;
+  long long launches = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;  // read at prof_collect
+};
+BucketProf& bucket_prof();
+int prof_collect();
+int prof_begin(cudaStream_t st, cudaEvent_t* ev0);
+int prof_end(cudaStream_t st, cudaEvent_t ev0);
 
 
 size_t bucketize_ws_bytes(int64_t B, int64_t nitems);
@@ -77,7 +92,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
                   int P, int64_t k, int max_it, const int64_t* ladder, int nlad, int cap,
                   int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
-                  int32_t* out_conv, int64_t* out_samples, void* ws, size_t ws_bytes,
-                  cudaStream_t st);
+                  int32_t* out_conv, int64_t* out_samples, int64_t* out_sched, void* ws,
+                  size_t ws_bytes, cudaStream_t st);
 
 }  // namespace sfft

@@ -113,10 +113,33 @@ __device__ __forceinline__ int64_t group_elem(const Group& g, const GroupSh& gs,
   return 0;
 }
 
+constexpr int kSchedWords = 5 + kMaxShifts;  // kind, a, tau, cnt, nsh, sh[]
+
+// Export the groups as int64 records [S][kMaxGroups][kSchedWords].
+static __global__ void k_export_groups(const Group* __restrict__ groups, const int32_t* ngroups,
+                                int S, int64_t* out) {
+  const int s = blockIdx.x;
+  const int G = min(ngroups[s], kMaxGroups);
+  for (int g = threadIdx.x; g < kMaxGroups; g += blockDim.x) {
+    int64_t* o = out + ((int64_t)s * kMaxGroups + g) * kSchedWords;
+    if (g >= G) {
+      o[0] = -1;
+      continue;
+    }
+    const Group& q = groups[(int64_t)s * kMaxGroups + g];
+    o[0] = q.kind;
+    o[1] = q.a;
+    o[2] = q.tau;
+    o[3] = q.cnt;
+    o[4] = q.nsh;
+    for (int i = 0; i < kMaxShifts; ++i) o[5 + i] = i < q.nsh ? q.sh[i] : 0;
+  }
+}
+
 constexpr int kUnionNT = 512;
 
 // One CTA per signal: samples[s] = |union of the read sets of groups[s][0..ngroups[s])|.
-__global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __restrict__ groups,
+static __global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __restrict__ groups,
                                                           const int32_t* ngroups, int gstride,
                                                           int64_t n, int64_t* samples) {
   __shared__ Group sg[kMaxGroups];

@@ -135,6 +135,24 @@ class BatchResult:
     iterations: object
     converged: object
     samples_read: object
+    schedule: object = None   # int64 [S][groups][words] read schedule (see schedule_records)
+
+    def schedule_records(self, s: int) -> list:
+        """Read records of signal s in TimeSignal-log form."""
+        if self.schedule is None:
+            return []
+        out = []
+        for row in self.schedule[s].cpu().numpy():
+            kind = int(row[0])
+            if kind < 0:
+                break
+            a, tau, cnt, nsh = (int(v) for v in row[1:5])
+            if kind == 0:
+                for d in row[5:5 + nsh]:
+                    out.append(("flat", a, (tau + int(d)) % self.n, cnt))
+            else:
+                out.append(("spike", a, tau % self.n, cnt))
+        return out
 
     def to_results(self) -> list:
         pos = self.pos.cpu().numpy()
@@ -171,6 +189,14 @@ def draw_perms(n: int, seed: int, count: int):
         p = PermutationParams.random(n, rng)
         sig[i], tau[i] = p.sigma, p.tau
     return sig, tau
+
+
+def _sched_buffer(S, dev):
+    import ctypes
+    import torch
+    g, w = ctypes.c_int32(), ctypes.c_int32()
+    lib().sfft_schedule_layout(ctypes.byref(g), ctypes.byref(w))
+    return torch.empty((S, g.value, w.value), dtype=torch.int64, device=dev)
 
 
 def _as_batch(xs):
@@ -243,6 +269,7 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
     out_it = torch.zeros(S, dtype=torch.int32, device=dev)
     out_cv = torch.zeros(S, dtype=torch.int32, device=dev)
     out_sm = torch.zeros(S, dtype=torch.int64, device=dev)
+    sched = _sched_buffer(S, dev)
     L = lib()
     wsb = L.sfft_iterative_ws_bytes(n, b, S, M, cap)
     ws = _WS.get(wsb, dev)
@@ -254,8 +281,9 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
                                ptr(filt.gtable), ptr(gmax), ptr(twiddles(b, dev)), ptr(psig),
                                ptr(ptau), P, k, cfg.max_iterations, lad, len(ladder), cap,
                                ptr(out_pos), ptr(out_coef), ptr(out_n), ptr(out_it), ptr(out_cv),
-                               ptr(out_sm), ptr(ws), wsb, stream_of(dev)), "sfft_run_iterative")
-    return BatchResult(n, k, out_pos, out_coef, out_n, out_it, out_cv, out_sm)
+                               ptr(out_sm), ptr(sched), ptr(ws), wsb, stream_of(dev)),
+          "sfft_run_iterative")
+    return BatchResult(n, k, out_pos, out_coef, out_n, out_it, out_cv, out_sm, sched)
 
 
 def run_iterative(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
@@ -265,10 +293,15 @@ def run_iterative(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult
 
 
 def _single(batch_fn, x, k, cfg) -> RecoveryResult:
-    res = batch_fn(x, k, cfg).to_results()[0]
-    if isinstance(x, TimeSignal) and x._log:
-        # earlier reads of this signal count too (access counter only grows)
-        res.samples_read = max(res.samples_read, x.access_count)
+    br = batch_fn(x, k, cfg)
+    res = br.to_results()[0]
+    if isinstance(x, TimeSignal):
+        had = bool(x._log)
+        for rec in br.schedule_records(0):
+            x.record(rec)
+        if had:
+            # the access counter only grows: earlier reads of x count too
+            res.samples_read = x.access_count
     return res
 
 

