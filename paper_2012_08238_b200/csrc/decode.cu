@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
     const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
     const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
     const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
-    const int32_t* tcount, int64_t tstride, const int32_t* gate) {
+    const int32_t* tcount, int64_t tstride, const int32_t* gate, double2* __restrict__ part) {
   __shared__ int64_t s_row[kSubChunk];
   __shared__ int64_t s_q[kSubChunk];
   __shared__ double2 s_c[kSubChunk];
@@ -457,15 +457,22 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
   const int64_t L = n / B;
   const int64_t sg = sigma[item];
   const int64_t tt = tau_tot[item];
-  const int64_t T = tcount[sig];
-  const int64_t* tp = tpos + (int64_t)sig * tstride;
-  const double2* tc = tcoef + (int64_t)sig * tstride;
+  const int64_t Tall = tcount[sig];
+  // tone split z of gridDim.z: tones [tb, te); with one split the running
+  // value starts at y and the tones are subtracted in order (reference order)
+  const int TS = gridDim.z;
+  const int64_t per = (Tall + TS - 1) / TS;
+  const int64_t tb = (int64_t)blockIdx.z * per;
+  const int64_t te = (tb + per < Tall) ? tb + per : Tall;
+  const int64_t T = te > tb ? te - tb : 0;
+  const int64_t* tp = tpos + (int64_t)sig * tstride + tb;
+  const double2* tc = tcoef + (int64_t)sig * tstride + tb;
   int64_t bk = 0;
   double2 acc = cmk(0.0, 0.0);
   const bool live = i < nb;
   if (live) {
     bk = blist ? blist[(int64_t)item * nb + i] : i;
-    acc = y[(int64_t)item * B + bk];
+    if (TS == 1) acc = y[(int64_t)item * B + bk];
   }
   for (int64_t t0 = 0; t0 < T; t0 += kSubChunk) {
     __syncthreads();
@@ -487,19 +494,43 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
       }
     }
   }
-  if (live) out[(int64_t)item * nb + i] = acc;
+  if (!live) return;
+  if (TS == 1) out[(int64_t)item * nb + i] = acc;
+  else part[((int64_t)item * TS + blockIdx.z) * nb + i] = acc;
+}
+
+// out = y + sum of the (negated) split partial sums, in split order.
+__global__ void k_sub_reduce(const double2* __restrict__ y, double2* __restrict__ out, int64_t B,
+                             int64_t nb, const int32_t* blist, const int32_t* item_sig,
+                             const int32_t* gate, const double2* __restrict__ part, int TS) {
+  const int item = blockIdx.y;
+  const int sig = item_sig ? item_sig[item] : item;
+  if (gate && !gate[sig]) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const int64_t bk = blist ? blist[(int64_t)item * nb + i] : i;
+  double2 acc = cmk(0.0, 0.0);
+  for (int t = 0; t < TS; ++t) acc = cadd(acc, part[((int64_t)item * TS + t) * nb + i]);
+  out[(int64_t)item * nb + i] = cadd(y[(int64_t)item * B + bk], acc);
 }
 
 int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        const int32_t* blist, int64_t nitems, const double2* gt, int64_t n,
                        const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
                        const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
-                       int64_t tstride, const int32_t* gate, cudaStream_t st) {
+                       int64_t tstride, const int32_t* gate, cudaStream_t st, int TS,
+                       double2* part) {
   if (nitems <= 0 || nb <= 0) return 0;
-  dim3 g((unsigned)cdiv_up(nb, kSubNT), (unsigned)nitems);
+  if (TS < 1 || !part) TS = 1;
+  dim3 g((unsigned)cdiv_up(nb, kSubNT), (unsigned)nitems, (unsigned)TS);
   k_subtract<<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma, tau_tot, tpos,
-                                   tcoef, tcount, tstride, gate);
+                                   tcoef, tcount, tstride, gate, part);
   SFFT_CHECK_LAUNCH("k_subtract");
+  if (TS > 1) {
+    dim3 g2((unsigned)cdiv_up(nb, 256), (unsigned)nitems);
+    k_sub_reduce<<<g2, 256, 0, st>>>(y, out, B, nb, blist, item_sig, gate, part, TS);
+    SFFT_CHECK_LAUNCH("k_sub_reduce");
+  }
   return 0;
 }
 

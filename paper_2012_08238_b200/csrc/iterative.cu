@@ -16,6 +16,7 @@
 //   |y0 - model(found)| < 1.3 floor ?                            (k_subtract, k_it_resid)
 #include "kernels.cuh"
 #include "schedule.cuh"
+#include "finalize.cuh"
 
 namespace sfft {
 
@@ -66,7 +67,44 @@ struct IterArgs {
   int32_t* pend;                 // [S][cap] polish pending flags
   double2* delta;                // [S][cap] polish corrections
   Group* groups;                 // [S][kMaxGroups]
+  int32_t* stats;                // [4]: n_active, max recovered, max heavy, spare
+  int64_t* ht_key;               // [S][HT] recovered-position hash (key f+1, 0 empty)
+  int32_t* ht_val;               // [S][HT] index into rec_*
+  int HT;                        // power of two >= 2*cap
+  double2* part;                 // tone-split partial sums (subtract / ladder)
 };
+
+__device__ __forceinline__ uint32_t ht_slot(int64_t f, int HT) {
+  return (uint32_t)(((unsigned long long)(f + 1) * 0x9E3779B97F4A7C15ull) >> 40) & (HT - 1);
+}
+
+// index of f in the recovered list of signal s, or -1
+__device__ __forceinline__ int ht_find(const IterArgs& a, int s, int64_t f) {
+  const int64_t* keys = a.ht_key + (int64_t)s * a.HT;
+  const int32_t* vals = a.ht_val + (int64_t)s * a.HT;
+  uint32_t h = ht_slot(f, a.HT);
+  for (int probe = 0; probe < a.HT; ++probe) {
+    const int64_t k = keys[h];
+    if (k == f + 1) return vals[h];
+    if (k == 0) return -1;
+    h = (h + 1) & (a.HT - 1);
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void ht_insert(const IterArgs& a, int s, int64_t f, int idx) {
+  unsigned long long* keys = (unsigned long long*)(a.ht_key + (int64_t)s * a.HT);
+  int32_t* vals = a.ht_val + (int64_t)s * a.HT;
+  uint32_t h = ht_slot(f, a.HT);
+  for (int probe = 0; probe < a.HT; ++probe) {
+    const unsigned long long old = atomicCAS(&keys[h], 0ull, (unsigned long long)(f + 1));
+    if (old == 0ull || old == (unsigned long long)(f + 1)) {
+      vals[h] = idx;
+      return;
+    }
+    h = (h + 1) & (a.HT - 1);
+  }
+}
 
 // ------------------------------------------------------------------ items
 __global__ void k_it_items(IterArgs a, int p, int nsh, const int64_t* shifts_dev,
@@ -163,16 +201,87 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a, int it) {
     block_bitonic<kDecNT>(k1, k2, pay, total, cap);
     for (int i = threadIdx.x; i < total; i += kDecNT) hv[i] = pay[i];
   }
-  if (threadIdx.x == 0) S.nheavy = total;
+  if (threadIdx.x == 0) {
+    S.nheavy = total;
+    atomicMax(a.stats + 2, total);
+  }
 }
 
 // ------------------------------------------------------------------ locate
 constexpr int kLocNT = 128;
 constexpr int kLocChunk = 32;
 
+// Sum of the recovered model over tones [tb, te) at heavy bucket b for the
+// ladder shifts j = 1..M-1, subtracted from ys[] (running, in tone order).
+__device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bool live,
+                                             int64_t tb, int64_t te, double2* ys,
+                                             int64_t (*t_row), int64_t (*t_q), double2* t_c,
+                                             double2 (*t_ph)[kMaxShifts]) {
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int M = a.M;
+  const int64_t sigma = a.item_sigma[s];
+  const int64_t tau = a.item_tau[s];
+  const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  const double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  for (int64_t t0 = tb; t0 < te; t0 += kLocChunk) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < kLocChunk * M; q += kLocNT) {
+      const int tt = q / M, j = q - tt * M;
+      if (t0 + tt >= te || j == 0) continue;
+      const int64_t m = mulmod(sigma, pmod(rp[t0 + tt], n), n);
+      const int64_t tj = pmod(tau + a.ladder[j - 1], n);
+      t_ph[tt][j] = unit_root(n, mulmod(tj, m, n));
+      if (j == 1) {
+        t_row[tt] = (L - m % L) % L;
+        t_q[tt] = (m + L - 1) / L;
+        t_c[tt] = rc[t0 + tt];
+      }
+    }
+    __syncthreads();
+    if (live) {
+      const int tn = (int)((te - t0 < kLocChunk) ? te - t0 : kLocChunk);
+      for (int tt = 0; tt < tn; ++tt) {
+        int64_t col = b - t_q[tt];
+        col += (col < 0) ? B : 0;
+        const double2 cw = cmul(t_c[tt], __ldg(a.gt + t_row[tt] * B + col));
+        for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cmul(cw, t_ph[tt][j]));
+      }
+    }
+  }
+}
+
+// Tone-split partial ladder sums for large recovered lists:
+// part[s][z][h][j-1] = -sum_{tones of split z} c w ph_j.
+__global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
+  __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
+  __shared__ double2 t_c[kLocChunk];
+  __shared__ double2 t_ph[kLocChunk][kMaxShifts];
+  const int s = blockIdx.y;
+  if (!a.active[s]) return;
+  const int nh = a.st[s].nheavy;
+  const int h0 = blockIdx.x * kLocNT;
+  if (h0 >= nh) return;
+  const int h = h0 + threadIdx.x;
+  const bool live = h < nh;
+  const int TS = gridDim.z;
+  const int64_t T = a.rec_count[s];
+  const int64_t per = (T + TS - 1) / TS;
+  const int64_t tb = (int64_t)blockIdx.z * per;
+  const int64_t te = (tb + per < T) ? tb + per : T;
+  const int b = live ? a.heavy[(int64_t)s * a.B + h] : 0;
+  double2 ys[kMaxShifts];
+  for (int j = 0; j < a.M; ++j) ys[j] = cmk(0.0, 0.0);
+  ladder_model(a, s, b, live, tb, te, ys, t_row, t_q, t_c, t_ph);
+  if (!live) return;
+  double2* o = a.part + (((int64_t)s * TS + blockIdx.z) * a.B + h) * (a.M - 1);
+  for (int j = 1; j < a.M; ++j) o[j - 1] = ys[j];
+}
+
 // Ladder values at heavy buckets minus the recovered model, phase unwrap,
 // passband / consistency / weight checks, coefficient (frameworks.py:493-516).
-__global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a) {
+// TS == 0: the model is subtracted here in tone order; TS > 0: summed from
+// k_it_ladder_part's splits.
+__global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
   __shared__ double2 t_ph[kLocChunk][kMaxShifts];
@@ -192,33 +301,12 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a) {
   double2 ys[kMaxShifts];
   ys[0] = a.y[(int64_t)s * B + b];
   for (int j = 1; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
-  // subtract the recovered model from the ladder values (y0 already clean)
-  const int T = a.rec_count[s];
-  const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
-  const double2* rc = a.rec_coef + (int64_t)s * a.cap;
-  for (int t0 = 0; t0 < T; t0 += kLocChunk) {
-    __syncthreads();
-    for (int q = threadIdx.x; q < kLocChunk * M; q += kLocNT) {
-      const int tt = q / M, j = q - tt * M;
-      if (t0 + tt >= T || j == 0) continue;
-      const int64_t m = mulmod(sigma, pmod(rp[t0 + tt], n), n);
-      const int64_t tj = pmod(tau + a.ladder[j - 1], n);
-      t_ph[tt][j] = unit_root(n, mulmod(tj, m, n));
-      if (j == 1) {
-        t_row[tt] = (L - m % L) % L;
-        t_q[tt] = (m + L - 1) / L;
-        t_c[tt] = rc[t0 + tt];
-      }
-    }
-    __syncthreads();
-    if (live) {
-      const int tn = min(kLocChunk, T - t0);
-      for (int tt = 0; tt < tn; ++tt) {
-        int64_t col = b - t_q[tt];
-        col += (col < 0) ? B : 0;
-        const double2 cw = cmul(t_c[tt], __ldg(a.gt + t_row[tt] * B + col));
-        for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cmul(cw, t_ph[tt][j]));
-      }
+  if (TS == 0) {
+    ladder_model(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_c, t_ph);
+  } else if (live) {
+    for (int z = 0; z < TS; ++z) {
+      const double2* p = a.part + (((int64_t)s * TS + z) * B + h) * (M - 1);
+      for (int j = 1; j < M; ++j) ys[j] = cadd(ys[j], p[j - 1]);
     }
   }
   if (!live) return;
@@ -275,6 +363,9 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a) {
 // ------------------------------------------------------------------ merge
 constexpr int kMrgNT = 512;
 
+// recovered[f] += c for every tone found now, new positions appended in
+// heavy order (dict insertion order, frameworks.py:556-557); lookups through a
+// per-signal open-addressing hash of the recovered positions.
 __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
   __shared__ int redi[32];
   const int s = blockIdx.x;
@@ -294,9 +385,7 @@ __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
   for (int h = h0; h < h1; ++h) {
     if (!fok[h]) continue;
     ++nok;
-    bool exists = false;
-    for (int t = 0; t < n_old && !exists; ++t) exists = rp[t] == fp[h];
-    nnew += !exists;
+    nnew += ht_find(a, s, fp[h]) < 0;
   }
   int tot_new, tot_ok;
   int off_new = block_exscan<kMrgNT>(nnew, redi, &tot_new);
@@ -308,9 +397,7 @@ __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
     cp[off_ok] = fp[h];
     cc[off_ok] = fcf[h];
     ++off_ok;
-    int where = -1;
-    for (int t = 0; t < n_old && where < 0; ++t)
-      if (rp[t] == fp[h]) where = t;
+    const int where = ht_find(a, s, fp[h]);
     if (where >= 0) {
       rc[where] = cadd(rc[where], fcf[h]);
     } else if (n_old + off_new < a.cap) {
@@ -319,7 +406,12 @@ __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
       ++off_new;
     }
   }
-  __syncthreads();
+  __syncthreads();  // all lookups of this iteration precede the inserts
+  {
+    // insert the appended positions
+    const int nrec = min(a.cap, n_old + tot_new);
+    for (int t = n_old + threadIdx.x; t < nrec; t += kMrgNT) ht_insert(a, s, rp[t], t);
+  }
   if (threadIdx.x == 0) {
     const int nrec = min(a.cap, n_old + tot_new);
     a.rec_count[s] = nrec;
@@ -327,6 +419,7 @@ __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
     S.nfound = tot_ok;
     a.fc_count[s] = tot_ok;
     a.gate[s] = (nrec >= a.k && tot_ok > 0) ? 1 : 0;
+    atomicMax(a.stats + 1, nrec);
   }
 }
 
@@ -509,58 +602,6 @@ __global__ void __launch_bounds__(kPoNT) k_po_correct(IterArgs a) {
   if (threadIdx.x == 0) a.st[s].pending -= tot;
 }
 
-// ------------------------------------------------------------------ finalize
-constexpr int kFinNT = 512;
-
-// entries with c != 0, top k by (-|c|, f) (sfft/frameworks.py:151-155).
-__global__ void __launch_bounds__(kFinNT) k_finalize(const int64_t* rec_pos,
-                                                     const double2* rec_coef,
-                                                     const int32_t* rec_count, int cap,
-                                                     int64_t k, int64_t* out_pos,
-                                                     double2* out_coef, int32_t* out_n,
-                                                     int32_t* overflow) {
-  extern __shared__ unsigned char fsm[];
-  const int s = blockIdx.x;
-  const int T = rec_count[s];
-  const int64_t* rp = rec_pos + (int64_t)s * cap;
-  const double2* rc = rec_coef + (int64_t)s * cap;
-  unsigned long long* k1 = (unsigned long long*)fsm;
-  long long* k2 = (long long*)(k1 + kFusedMaxB);
-  int* pay = (int*)(k2 + kFusedMaxB);
-  if (T > kFusedMaxB) {
-    if (threadIdx.x == 0) {
-      overflow[0] = 1;
-      out_n[s] = 0;
-    }
-    return;
-  }
-  __shared__ int redi[32];
-  int mine = 0;
-  const int per = (T + kFinNT - 1) / kFinNT;
-  const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
-  for (int t = t0; t < t1; ++t) mine += (rc[t].x != 0.0 || rc[t].y != 0.0);
-  int tot;
-  int off = block_exscan<kFinNT>(mine, redi, &tot);
-  for (int t = t0; t < t1; ++t) {
-    if (rc[t].x != 0.0 || rc[t].y != 0.0) {
-      k1[off] = ~dbits(cabs_scalar(rc[t]));
-      k2[off] = rp[t];
-      pay[off] = t;
-      ++off;
-    }
-  }
-  __syncthreads();
-  int capp = 1;
-  while (capp < tot) capp <<= 1;
-  block_bitonic<kFinNT>(k1, k2, pay, tot, capp);
-  const int kk = (int)(k < (int64_t)tot ? k : (int64_t)tot);
-  for (int i = threadIdx.x; i < kk; i += kFinNT) {
-    out_pos[(int64_t)s * k + i] = rp[pay[i]];
-    out_coef[(int64_t)s * k + i] = rc[pay[i]];
-  }
-  if (threadIdx.x == 0) out_n[s] = kk;
-}
-
 // ------------------------------------------------------------------ host driver
 
 struct IterLayout {
@@ -570,14 +611,25 @@ struct IterLayout {
 
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+constexpr int kMaxSubSplit = 16;   // tone splits of the full-B subtraction
+constexpr int kMaxLadSplit = 4;    // tone splits of the ladder model
+
+static int ht_size(int cap) {
+  int h = 1;
+  while (h < 2 * cap) h <<= 1;
+  return h;
+}
+
 static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
   IterLayout L{};
   size_t o = 0;
+  const size_t HT = (size_t)ht_size(cap);
+  const size_t part = std::max((size_t)kMaxSubSplit * B, (size_t)kMaxLadSplit * B * (M - 1));
   size_t sizes[] = {
       sizeof(IterState) * S,                 // 0 st
       sizeof(int32_t) * S,                   // 1 active
       sizeof(int32_t) * S,                   // 2 gate
-      sizeof(int32_t) * 4,                   // 3 n_active + overflow
+      sizeof(int32_t) * 8,                   // 3 stats
       sizeof(int32_t) * M * S,               // 4 item_sig
       sizeof(int64_t) * M * S,               // 5 item_sigma
       sizeof(int64_t) * M * S,               // 6 item_tau
@@ -598,6 +650,9 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(Group) * (size_t)S * kMaxGroups,// 21 groups
       sizeof(int64_t) * 3,                   // 22 shifts (polish)
       sizeof(int32_t) * S,                   // 23 ngroups copy
+      sizeof(int64_t) * (size_t)S * HT,      // 24 ht_key
+      sizeof(int32_t) * (size_t)S * HT,      // 25 ht_val
+      sizeof(double2) * (size_t)S * part,    // 26 part
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -624,6 +679,11 @@ __global__ void k_it_outputs(const IterState* st, int S, int32_t* iters, int32_t
   conv[s] = st[s].converged;
 }
 
+static int splits(int T, int per, int mx) {
+  const int z = (T + per - 1) / per;
+  return z < 1 ? 1 : (z > mx ? mx : z);
+}
+
 int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
                   const double* taps, int64_t omega, int64_t B, const double2* gt,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
@@ -635,6 +695,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   SFFT_REQUIRE(M <= kMaxShifts, "iterative: ladder too long");
   SFFT_REQUIRE(max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
   SFFT_REQUIRE(P >= max_it + 6, "iterative: need max_iterations + 6 permutations");
+  SFFT_REQUIRE(k <= kFusedMaxB, "iterative: k must be <= 8192");
   SFFT_REQUIRE(ws_bytes >= iterative_ws_bytes(n, B, S, M, cap), "iterative: workspace too small");
   const IterLayout Lo = iter_layout(n, B, S, M, cap);
   char* w = (char*)ws;
@@ -657,8 +718,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   a.st = (IterState*)(w + Lo.off[0]);
   a.active = (int32_t*)(w + Lo.off[1]);
   a.gate = (int32_t*)(w + Lo.off[2]);
-  a.n_active = (int32_t*)(w + Lo.off[3]);
-  int32_t* overflow = a.n_active + 1;
+  a.stats = (int32_t*)(w + Lo.off[3]);
+  a.n_active = a.stats;
   a.item_sig = (int32_t*)(w + Lo.off[4]);
   a.item_sigma = (int64_t*)(w + Lo.off[5]);
   a.item_tau = (int64_t*)(w + Lo.off[6]);
@@ -679,13 +740,18 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   a.groups = (Group*)(w + Lo.off[21]);
   int64_t* po_shifts = (int64_t*)(w + Lo.off[22]);
   int32_t* ngroups = (int32_t*)(w + Lo.off[23]);
+  a.HT = ht_size(cap);
+  a.ht_key = (int64_t*)(w + Lo.off[24]);
+  a.ht_val = (int32_t*)(w + Lo.off[25]);
+  a.part = (double2*)(w + Lo.off[26]);
   void* bws = w + Lo.total;
   const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
 
   // state init
   SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
   SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
-  SFFT_CUDA(cudaMemsetAsync(a.n_active, 0, sizeof(int32_t) * 4, st));
+  SFFT_CUDA(cudaMemsetAsync(a.stats, 0, sizeof(int32_t) * 8, st));
+  SFFT_CUDA(cudaMemsetAsync(a.ht_key, 0, sizeof(int64_t) * (size_t)S * a.HT, st));
   {
     std::vector<int32_t> ones(S, 1);
     SFFT_CUDA(cudaMemcpyAsync(a.active, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st));
@@ -693,7 +759,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
     SFFT_CUDA(cudaMemcpyAsync(a.n_active, &na, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     const int64_t ps[3] = {0, 1, 2};
     SFFT_CUDA(cudaMemcpyAsync(po_shifts, ps, sizeof(ps), cudaMemcpyHostToDevice, st));
-    SFFT_CUDA(cudaStreamSynchronize(st));  // host vectors above are stack-owned
+    SFFT_CUDA(cudaStreamSynchronize(st));  // host sources above are stack-owned
   }
 
   Prod p{};
@@ -717,32 +783,44 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
                                  (int)std::max<size_t>(occ_sm, 1)));
 
   const unsigned sb = (unsigned)cdiv_up(S, 128);
+  int t_max = 0;  // largest recovered list (host copy, refreshed every iteration)
+  int h_max = 0;  // largest heavy list so far
   for (int it = 1; it <= max_it; ++it) {
     k_it_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a, it - 1, M, nullptr, false);
     SFFT_CHECK_LAUNCH("k_it_items");
     int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
     if (rc) return rc;
-    // y0 -= model(recovered), all buckets
+    // y0 -= model(recovered), all buckets (tone-split when the lists are long)
     rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
-                            a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st);
+                            a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st,
+                            splits(t_max, 512, kMaxSubSplit), a.part);
     if (rc) return rc;
     k_it_decide<<<S, kDecNT, dsm, st>>>(a, it);
     SFFT_CHECK_LAUNCH("k_it_decide");
     dim3 gl((unsigned)cdiv_up(B, kLocNT), S);
-    k_it_locate<<<gl, kLocNT, 0, st>>>(a);
+    const int lts = t_max > 512 ? splits(t_max, 512, kMaxLadSplit) : 0;
+    if (lts) {
+      dim3 gp((unsigned)cdiv_up(B, kLocNT), S, lts);
+      k_it_ladder_part<<<gp, kLocNT, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_it_ladder_part");
+    }
+    k_it_locate<<<gl, kLocNT, 0, st>>>(a, lts);
     SFFT_CHECK_LAUNCH("k_it_locate");
     k_it_merge<<<S, kMrgNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_merge");
     // residual of y0 after the tones found now (only where gate[s])
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
-                            a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st);
+                            a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
+                            splits(h_max, 512, kMaxSubSplit), a.part);
     if (rc) return rc;
     k_it_resid<<<S, kDecNT, 0, st>>>(a, it);
     SFFT_CHECK_LAUNCH("k_it_resid");
-    int32_t na = 0;
-    SFFT_CUDA(cudaMemcpyAsync(&na, a.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    int32_t hs[4] = {0, 0, 0, 0};
+    SFFT_CUDA(cudaMemcpyAsync(hs, a.stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
     SFFT_CUDA(cudaStreamSynchronize(st));
-    if (na <= 0) break;
+    t_max = hs[1];
+    h_max = hs[2];
+    if (hs[0] <= 0) break;
   }
 
   // polish (2 epochs x <= 3 passes x shifts 0,1,2)
@@ -754,9 +832,11 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
     SFFT_CHECK_LAUNCH("k_po_epoch");
     for (int pass = 0; pass < 3; ++pass) {
       k_po_gate<<<sb, 128, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_po_gate");
       k_it_items<<<(unsigned)cdiv_up((int64_t)3 * S, 256), 256, 0, st>>>(a, 0, 3, po_shifts, true);
       SFFT_CHECK_LAUNCH("k_it_items(polish)");
       k_po_log<<<sb, 128, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_po_log");
       int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)3 * S, W, a.y, bws, bws_bytes, st);
       if (rc) return rc;
       k_po_correct<<<S, kPoNT, occ_sm, st>>>(a);
@@ -765,12 +845,14 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   }
 
   k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
-                                      out_coef, out_n, overflow);
+                                      out_coef, out_n);
   SFFT_CHECK_LAUNCH("k_finalize");
   k_it_outputs<<<sb, 128, 0, st>>>(a.st, S, out_iters, out_conv);
+  SFFT_CHECK_LAUNCH("k_it_outputs");
   k_copy_ngroups<<<sb, 128, 0, st>>>(a.st, S, ngroups);
-  k_union_count<<<S, kUnionNT, 0, st>>>(a.groups, ngroups, kMaxGroups, n, out_samples);
-  SFFT_CHECK_LAUNCH("k_union_count");
+  SFFT_CHECK_LAUNCH("k_copy_ngroups");
+  int rc = run_union_count(a.groups, ngroups, S, n, out_samples, st);
+  if (rc) return rc;
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched);
     SFFT_CHECK_LAUNCH("k_export_groups");

@@ -83,7 +83,8 @@ int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        const int32_t* blist, int64_t nitems, const double2* gt, int64_t n,
                        const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
                        const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
-                       int64_t tstride, const int32_t* gate, cudaStream_t st);
+                       int64_t tstride, const int32_t* gate, cudaStream_t st, int TS = 1,
+                       double2* part = nullptr);
 
 // iterative.cu
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap);

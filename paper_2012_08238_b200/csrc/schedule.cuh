@@ -174,3 +174,69 @@ static __global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __
 }
 
 }  // namespace sfft
+
+namespace sfft {
+
+// Multi-CTA variant: grid (chunks, S); the element space of all groups is cut
+// into gridDim.x ranges; counts are accumulated with integer atomics into
+// samples[s] (zeroed by the caller), so the result is exact and deterministic.
+static __global__ void __launch_bounds__(kUnionNT) k_union_count_mc(
+    const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
+    unsigned long long* samples) {
+  __shared__ Group sg[kMaxGroups];
+  __shared__ GroupSh sp[kMaxGroups];
+  __shared__ int64_t gstart[kMaxGroups + 1];
+  __shared__ unsigned long long red[32];
+  const int s = blockIdx.y;
+  const int G = min(ngroups[s], kMaxGroups);
+  const Group* gs = groups + (int64_t)s * gstride;
+  for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += kUnionNT) merge_pieces(sg[i], n, &sp[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int g = 0; g < G; ++g) {
+      gstart[g] = acc;
+      acc += sp[g].total;
+    }
+    gstart[G] = acc;
+  }
+  __syncthreads();
+  const int64_t all = gstart[G];
+  const int64_t per = (all + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = (int64_t)blockIdx.x * per;
+  const int64_t c1 = min(all, c0 + per);
+  unsigned long long cnt = 0;
+  for (int g = 0; g < G; ++g) {
+    const int64_t lo = max(c0, gstart[g]), hi = min(c1, gstart[g + 1]);
+    for (int64_t j = lo + threadIdx.x; j < hi; j += kUnionNT) {
+      const int64_t e = group_elem(sg[g], sp[g], n, j - gstart[g]);
+      bool fresh = true;
+      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e);
+      cnt += fresh;
+    }
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < kUnionNT / 32; ++i) t += red[i];
+    if (t) atomicAdd(samples + s, t);
+  }
+}
+
+// samples[s] = |union of read sets| for every signal (exact, multi-CTA).
+inline int run_union_count(const Group* groups, const int32_t* ngroups, int S, int64_t n,
+                           int64_t* samples, cudaStream_t st, int chunks = 48) {
+  SFFT_CUDA(cudaMemsetAsync(samples, 0, sizeof(int64_t) * S, st));
+  dim3 g(chunks, S);
+  k_union_count_mc<<<g, kUnionNT, 0, st>>>(groups, ngroups, kMaxGroups, n,
+                                           (unsigned long long*)samples);
+  SFFT_CHECK_LAUNCH("k_union_count_mc");
+  return 0;
+}
+
+}  // namespace sfft
