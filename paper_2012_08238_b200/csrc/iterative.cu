@@ -502,104 +502,104 @@ __global__ void k_po_log(IterArgs a) {
   S.cursor += 1;
 }
 
-constexpr int kPoNT = 256;
+constexpr int kPoNT = 64;
 constexpr int kPoChunk = 128;
 
-// One pass of _polish_flat_estimates for one signal (frameworks.py:590-608):
-// occupancy of every recovered tone's bucket, then each pending, non-collided
-// tone with a usable weight gets mean_t(resid_t[b] w^{-(tau+t)m}) / w.
-__global__ void __launch_bounds__(kPoNT) k_po_correct(IterArgs a) {
-  extern __shared__ int occ[];
+// Occupancy of the buckets of every recovered tone under this pass's
+// permutation (frameworks.py:596-598).  occ zeroed by the caller.
+__global__ void k_po_occ(IterArgs a, int32_t* occ) {
+  const int s = blockIdx.y;
+  if (!a.gate[s]) return;
+  const int T = a.rec_count[s];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int64_t n = a.n, L = a.L;
+  const int64_t m = mulmod(a.item_sigma[s], pmod(a.rec_pos[(int64_t)s * a.cap + t], n), n);
+  atomicAdd(&occ[(int64_t)s * a.B + pmod(m + L / 2, n) / L], 1);
+}
+
+// Correction of every pending, non-collided tone with a usable weight:
+// mean_t(resid_t[b] * w^{-(tau+t)m}) / w, resid_t = y_t - model(all recovered)
+// at the tone's own bucket, with the pre-pass coefficients (frameworks.py:599-608).
+__global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* occ,
+                                                    int32_t* corr) {
   __shared__ int64_t u_row[kPoChunk], u_q[kPoChunk];
   __shared__ double2 u_c[kPoChunk];
   __shared__ double2 u_ph[kPoChunk][3];
-  __shared__ int redi[32];
-  const int s = blockIdx.x;
+  const int s = blockIdx.y;
   if (!a.gate[s]) return;
   const int64_t n = a.n, B = a.B, L = a.L;
   const int T = a.rec_count[s];
+  const int t = blockIdx.x * kPoNT + threadIdx.x;
+  if (blockIdx.x * kPoNT >= T) return;
   const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
   const double2* rc = a.rec_coef + (int64_t)s * a.cap;
-  int32_t* pend = a.pend + (int64_t)s * a.cap;
-  double2* dl = a.delta + (int64_t)s * a.cap;
   const int64_t sigma = a.item_sigma[s];
   const int64_t tau = a.item_tau[s];
-  for (int64_t i = threadIdx.x; i < B; i += kPoNT) occ[i] = 0;
-  __syncthreads();
-  for (int t = threadIdx.x; t < T; t += kPoNT) {
-    const int64_t m = mulmod(sigma, pmod(rp[t], n), n);
-    atomicAdd(&occ[pmod(m + L / 2, n) / L], 1);
+  bool mine = false;
+  int64_t m = 0, bi = 0;
+  double2 w = cmk(0.0, 0.0);
+  if (t < T && a.pend[(int64_t)s * a.cap + t]) {
+    m = mulmod(sigma, pmod(rp[t], n), n);
+    bi = pmod(m + L / 2, n) / L;
+    if (occ[(int64_t)s * B + bi] == 1) {
+      const int64_t e = pmod(bi * L - m, n);
+      w = a.gt[(e % L) * B + e / L];
+      mine = cabs_scalar(w) >= 0.05 * a.gmax[0];
+    }
   }
-  __syncthreads();
-  const double wfloor = 0.05 * a.gmax[0];
-  int corrected = 0;
-  for (int base = 0; base < T; base += kPoNT) {
-    const int t = base + threadIdx.x;
-    bool mine = false;
-    int64_t m = 0, bi = 0;
-    double2 w = cmk(0.0, 0.0);
-    if (t < T && pend[t]) {
-      m = mulmod(sigma, pmod(rp[t], n), n);
-      bi = pmod(m + L / 2, n) / L;
-      if (occ[bi] == 1) {
-        const int64_t e = pmod(bi * L - m, n);
-        w = a.gt[(e % L) * B + e / L];
-        mine = cabs_scalar(w) >= wfloor;
-      }
+  if (t < T) corr[(int64_t)s * a.cap + t] = mine;
+  double2 r[3];
+  for (int d = 0; d < 3; ++d) r[d] = mine ? a.y[((int64_t)d * a.S + s) * B + bi] : cmk(0, 0);
+  for (int u0 = 0; u0 < T; u0 += kPoChunk) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < kPoChunk; q += kPoNT) {
+      if (u0 + q >= T) continue;
+      const int64_t mu = mulmod(sigma, pmod(rp[u0 + q], n), n);
+      u_row[q] = (L - mu % L) % L;
+      u_q[q] = (mu + L - 1) / L;
+      u_c[q] = rc[u0 + q];
+      for (int d = 0; d < 3; ++d) u_ph[q][d] = unit_root(n, mulmod(pmod(tau + d, n), mu, n));
     }
-    double2 r[3];
-    for (int d = 0; d < 3; ++d) r[d] = mine ? a.y[((int64_t)d * a.S + s) * B + bi] : cmk(0, 0);
-    for (int u0 = 0; u0 < T; u0 += kPoChunk) {
-      __syncthreads();
-      for (int q = threadIdx.x; q < kPoChunk; q += kPoNT) {
-        if (u0 + q >= T) continue;
-        const int64_t mu = mulmod(sigma, pmod(rp[u0 + q], n), n);
-        u_row[q] = (L - mu % L) % L;
-        u_q[q] = (mu + L - 1) / L;
-        u_c[q] = rc[u0 + q];
-        for (int d = 0; d < 3; ++d) u_ph[q][d] = unit_root(n, mulmod(pmod(tau + d, n), mu, n));
-      }
-      __syncthreads();
-      if (mine) {
-        const int un = min(kPoChunk, T - u0);
-        for (int q = 0; q < un; ++q) {
-          int64_t col = bi - u_q[q];
-          col += (col < 0) ? B : 0;
-          const double2 cw = cmul(u_c[q], __ldg(a.gt + u_row[q] * B + col));
-          for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q][d]));
-        }
-      }
-    }
+    __syncthreads();
     if (mine) {
-      double2 acc = cmk(0.0, 0.0);
-      for (int d = 0; d < 3; ++d) {
-        const int64_t ex = pmod(-mulmod(pmod(tau + d, n), m, n), n);
-        acc = cadd(acc, cmul(r[d], unit_root(n, ex)));
+      const int un = min(kPoChunk, T - u0);
+#pragma unroll 4
+      for (int q = 0; q < un; ++q) {
+        int64_t col = bi - u_q[q];
+        col += (col < 0) ? B : 0;
+        const double2 cw = cmul(u_c[q], __ldg(a.gt + u_row[q] * B + col));
+        for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q][d]));
       }
-      dl[t] = cdiv(cdivr(acc, 3.0), w);
-      ++corrected;
     }
+  }
+  if (mine) {
+    double2 acc = cmk(0.0, 0.0);
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ex = pmod(-mulmod(pmod(tau + d, n), m, n), n);
+      acc = cadd(acc, cmul(r[d], unit_root(n, ex)));
+    }
+    a.delta[(int64_t)s * a.cap + t] = cdiv(cdivr(acc, 3.0), w);
+  }
+}
+
+// Apply after every residual has been formed with the pre-pass coefficients.
+__global__ void k_po_apply(IterArgs a, const int32_t* corr) {
+  __shared__ int cnt;
+  const int s = blockIdx.y;
+  if (!a.gate[s]) return;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const int T = a.rec_count[s];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T && corr[(int64_t)s * a.cap + t]) {
+    const int64_t i = (int64_t)s * a.cap + t;
+    a.rec_coef[i] = cadd(a.rec_coef[i], a.delta[i]);
+    a.pend[i] = 0;
+    atomicAdd(&cnt, 1);
   }
   __syncthreads();
-  // apply after every residual has been formed with the pre-pass coefficients
-  double2* rcw = a.rec_coef + (int64_t)s * a.cap;
-  for (int base = 0; base < T; base += kPoNT) {
-    const int t = base + threadIdx.x;
-    if (t < T && pend[t]) {
-      const int64_t m = mulmod(sigma, pmod(rp[t], n), n);
-      const int64_t bi = pmod(m + L / 2, n) / L;
-      if (occ[bi] == 1) {
-        const int64_t e = pmod(bi * L - m, n);
-        const double2 w = a.gt[(e % L) * B + e / L];
-        if (cabs_scalar(w) >= wfloor) {
-          rcw[t] = cadd(rcw[t], dl[t]);
-          pend[t] = 0;
-        }
-      }
-    }
-  }
-  const int tot = block_sum_int<kPoNT>(corrected, redi);
-  if (threadIdx.x == 0) a.st[s].pending -= tot;
+  if (threadIdx.x == 0 && cnt) atomicSub(&a.st[s].pending, cnt);
 }
 
 // ------------------------------------------------------------------ host driver
@@ -612,7 +612,7 @@ struct IterLayout {
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 constexpr int kMaxSubSplit = 16;   // tone splits of the full-B subtraction
-constexpr int kMaxLadSplit = 4;    // tone splits of the ladder model
+constexpr int kMaxLadSplit = 16;   // tone splits of the ladder model
 
 static int ht_size(int cap) {
   int h = 1;
@@ -653,6 +653,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int64_t) * (size_t)S * HT,      // 24 ht_key
       sizeof(int32_t) * (size_t)S * HT,      // 25 ht_val
       sizeof(double2) * (size_t)S * part,    // 26 part
+      sizeof(int32_t) * (size_t)S * B,       // 27 occ (polish)
+      sizeof(int32_t) * (size_t)S * cap,     // 28 corr (polish)
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -777,10 +779,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   const size_t dsm = (size_t)kFusedMaxB * (8 + 8 + 4);
   SFFT_CUDA(cudaFuncSetAttribute(k_it_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   SFFT_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  const size_t occ_sm = (size_t)B * sizeof(int);
-  SFFT_REQUIRE(occ_sm <= 160 * 1024, "iterative: B too large for the polish occupancy table");
-  SFFT_CUDA(cudaFuncSetAttribute(k_po_correct, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(occ_sm, 1)));
+  int32_t* occ = (int32_t*)(w + Lo.off[27]);
+  int32_t* corr = (int32_t*)(w + Lo.off[28]);
 
   const unsigned sb = (unsigned)cdiv_up(S, 128);
   int t_max = 0;  // largest recovered list (host copy, refreshed every iteration)
@@ -798,7 +798,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
     k_it_decide<<<S, kDecNT, dsm, st>>>(a, it);
     SFFT_CHECK_LAUNCH("k_it_decide");
     dim3 gl((unsigned)cdiv_up(B, kLocNT), S);
-    const int lts = t_max > 512 ? splits(t_max, 512, kMaxLadSplit) : 0;
+    const int lts = t_max > 256 ? splits(t_max, 256, kMaxLadSplit) : 0;
     if (lts) {
       dim3 gp((unsigned)cdiv_up(B, kLocNT), S, lts);
       k_it_ladder_part<<<gp, kLocNT, 0, st>>>(a);
@@ -839,8 +839,15 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
       SFFT_CHECK_LAUNCH("k_po_log");
       int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)3 * S, W, a.y, bws, bws_bytes, st);
       if (rc) return rc;
-      k_po_correct<<<S, kPoNT, occ_sm, st>>>(a);
-      SFFT_CHECK_LAUNCH("k_po_correct");
+      SFFT_CUDA(cudaMemsetAsync(occ, 0, sizeof(int32_t) * (size_t)S * B, st));
+      const unsigned tb = (unsigned)std::max<int64_t>(1, cdiv_up(t_max, 256));
+      k_po_occ<<<dim3(tb, S), 256, 0, st>>>(a, occ);
+      SFFT_CHECK_LAUNCH("k_po_occ");
+      const unsigned td = (unsigned)std::max<int64_t>(1, cdiv_up(t_max, kPoNT));
+      k_po_delta<<<dim3(td, S), kPoNT, 0, st>>>(a, occ, corr);
+      SFFT_CHECK_LAUNCH("k_po_delta");
+      k_po_apply<<<dim3(tb, S), 256, 0, st>>>(a, corr);
+      SFFT_CHECK_LAUNCH("k_po_apply");
     }
   }
 
