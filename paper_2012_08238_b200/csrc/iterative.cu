@@ -213,12 +213,12 @@ constexpr int kLocChunk = 32;
 
 // Sum of the recovered model over tones [tb, te) at heavy bucket b for the
 // ladder shifts j = 1..M-1, subtracted from ys[] (running, in tone order).
+template <int M>
 __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bool live,
                                              int64_t tb, int64_t te, double2* ys,
                                              int64_t (*t_row), int64_t (*t_q), double2* t_c,
                                              double2 (*t_ph)[kMaxShifts]) {
   const int64_t n = a.n, B = a.B, L = a.L;
-  const int M = a.M;
   const int64_t sigma = a.item_sigma[s];
   const int64_t tau = a.item_tau[s];
   const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
@@ -244,6 +244,7 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
         int64_t col = b - t_q[tt];
         col += (col < 0) ? B : 0;
         const double2 cw = cmul(t_c[tt], __ldg(a.gt + t_row[tt] * B + col));
+#pragma unroll
         for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cmul(cw, t_ph[tt][j]));
       }
     }
@@ -252,6 +253,7 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
 
 // Tone-split partial ladder sums for large recovered lists:
 // part[s][z][h][j-1] = -sum_{tones of split z} c w ph_j.
+template <int M>
 __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
@@ -269,18 +271,21 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   const int64_t tb = (int64_t)blockIdx.z * per;
   const int64_t te = (tb + per < T) ? tb + per : T;
   const int b = live ? a.heavy[(int64_t)s * a.B + h] : 0;
-  double2 ys[kMaxShifts];
-  for (int j = 0; j < a.M; ++j) ys[j] = cmk(0.0, 0.0);
-  ladder_model(a, s, b, live, tb, te, ys, t_row, t_q, t_c, t_ph);
+  double2 ys[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) ys[j] = cmk(0.0, 0.0);
+  ladder_model<M>(a, s, b, live, tb, te, ys, t_row, t_q, t_c, t_ph);
   if (!live) return;
-  double2* o = a.part + (((int64_t)s * TS + blockIdx.z) * a.B + h) * (a.M - 1);
-  for (int j = 1; j < a.M; ++j) o[j - 1] = ys[j];
+  double2* o = a.part + (((int64_t)s * TS + blockIdx.z) * a.B + h) * (M - 1);
+#pragma unroll
+  for (int j = 1; j < M; ++j) o[j - 1] = ys[j];
 }
 
 // Ladder values at heavy buckets minus the recovered model, phase unwrap,
 // passband / consistency / weight checks, coefficient (frameworks.py:493-516).
 // TS == 0: the model is subtracted here in tone order; TS > 0: summed from
 // k_it_ladder_part's splits.
+template <int M>
 __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
@@ -294,18 +299,18 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   const int h = h0 + threadIdx.x;
   const bool live = h < nh;
   const int64_t n = a.n, B = a.B, L = a.L;
-  const int M = a.M;
   const int64_t sigma = a.item_sigma[s];
   const int64_t tau = a.item_tau[s];  // shift 0 item
   const int b = live ? a.heavy[(int64_t)s * B + h] : 0;
-  double2 ys[kMaxShifts];
-  ys[0] = a.y[(int64_t)s * B + b];
-  for (int j = 1; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
+  double2 ys[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
   if (TS == 0) {
-    ladder_model(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_c, t_ph);
+    ladder_model<M>(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_c, t_ph);
   } else if (live) {
     for (int z = 0; z < TS; ++z) {
       const double2* p = a.part + (((int64_t)s * TS + z) * B + h) * (M - 1);
+#pragma unroll
       for (int j = 1; j < M; ++j) ys[j] = cadd(ys[j], p[j - 1]);
     }
   }
@@ -325,6 +330,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   };
   double2 r1 = cdiv(ys[1], y0);
   double q = fmodpos(atan2(r1.y, r1.x) * scl, nd);
+#pragma unroll
   for (int j = 2; j < M; ++j) {
     const double2 rj = cdiv(ys[j], y0);
     const double phi = fmodpos(atan2(rj.y, rj.x) * scl, nd);
@@ -339,6 +345,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   if (pmod(qi - lo, n) >= L) return;
   // ladder consistency
   const double tol = fmax(3.0 * S.floor, 0.15 * cabs_scalar(y0));
+#pragma unroll
   for (int j = 1; j < M; ++j) {
     const double2 pred = cmul(y0, unit_root(n, mulmod(a.ladder[j - 1] % n, qi, n)));
     if (cabs_scalar(csub(ys[j], pred)) > tol) return;
@@ -348,6 +355,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   if (cabs_scalar(w) < 0.05 * a.gmax[0]) return;
   // mean of the dephased ladder values / w
   double2 sum = cmk(0.0, 0.0);
+#pragma unroll
   for (int j = 0; j < M; ++j) {
     const int64_t sh = (j == 0) ? 0 : a.ladder[j - 1];
     const int64_t ex = pmod(-mulmod(pmod(tau + sh, n), qi, n), n);
@@ -681,6 +689,38 @@ __global__ void k_it_outputs(const IterState* st, int S, int32_t* iters, int32_t
   conv[s] = st[s].converged;
 }
 
+template <int M>
+static int launch_locate_t(const IterArgs& a, int64_t B, int S, int lts, cudaStream_t st) {
+  if (lts) {
+    dim3 gp((unsigned)cdiv_up(B, kLocNT), S, lts);
+    k_it_ladder_part<M><<<gp, kLocNT, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_it_ladder_part");
+  }
+  dim3 gl((unsigned)cdiv_up(B, kLocNT), S);
+  k_it_locate<M><<<gl, kLocNT, 0, st>>>(a, lts);
+  SFFT_CHECK_LAUNCH("k_it_locate");
+  return 0;
+}
+
+// ladder lengths 1..12 (M = 2..13); _phase_ladder(N) has ~log8(N/16)+1 rungs
+static int launch_locate(const IterArgs& a, int M, int64_t B, int S, int lts, cudaStream_t st) {
+  switch (M) {
+    case 2: return launch_locate_t<2>(a, B, S, lts, st);
+    case 3: return launch_locate_t<3>(a, B, S, lts, st);
+    case 4: return launch_locate_t<4>(a, B, S, lts, st);
+    case 5: return launch_locate_t<5>(a, B, S, lts, st);
+    case 6: return launch_locate_t<6>(a, B, S, lts, st);
+    case 7: return launch_locate_t<7>(a, B, S, lts, st);
+    case 8: return launch_locate_t<8>(a, B, S, lts, st);
+    case 9: return launch_locate_t<9>(a, B, S, lts, st);
+    case 10: return launch_locate_t<10>(a, B, S, lts, st);
+    case 11: return launch_locate_t<11>(a, B, S, lts, st);
+    case 12: return launch_locate_t<12>(a, B, S, lts, st);
+    case 13: return launch_locate_t<13>(a, B, S, lts, st);
+    default: set_error("iterative: phase ladder length outside 1..12"); return -2;
+  }
+}
+
 static int splits(int T, int per, int mx) {
   const int z = (T + per - 1) / per;
   return z < 1 ? 1 : (z > mx ? mx : z);
@@ -797,15 +837,9 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
     if (rc) return rc;
     k_it_decide<<<S, kDecNT, dsm, st>>>(a, it);
     SFFT_CHECK_LAUNCH("k_it_decide");
-    dim3 gl((unsigned)cdiv_up(B, kLocNT), S);
     const int lts = t_max > 256 ? splits(t_max, 256, kMaxLadSplit) : 0;
-    if (lts) {
-      dim3 gp((unsigned)cdiv_up(B, kLocNT), S, lts);
-      k_it_ladder_part<<<gp, kLocNT, 0, st>>>(a);
-      SFFT_CHECK_LAUNCH("k_it_ladder_part");
-    }
-    k_it_locate<<<gl, kLocNT, 0, st>>>(a, lts);
-    SFFT_CHECK_LAUNCH("k_it_locate");
+    rc = launch_locate(a, M, B, S, lts, st);
+    if (rc) return rc;
     k_it_merge<<<S, kMrgNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_merge");
     // residual of y0 after the tones found now (only where gate[s])
@@ -858,7 +892,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   SFFT_CHECK_LAUNCH("k_it_outputs");
   k_copy_ngroups<<<sb, 128, 0, st>>>(a.st, S, ngroups);
   SFFT_CHECK_LAUNCH("k_copy_ngroups");
-  int rc = run_union_count(a.groups, ngroups, S, n, out_samples, st);
+  int rc = run_union_count(a.groups, ngroups, S, n, out_samples, st, 128);
   if (rc) return rc;
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched);
