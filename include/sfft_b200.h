@@ -172,6 +172,25 @@ int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int
                        int32_t* out_converged, int64_t* out_samples, int64_t* out_sched, void* ws,
                        size_t ws_bytes, void* stream);
 
+/* Workspace bytes of sfft_run_voting. */
+size_t sfft_voting_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t rounds, int64_t k,
+                            int64_t prestage_buckets);
+
+/* A15 run_voting (sfft/frameworks.py:354-417) for nsig signals: rounds
+ * bucketizations each (perm_sigma/perm_tau [nsig][rounds]), floors, top-2k
+ * heavy sets, votes, candidates with >= need_votes votes ((-votes, pos),
+ * first 2k), optional spike pre-stage filter (prestage_buckets > 0, with its
+ * twiddle table W_pre), energy estimates, trimmed mean and two
+ * model-refinement passes.  Outputs as sfft_run_iterative (iterations =
+ * rounds, converged = 1 are implied).  Never synchronises. */
+int sfft_run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                    const double* taps, int64_t omega, int64_t B, const void* gtable,
+                    const double* gmax, const void* W, const int64_t* perm_sigma,
+                    const int64_t* perm_tau, int64_t rounds, int64_t k, int64_t need_votes,
+                    int64_t prestage_buckets, const void* W_pre, int64_t* out_pos,
+                    void* out_coef, int32_t* out_count, int64_t* out_samples, int64_t* out_sched,
+                    void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

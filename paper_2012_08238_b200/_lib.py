@@ -116,3 +116,9 @@ SIGNATURES.update({
     "sfft_prof_enable": (C.c_int, [C.c_int]),
     "sfft_prof_read": (C.c_int, [vp, vp, vp]),
 })
+SIGNATURES.update({
+    "sfft_voting_ws_bytes": (sz, [i64, i64, i64, i64, i64, i64]),
+    "sfft_run_voting": (C.c_int, [C.c_int, vp, i64, i64, i64, P_f64, i64, i64, vp, P_f64, vp,
+                                  P_i64, P_i64, i64, i64, i64, i64, vp, P_i64, vp, P_i32, P_i64,
+                                  P_i64, vp, sz, vp]),
+})

@@ -271,3 +271,32 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
                        (double2*)out_coef, out_count, out_iterations, out_converged, out_samples,
                        out_sched, ws, ws_bytes, (cudaStream_t)stream);
 }
+
+SFFT_API size_t sfft_voting_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t rounds,
+                                     int64_t k, int64_t prestage_buckets) {
+  return voting_ws_bytes(n, B, (int)nsig, (int)rounds, (int)(2 * k), prestage_buckets);
+}
+
+SFFT_API int sfft_run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                             const double* taps, int64_t omega, int64_t B, const void* gtable,
+                             const double* gmax, const void* W, const int64_t* perm_sigma,
+                             const int64_t* perm_tau, int64_t rounds, int64_t k,
+                             int64_t need_votes, int64_t prestage_buckets, const void* W_pre,
+                             int64_t* out_pos, void* out_coef, int32_t* out_count,
+                             int64_t* out_samples, int64_t* out_sched, void* ws, size_t ws_bytes,
+                             void* stream) {
+  SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_voting: dtype must be 0 or 1");
+  SFFT_REQUIRE(x && taps && gtable && gmax && W && perm_sigma && perm_tau,
+               "sfft_run_voting: null pointer");
+  SFFT_REQUIRE(n > 0 && B > 0 && n % B == 0 && nsig >= 1 && k >= 1 && need_votes >= 1,
+               "sfft_run_voting: bad sizes");
+  SFFT_REQUIRE(n < (int64_t(1) << 31), "sfft_run_voting: n must be < 2^31");
+  SFFT_REQUIRE(prestage_buckets == 0 || (n % prestage_buckets == 0 && W_pre),
+               "sfft_run_voting: pre-stage buckets must divide n (and need twiddles)");
+  SFFT_REQUIRE(out_pos && out_coef && out_count && out_samples, "sfft_run_voting: null output");
+  return run_voting(dtype, x, n, xstride, (int)nsig, taps, omega, B, (const double2*)gtable,
+                    gmax, (const double2*)W, perm_sigma, perm_tau, (int)rounds, k,
+                    (int)need_votes, prestage_buckets, (const double2*)W_pre, out_pos,
+                    (double2*)out_coef, out_count, out_samples, out_sched, ws, ws_bytes,
+                    (cudaStream_t)stream);
+}

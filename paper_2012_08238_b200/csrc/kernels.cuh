@@ -86,6 +86,15 @@ int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        int64_t tstride, const int32_t* gate, cudaStream_t st, int TS = 1,
                        double2* part = nullptr);
 
+// voting.cu
+size_t voting_ws_bytes(int64_t n, int64_t B, int S, int R, int C, int64_t Bpre);
+int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, const double* taps,
+               int64_t omega, int64_t B, const double2* gt, const double* gmax, const double2* W,
+               const int64_t* psig, const int64_t* ptau, int R, int64_t k, int need,
+               int64_t Bpre, const double2* Wpre, int64_t* out_pos, double2* out_coef,
+               int32_t* out_n, int64_t* out_samples, int64_t* out_sched, void* ws,
+               size_t ws_bytes, cudaStream_t st);
+
 // iterative.cu
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap);
 int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,

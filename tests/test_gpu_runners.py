@@ -125,3 +125,22 @@ def test_schedule_matches_oracle_c1s2(sb):
     br = sb.run_iterative_batch(sb.TimeSignal(x), 16, _cfg(sb, rec))
     got = [(r[1], r[2]) for r in br.schedule_records(0)]
     assert got == calls
+
+
+VOTE = _select("voting")
+
+
+@pytest.mark.parametrize("case", VOTE, ids=[c[0]["name"] for c in VOTE])
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-10), ("complex64", 1e-4)])
+def test_voting_golden(sb, case, dtype, tol):
+    rec, arr = case
+    check_case(sb, rec, arr, dtype, tol,
+               diagnostics=(dtype == "complex128" or not _exact(rec)))
+
+
+VOTE_SMALL = [c for c in VOTE if not c[0]["name"].startswith("C2")]
+
+
+@pytest.mark.parametrize("case", VOTE_SMALL, ids=[c[0]["name"] for c in VOTE_SMALL])
+def test_voting_rounded(sb, case):
+    check_rounded(sb, *case)
