@@ -191,6 +191,25 @@ int sfft_run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int64_
                     void* out_coef, int32_t* out_count, int64_t* out_samples, int64_t* out_sched,
                     void* ws, size_t ws_bytes, void* stream);
 
+/* Workspace bytes of sfft_run_peeling (factors_host: HOST int64[nfactors]). */
+size_t sfft_peeling_ws_bytes(int64_t n, int64_t nsig, const int64_t* factors_host,
+                             int64_t nfactors, int64_t k);
+
+/* A17 run_peeling (sfft/frameworks.py:614-699) for nsig signals: one spike
+ * stage per co-prime factor p (B = n/p buckets, 3 shifts when p > 3 else
+ * max(p-1, 1)), floors, a_max = 1 classification of every active bucket,
+ * two-tier FIFO single-ton queues and the sequential peel (one warp per
+ * signal).  W_stages_host: HOST array of device twiddle tables, one per
+ * stage (size n/p).  out_error[s] = 1 where the reference would raise
+ * InvalidParameter (an active bucket in a one-shift stage).  out_iterations
+ * = peels, out_converged = no multi-ton left.  Never synchronises. */
+int sfft_run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                     const int64_t* factors_host, int64_t nfactors,
+                     const void* const* W_stages_host, int64_t k, int64_t* out_pos,
+                     void* out_coef, int32_t* out_count, int32_t* out_iterations,
+                     int32_t* out_converged, int32_t* out_error, int64_t* out_samples,
+                     int64_t* out_sched, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

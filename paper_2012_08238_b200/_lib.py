@@ -122,3 +122,8 @@ SIGNATURES.update({
                                   P_i64, P_i64, i64, i64, i64, i64, vp, P_i64, vp, P_i32, P_i64,
                                   P_i64, vp, sz, vp]),
 })
+SIGNATURES.update({
+    "sfft_peeling_ws_bytes": (sz, [i64, i64, vp, i64, i64]),
+    "sfft_run_peeling": (C.c_int, [C.c_int, vp, i64, i64, i64, vp, i64, vp, i64, P_i64, vp,
+                                   P_i32, P_i32, P_i32, P_i32, P_i64, P_i64, vp, sz, vp]),
+})

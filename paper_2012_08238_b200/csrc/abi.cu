@@ -300,3 +300,33 @@ SFFT_API int sfft_run_voting(int dtype, const void* x, int64_t n, int64_t xstrid
                     (double2*)out_coef, out_count, out_samples, out_sched, ws, ws_bytes,
                     (cudaStream_t)stream);
 }
+
+SFFT_API size_t sfft_peeling_ws_bytes(int64_t n, int64_t nsig, const int64_t* factors_host,
+                                      int64_t nfactors, int64_t k) {
+  return peeling_ws_bytes(n, (int)nsig, factors_host, (int)nfactors, k);
+}
+
+SFFT_API int sfft_run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                              const int64_t* factors_host, int64_t nfactors,
+                              const void* const* W_stages_host, int64_t k, int64_t* out_pos,
+                              void* out_coef, int32_t* out_count, int32_t* out_iterations,
+                              int32_t* out_converged, int32_t* out_error, int64_t* out_samples,
+                              int64_t* out_sched, void* ws, size_t ws_bytes, void* stream) {
+  SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_peeling: dtype must be 0 or 1");
+  SFFT_REQUIRE(x && factors_host && W_stages_host && nfactors >= 1 && k >= 1 && nsig >= 1,
+               "sfft_run_peeling: bad argument");
+  SFFT_REQUIRE(n > 0 && n < (int64_t(1) << 31), "sfft_run_peeling: n must be in (0, 2^31)");
+  int64_t prod = 1;
+  for (int64_t j = 0; j < nfactors; ++j) {
+    SFFT_REQUIRE(factors_host[j] > 1 && n % factors_host[j] == 0,
+                 "sfft_run_peeling: factors must be > 1 and divide n");
+    prod *= factors_host[j];
+  }
+  SFFT_REQUIRE(prod == n, "sfft_run_peeling: factors must multiply to n");
+  SFFT_REQUIRE(out_pos && out_coef && out_count && out_iterations && out_converged && out_error &&
+               out_samples, "sfft_run_peeling: null output");
+  return run_peeling(dtype, x, n, xstride, (int)nsig, factors_host, (int)nfactors,
+                     (const double2* const*)W_stages_host, k, out_pos, (double2*)out_coef,
+                     out_count, out_iterations, out_converged, out_error, out_samples, out_sched,
+                     ws, ws_bytes, (cudaStream_t)stream);
+}

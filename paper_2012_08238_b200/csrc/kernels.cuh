@@ -95,6 +95,14 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
                int32_t* out_n, int64_t* out_samples, int64_t* out_sched, void* ws,
                size_t ws_bytes, cudaStream_t st);
 
+// peeling.cu
+size_t peeling_ws_bytes(int64_t n, int S, const int64_t* factors, int nst, int64_t k);
+int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
+                const int64_t* factors, int nst, const double2* const* Wst, int64_t k,
+                int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
+                int32_t* out_conv, int32_t* out_err, int64_t* out_samples, int64_t* out_sched,
+                void* ws, size_t ws_bytes, cudaStream_t st);
+
 // iterative.cu
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap);
 int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,

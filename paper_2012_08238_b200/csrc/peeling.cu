@@ -1,0 +1,477 @@
+// Batched FFAST-style peeling (sfft/frameworks.py:614-699), device-resident.
+//
+//   stage j: B_j = n/p_j buckets, shifts t < s_j (3 when p_j > 3, else
+//            max(p_j-1, 1)); meas_j[t] = bucketize_spike(x, B_j, t)     (A7)
+//   floor_j  = robust_noise_floor(meas_j[0])                             (A8)
+//   classify every bucket with mean_t|m_t| >= floor_j (a_max = 1):
+//            zero / single (phase location + carrier check) / multi      (A17)
+//   queues   = singles in (stage, bucket) order, verified stages (3 shifts)
+//              first; then one warp per signal peels sequentially: pop a
+//              still-single entry, recovered[f] += c, subtract c w^{t f} from
+//              bucket f mod B_j of every stage, reclassify, push new singles
+//   stuck    = any bucket's latest class is multi
+#include "kernels.cuh"
+#include "schedule.cuh"
+#include "finalize.cuh"
+
+namespace sfft {
+
+constexpr int kMaxPeelStages = 16;
+
+struct PeelArgs {
+  int64_t n, k;
+  int S, nst;
+  int64_t p[kMaxPeelStages], Bs[kMaxPeelStages], sh[kMaxPeelStages];
+  int64_t moff[kMaxPeelStages];      // meas offset of stage j (elements), layout [s_j][S][B_j]
+  int64_t boff[kMaxPeelStages + 1];  // bucket offset of stage j in the per-signal class arrays
+  int64_t sumB;
+  double2* meas;
+  double* floor;                 // [nst][S]
+  int32_t* kind;                 // [S][sumB] 0 none/zero, 1 single, 2 multi
+  int64_t* cf;                   // [S][sumB] single position
+  double2* cc;                   // [S][sumB] single coefficient
+  int64_t* q[2];                 // [S][qcap] tier 0 = verified (3 shifts), 1 = others
+  int32_t* qtail[2];             // [S]
+  int64_t qcap;
+  int64_t* rec_pos;              // [S][cap]
+  double2* rec_coef;             // [S][cap]
+  int32_t* rec_count;            // [S]
+  int cap;
+  int64_t* ht_key;               // [S][HT]
+  int32_t* ht_val;
+  int HT;
+  int32_t* peels;                // [S]
+  int32_t* err;                  // [S] 1: a 1-shift stage had an active bucket
+};
+
+__device__ __forceinline__ int stage_of(const PeelArgs& a, int64_t g) {
+  int j = 0;
+  while (j + 1 < a.nst && g >= a.boff[j + 1]) ++j;
+  return j;
+}
+
+__device__ __forceinline__ double2 moment(const PeelArgs& a, int j, int s, int t, int64_t b) {
+  return a.meas[a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b];
+}
+
+struct Verdict {
+  int kind;
+  int64_t f;
+  double2 c;
+};
+
+// classify_bucket with a_max = 1 (sfft/reconstruct.py:412-440) after the
+// peeling pre-check (sfft/frameworks.py:653-658).  Warp-cooperative: the
+// nearest-candidate search (_nearest_candidate, reconstruct.py:136-140) is
+// split over the lanes; every lane returns the same verdict.
+__device__ Verdict classify_warp(const PeelArgs& a, int s, int j, int64_t b, int lane,
+                                 int32_t* err) {
+  Verdict v{0, 0, cmk(0.0, 0.0)};
+  const int ns = (int)a.sh[j];
+  const int64_t n = a.n, B = a.Bs[j], L = a.p[j];
+  const double fl = a.floor[(int64_t)j * a.S + s];
+  double2 m[3];
+  double sabs = 0.0;
+  for (int t = 0; t < ns; ++t) {
+    m[t] = moment(a, j, s, t, b);
+    sabs += cabs_(m[t]);
+  }
+  if (sabs / ns < fl) return v;  // zero
+  if (ns < 2) {                  // MomentSequence raises InvalidParameter
+    if (lane == 0) atomicExch(err, 1);
+    v.kind = 2;
+    return v;
+  }
+  if (cabs_scalar(m[0]) < fl) {
+    v.kind = 2;
+    return v;
+  }
+  const double nd = (double)n;
+  const double2 r = cdiv(m[1], m[0]);
+  double raw = fmod(atan2(r.y, r.x) * (-nd / (2.0 * 3.141592653589793)), nd);
+  if (raw != 0.0 && raw < 0.0) raw += nd;
+  if (raw == 0.0) raw = 0.0;
+  // nearest admissible candidate (bucket + B*i) mod n, ties to the smaller
+  double bd = CUDART_INF;
+  int64_t bc = 0x7fffffffffffffffll;
+  for (int64_t i = lane; i < L; i += 32) {
+    const int64_t cnd = pmod(b + B * i, n);
+    double d = fmod(((double)cnd - raw) + nd / 2.0, nd);
+    if (d != 0.0 && d < 0.0) d += nd;
+    d = fabs(d - nd / 2.0);
+    if (d < bd || (d == bd && cnd < bc)) {
+      bd = d;
+      bc = cnd;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const long long oc = __shfl_xor_sync(0xffffffffu, (long long)bc, o);
+    if (od < bd || (od == bd && oc < bc)) {
+      bd = od;
+      bc = oc;
+    }
+  }
+  const int64_t f = bc;
+  const double tol = fmax(fl, 0.05 * cabs_scalar(m[0]));
+  double mx = 0.0;
+  double2 sum = cmk(0.0, 0.0);
+  for (int t = 0; t < ns; ++t) {
+    const double2 car = unit_root(n, mulmod(t, f, n));
+    mx = fmax(mx, cabs_(csub(m[t], cmul(m[0], car))));
+    sum = cadd(sum, cmul(m[t], cconj(car)));
+  }
+  if (mx < tol) {
+    v.kind = 1;
+    v.f = f;
+    v.c = cdivr(sum, (double)ns);
+  } else {
+    v.kind = 2;
+  }
+  return v;
+}
+
+// Initial classification of every bucket of every stage (warp per bucket).
+__global__ void k_pe_classify_all(PeelArgs a) {
+  const int s = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (g >= a.sumB) return;
+  const int j = stage_of(a, g);
+  const int64_t b = g - a.boff[j];
+  const Verdict v = classify_warp(a, s, j, b, lane, a.err + s);
+  if (lane == 0) {
+    const int64_t i = (int64_t)s * a.sumB + g;
+    a.kind[i] = v.kind;
+    a.cf[i] = v.f;
+    a.cc[i] = v.c;
+  }
+}
+
+// Singles in (stage, bucket) order into the two tier queues.
+__global__ void __launch_bounds__(1024) k_pe_queue_init(PeelArgs a) {
+  __shared__ int red[32];
+  const int s = blockIdx.x;
+  const int64_t per = (a.sumB + 1023) / 1024;
+  const int64_t g0 = threadIdx.x * per, g1 = min(a.sumB, g0 + per);
+  int c[2] = {0, 0};
+  for (int64_t g = g0; g < g1; ++g)
+    if (a.kind[(int64_t)s * a.sumB + g] == 1) ++c[a.sh[stage_of(a, g)] >= 3 ? 0 : 1];
+  int tot[2];
+  int off[2];
+  off[0] = block_exscan<1024>(c[0], red, &tot[0]);
+  off[1] = block_exscan<1024>(c[1], red, &tot[1]);
+  for (int64_t g = g0; g < g1; ++g) {
+    if (a.kind[(int64_t)s * a.sumB + g] != 1) continue;
+    const int tier = a.sh[stage_of(a, g)] >= 3 ? 0 : 1;
+    a.q[tier][(int64_t)s * a.qcap + off[tier]++] = g;
+  }
+  if (threadIdx.x == 0) {
+    a.qtail[0][s] = tot[0];
+    a.qtail[1][s] = tot[1];
+  }
+}
+
+__device__ __forceinline__ uint32_t pe_slot(int64_t f, int HT) {
+  return (uint32_t)(((unsigned long long)(f + 1) * 0x9E3779B97F4A7C15ull) >> 40) & (HT - 1);
+}
+
+// The sequential peel of one signal, one warp (frameworks.py:669-695).
+__global__ void k_pe_peel(PeelArgs a, int64_t budget) {
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x;
+  int64_t head[2] = {0, 0};
+  int32_t tail[2] = {a.qtail[0][s], a.qtail[1][s]};
+  int64_t* q[2] = {a.q[0] + (int64_t)s * a.qcap, a.q[1] + (int64_t)s * a.qcap};
+  int32_t* kind = a.kind + (int64_t)s * a.sumB;
+  int64_t* cfs = a.cf + (int64_t)s * a.sumB;
+  double2* ccs = a.cc + (int64_t)s * a.sumB;
+  int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  int64_t* hk = a.ht_key + (int64_t)s * a.HT;
+  int32_t* hv = a.ht_val + (int64_t)s * a.HT;
+  int nrec = 0;
+  int64_t peels = 0;
+  while (peels < budget) {
+    // pop the first still-single entry, verified tier first (all lanes agree)
+    int64_t g = -1;
+    for (int tier = 0; tier < 2 && g < 0; ++tier) {
+      while (head[tier] < tail[tier]) {
+        const int64_t e = q[tier][head[tier]++];
+        if (kind[e] == 1) {
+          g = e;
+          break;
+        }
+      }
+    }
+    if (g < 0) break;
+    const int64_t f = cfs[g];
+    const double2 c = ccs[g];
+    int grew = 0;
+    if (lane == 0) {
+      uint32_t h = pe_slot(f, a.HT);
+      int where = -1;
+      for (int pr = 0; pr < a.HT; ++pr) {
+        const int64_t key = hk[h];
+        if (key == f + 1) { where = hv[h]; break; }
+        if (key == 0) break;
+        h = (h + 1) & (a.HT - 1);
+      }
+      if (where >= 0) {
+        rc[where] = cadd(rc[where], c);
+      } else if (nrec < a.cap) {
+        hk[h] = f + 1;
+        hv[h] = nrec;
+        rp[nrec] = f;
+        rc[nrec] = c;
+        grew = 1;
+      }
+    }
+    nrec += __shfl_sync(0xffffffffu, grew, 0);
+    ++peels;
+    for (int j = 0; j < a.nst; ++j) {
+      const int64_t b = f % a.Bs[j];
+      if (lane < a.sh[j]) {
+        const int t = lane;
+        double2* mp = a.meas + a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b;
+        *mp = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
+      }
+      __syncwarp();
+      const Verdict v = classify_warp(a, s, j, b, lane, a.err + s);
+      const int64_t gi = a.boff[j] + b;
+      if (lane == 0) {
+        kind[gi] = v.kind;
+        cfs[gi] = v.f;
+        ccs[gi] = v.c;
+        if (v.kind == 1) {
+          const int tier = a.sh[j] >= 3 ? 0 : 1;
+          if (tail[tier] < a.qcap) q[tier][tail[tier]] = gi;
+        }
+      }
+      if (v.kind == 1) {
+        const int tier = a.sh[j] >= 3 ? 0 : 1;
+        if (tail[tier] < a.qcap) ++tail[tier];
+      }
+      __syncwarp();
+    }
+  }
+  if (lane == 0) {
+    a.rec_count[s] = nrec;
+    a.peels[s] = (int32_t)peels;
+  }
+}
+
+__global__ void k_pe_stuck(PeelArgs a, int32_t* conv, int32_t* iters) {
+  __shared__ int any;
+  const int s = blockIdx.x;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int64_t g = threadIdx.x; g < a.sumB; g += blockDim.x)
+    mine |= a.kind[(int64_t)s * a.sumB + g] == 2;
+  if (mine) atomicOr(&any, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    conv[s] = !any;
+    iters[s] = a.peels[s];
+  }
+}
+
+__global__ void k_pe_items(int S, int ns, int32_t* item_sig, int64_t* tau) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S * ns) return;
+  item_sig[i] = i % S;
+  tau[i] = i / S;
+}
+
+__global__ void k_pe_groups(PeelArgs a, Group* groups, int32_t* ngroups) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  int ng = 0;
+  for (int j = 0; j < a.nst; ++j)
+    for (int t = 0; t < a.sh[j] && ng < kMaxGroups; ++t, ++ng) {
+      Group& g = groups[(int64_t)s * kMaxGroups + ng];
+      g.kind = 1;
+      g.a = a.p[j];
+      g.tau = t;
+      g.cnt = a.Bs[j];
+      g.nsh = 1;
+      g.sh[0] = 0;
+    }
+  ngroups[s] = ng;
+}
+
+struct PeelLayout {
+  size_t off[24];
+  size_t total;
+};
+
+static size_t alp(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int pe_ht(int cap) {
+  int h = 1;
+  while (h < 2 * cap) h <<= 1;
+  return h;
+}
+
+static PeelLayout peel_layout(int S, int64_t msize, int64_t sumB, int64_t qcap, int cap,
+                              int nst, int64_t maxitems) {
+  PeelLayout L{};
+  const size_t HT = (size_t)pe_ht(cap);
+  size_t sizes[] = {
+      sizeof(double2) * (size_t)msize,            // 0 meas
+      sizeof(double) * (size_t)nst * S,           // 1 floor
+      sizeof(int32_t) * (size_t)S * sumB,         // 2 kind
+      sizeof(int64_t) * (size_t)S * sumB,         // 3 cf
+      sizeof(double2) * (size_t)S * sumB,         // 4 cc
+      sizeof(int64_t) * (size_t)S * qcap,         // 5 q0
+      sizeof(int64_t) * (size_t)S * qcap,         // 6 q1
+      sizeof(int32_t) * (size_t)S * 2,            // 7 qtail
+      sizeof(int64_t) * (size_t)S * cap,          // 8 rec_pos
+      sizeof(double2) * (size_t)S * cap,          // 9 rec_coef
+      sizeof(int32_t) * (size_t)S,                // 10 rec_count
+      sizeof(int64_t) * (size_t)S * HT,           // 11 ht_key
+      sizeof(int32_t) * (size_t)S * HT,           // 12 ht_val
+      sizeof(int32_t) * (size_t)S,                // 13 peels
+      sizeof(int32_t) * (size_t)S,                // 14 err
+      sizeof(Group) * (size_t)S * kMaxGroups,     // 15 groups
+      sizeof(int32_t) * (size_t)S,                // 16 ngroups
+      sizeof(int32_t) * (size_t)maxitems,         // 17 item_sig
+      sizeof(int64_t) * (size_t)maxitems,         // 18 item tau
+  };
+  size_t o = 0;
+  const int cnt = sizeof(sizes) / sizeof(sizes[0]);
+  for (int i = 0; i < cnt; ++i) {
+    L.off[i] = o;
+    o += alp(sizes[i]);
+  }
+  L.total = o;
+  return L;
+}
+
+struct PeelDims {
+  int64_t msize, sumB, qcap, maxitems, budget, bws;
+  int cap;
+};
+
+static PeelDims peel_dims(int64_t n, int S, const int64_t* factors, int nst, int64_t k) {
+  PeelDims d{};
+  for (int j = 0; j < nst; ++j) {
+    const int64_t p = factors[j], B = n / p;
+    const int64_t sh = p > 3 ? 3 : (p - 1 > 1 ? p - 1 : 1);
+    d.msize += sh * S * B;
+    d.sumB += B;
+    d.maxitems = std::max<int64_t>(d.maxitems, sh * S);
+    d.bws = std::max<int64_t>(d.bws, (int64_t)bucketize_ws_bytes(B, sh * S));
+  }
+  d.budget = k + d.sumB;
+  d.qcap = d.sumB + d.budget * nst;
+  d.cap = (int)std::min<int64_t>(d.budget, (int64_t)1 << 30);
+  return d;
+}
+
+size_t peeling_ws_bytes(int64_t n, int S, const int64_t* factors, int nst, int64_t k) {
+  const PeelDims d = peel_dims(n, S, factors, nst, k);
+  return peel_layout(S, d.msize, d.sumB, d.qcap, d.cap, nst, d.maxitems).total + d.bws;
+}
+
+int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
+                const int64_t* factors, int nst, const double2* const* Wst, int64_t k,
+                int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
+                int32_t* out_conv, int32_t* out_err, int64_t* out_samples, int64_t* out_sched,
+                void* ws, size_t ws_bytes, cudaStream_t st) {
+  SFFT_REQUIRE(nst >= 1 && nst <= kMaxPeelStages, "peeling: 1..16 co-prime factors");
+  SFFT_REQUIRE(k <= kFusedMaxB, "peeling: k must be <= 8192");
+  SFFT_REQUIRE(ws_bytes >= peeling_ws_bytes(n, S, factors, nst, k), "peeling: workspace too small");
+  const PeelDims d = peel_dims(n, S, factors, nst, k);
+  const PeelLayout Lo = peel_layout(S, d.msize, d.sumB, d.qcap, d.cap, nst, d.maxitems);
+  char* w = (char*)ws;
+  PeelArgs a{};
+  a.n = n;
+  a.k = k;
+  a.S = S;
+  a.nst = nst;
+  int64_t mo = 0, bo = 0;
+  for (int j = 0; j < nst; ++j) {
+    a.p[j] = factors[j];
+    a.Bs[j] = n / factors[j];
+    a.sh[j] = factors[j] > 3 ? 3 : std::max<int64_t>(factors[j] - 1, 1);
+    a.moff[j] = mo;
+    a.boff[j] = bo;
+    mo += a.sh[j] * S * a.Bs[j];
+    bo += a.Bs[j];
+  }
+  a.boff[nst] = bo;
+  a.sumB = d.sumB;
+  a.meas = (double2*)(w + Lo.off[0]);
+  a.floor = (double*)(w + Lo.off[1]);
+  a.kind = (int32_t*)(w + Lo.off[2]);
+  a.cf = (int64_t*)(w + Lo.off[3]);
+  a.cc = (double2*)(w + Lo.off[4]);
+  a.q[0] = (int64_t*)(w + Lo.off[5]);
+  a.q[1] = (int64_t*)(w + Lo.off[6]);
+  a.qtail[0] = (int32_t*)(w + Lo.off[7]);
+  a.qtail[1] = a.qtail[0] + S;
+  a.qcap = d.qcap;
+  a.rec_pos = (int64_t*)(w + Lo.off[8]);
+  a.rec_coef = (double2*)(w + Lo.off[9]);
+  a.rec_count = (int32_t*)(w + Lo.off[10]);
+  a.cap = d.cap;
+  a.HT = pe_ht(d.cap);
+  a.ht_key = (int64_t*)(w + Lo.off[11]);
+  a.ht_val = (int32_t*)(w + Lo.off[12]);
+  a.peels = (int32_t*)(w + Lo.off[13]);
+  a.err = (int32_t*)(w + Lo.off[14]);
+  Group* groups = (Group*)(w + Lo.off[15]);
+  int32_t* ngroups = (int32_t*)(w + Lo.off[16]);
+  int32_t* item_sig = (int32_t*)(w + Lo.off[17]);
+  int64_t* item_tau = (int64_t*)(w + Lo.off[18]);
+  void* bws = w + Lo.total;
+
+  SFFT_CUDA(cudaMemsetAsync(a.ht_key, 0, sizeof(int64_t) * (size_t)S * a.HT, st));
+  SFFT_CUDA(cudaMemsetAsync(a.err, 0, sizeof(int32_t) * S, st));
+  for (int j = 0; j < nst; ++j) {
+    const int ns = (int)a.sh[j];
+    k_pe_items<<<(unsigned)cdiv_up((int64_t)S * ns, 256), 256, 0, st>>>(S, ns, item_sig, item_tau);
+    SFFT_CHECK_LAUNCH("k_pe_items");
+    Prod p{};
+    p.x = x;
+    p.xstride = xstride;
+    p.n = n;
+    p.B = a.Bs[j];
+    p.item_sig = item_sig;
+    p.item_a = item_tau;
+    int rc = run_bucketize(dtype, PROD_SPIKE, p, (int64_t)S * ns, Wst[j], a.meas + a.moff[j], bws,
+                           (size_t)d.bws, st);
+    if (rc) return rc;
+    rc = run_floor(a.meas + a.moff[j], S, a.Bs[j], 3.0, nullptr, nullptr, a.floor + (int64_t)j * S,
+                   nullptr, st);
+    if (rc) return rc;
+  }
+  dim3 gc((unsigned)cdiv_up(d.sumB, 8), S);
+  k_pe_classify_all<<<gc, 256, 0, st>>>(a);
+  SFFT_CHECK_LAUNCH("k_pe_classify_all");
+  k_pe_queue_init<<<S, 1024, 0, st>>>(a);
+  SFFT_CHECK_LAUNCH("k_pe_queue_init");
+  k_pe_peel<<<S, 32, 0, st>>>(a, d.budget);
+  SFFT_CHECK_LAUNCH("k_pe_peel");
+  k_pe_stuck<<<S, 256, 0, st>>>(a, out_conv, out_iters);
+  SFFT_CHECK_LAUNCH("k_pe_stuck");
+  SFFT_CUDA(cudaMemcpyAsync(out_err, a.err, sizeof(int32_t) * S, cudaMemcpyDeviceToDevice, st));
+  const size_t dsm = (size_t)kFusedMaxB * (8 + 8 + 4);
+  SFFT_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, a.cap, k, out_pos,
+                                      out_coef, out_n);
+  SFFT_CHECK_LAUNCH("k_finalize");
+  k_pe_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(a, groups, ngroups);
+  SFFT_CHECK_LAUNCH("k_pe_groups");
+  int rc = run_union_count(groups, ngroups, S, n, out_samples, st, 32);
+  if (rc) return rc;
+  if (out_sched) {
+    k_export_groups<<<S, 64, 0, st>>>(groups, ngroups, S, out_sched);
+    SFFT_CHECK_LAUNCH("k_export_groups");
+  }
+  return 0;
+}
+
+}  // namespace sfft

@@ -144,3 +144,22 @@ VOTE_SMALL = [c for c in VOTE if not c[0]["name"].startswith("C2")]
 @pytest.mark.parametrize("case", VOTE_SMALL, ids=[c[0]["name"] for c in VOTE_SMALL])
 def test_voting_rounded(sb, case):
     check_rounded(sb, *case)
+
+
+PEEL = _select("peeling")
+
+
+@pytest.mark.parametrize("case", PEEL, ids=[c[0]["name"] for c in PEEL])
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-10), ("complex64", 1e-4)])
+def test_peeling_golden(sb, case, dtype, tol):
+    rec, arr = case
+    check_case(sb, rec, arr, dtype, tol,
+               diagnostics=(dtype == "complex128" or not _exact(rec)))
+
+
+PEEL_SMALL = [c for c in PEEL if not c[0]["name"].startswith("C4")]
+
+
+@pytest.mark.parametrize("case", PEEL_SMALL, ids=[c[0]["name"] for c in PEEL_SMALL])
+def test_peeling_rounded(sb, case):
+    check_rounded(sb, *case)
