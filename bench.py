@@ -322,7 +322,7 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB per GPU)" % (S * N * 8 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
-                         "kernel": "k_fused<float2,FLAT> (gather+window+fold+FFT_B)",
+                         "kernel": "k_cluster<float2,FLAT,8> (gather+window+fold, DSMEM radix-8 stage, FFT_512)",
                          "bytes_per_item": item_bytes, "items": pi.value,
                          "launches": pl.value, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / ms if ms else None},

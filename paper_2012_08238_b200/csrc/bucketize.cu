@@ -13,6 +13,8 @@
 // memory, and the CTA runs the B-point FFT in place.  Larger B (config 5,
 // FFAST stages) use a four-step split B = B1*B2 whose column pass produces
 // the slots directly (no z round trip) and whose row pass writes y.
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace sfft {
@@ -131,6 +133,85 @@ __global__ void __launch_bounds__(kNT) k_fused(Prod p, FftPlan P, const double2*
   double2* o = out + (int64_t)item * B;
   const double bd = (double)B;
   for (int k = threadIdx.x; k < B; k += kNT) o[k] = cdivr(sm[fft_pos(k, P)], bd);
+}
+
+// Cluster path (B = CL * M, CL in {2,4,8}): the CL CTAs of a thread-block
+// cluster own one item.  CTA p folds slots [pM, pM + M) into its shared
+// memory; the radix-CL first DIF stage reads the CL slot slices over DSMEM
+// (b_q[j] = w_B^{jq} sum_p a_p[j] w_CL^{pq}, q = cluster rank), and each CTA
+// finishes its length-M sub-transform locally: y[q + CL k] = FFT_M(b_q)[k]/B.
+// CL x more CTAs per bucketization than k_fused, so a 77k-sample gather is
+// spread over 8 SMs instead of one.
+constexpr int kClNT = 256;
+
+template <typename Tin, int MODE, int CL>
+__global__ void __launch_bounds__(kClNT) k_cluster(Prod p, FftPlan Pm,
+                                                   const double2* __restrict__ W,
+                                                   double2* __restrict__ out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double2 sm[];
+  const int q = (int)cl.block_rank();
+  const int item = blockIdx.x / CL;
+  const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
+  if (c.skip) return;  // uniform over the cluster (same item)
+  if (p.prof_items && threadIdx.x == 0 && q == 0) atomicAdd(p.prof_items, 1ull);
+  const int B = (int)p.B;
+  const int M = B / CL;
+  double2* a = sm;
+  double2* bq = sm + M;
+  for (int j = threadIdx.x; j < M; j += kClNT)
+    a[j] = produce<Tin, MODE>(p, c, item, (int64_t)q * M + j);
+  cl.sync();
+  const double2* rem[CL];
+#pragma unroll
+  for (int r = 0; r < CL; ++r) rem[r] = cl.map_shared_rank(a, r);
+  double2 wr[CL];
+#pragma unroll
+  for (int r = 0; r < CL; ++r) wr[r] = __ldg(W + ((r * q) % CL) * M);
+  for (int j = threadIdx.x; j < M; j += kClNT) {
+    double2 acc = rem[0][j];
+#pragma unroll
+    for (int r = 1; r < CL; ++r) acc = cadd(acc, cmul(rem[r][j], wr[r]));
+    const int e = j * q;
+    bq[j] = e ? cmul(acc, __ldg(W + e)) : acc;
+  }
+  cl.sync();  // remote reads complete before any CTA of the cluster moves on
+  fft_dif(bq, 1, M, Pm, W, B, threadIdx.x, kClNT);
+  double2* o = out + (int64_t)item * B + q;
+  const double bd = (double)B;
+  for (int k = threadIdx.x; k < M; k += kClNT) o[(int64_t)CL * k] = cdivr(bq[fft_pos(k, Pm)], bd);
+}
+
+template <typename Tin, int MODE, int CL>
+static int launch_cluster(const Prod& p, int64_t nitems, const FftPlan& Pm, const double2* W,
+                          double2* out, cudaStream_t st) {
+  const int M = (int)(p.B / CL);
+  const size_t sm = (size_t)2 * M * sizeof(double2);
+  auto kern = k_cluster<Tin, MODE, CL>;
+  SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nitems * CL));
+  cfg.blockDim = dim3(kClNT);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, p, Pm, W, out));
+  SFFT_CHECK_LAUNCH("k_cluster");
+  return 0;
+}
+
+// cluster size for B (0: use the one-CTA path)
+static int cluster_size(int64_t B) {
+  if (B < 1024 || B > kFusedMaxB || (B & (B - 1))) return 0;
+  const int64_t M = std::max<int64_t>(256, B / 8);
+  return (int)(B / M);
 }
 
 // Four-step column pass: DFT_B1 over n1 of z[n1*B2 + n2] for CG columns, times
@@ -293,6 +374,15 @@ static bool split_plan(int64_t B, int64_t* B1, int64_t* B2) {
   return true;
 }
 
+// SFFT_NO_CLUSTER=1 forces the one-CTA path (A/B measurements).
+static bool cluster_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("SFFT_NO_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
 size_t bucketize_ws_bytes(int64_t B, int64_t nitems) {
   FftPlan P;
   if (B <= kFusedMaxB && make_plan(B, &P)) return 0;
@@ -305,9 +395,19 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
   if (nitems <= 0) return 0;
   const int64_t B = p.B;
   FftPlan P;
+  const int CL = cluster_size(B);
+  if (CL > 1 && !cluster_disabled()) {
+    FftPlan Pm;
+    make_plan(B / CL, &Pm);
+    if (CL == 8) return launch_cluster<Tin, MODE, 8>(p, nitems, Pm, W, out, st);
+    if (CL == 4) return launch_cluster<Tin, MODE, 4>(p, nitems, Pm, W, out, st);
+    return launch_cluster<Tin, MODE, 2>(p, nitems, Pm, W, out, st);
+  }
   if (B <= kFusedMaxB && make_plan(B, &P)) {
     const size_t sm = (size_t)B * sizeof(double2);
     if (ensure_smem(k_fused<Tin, MODE>, sm)) return -3;
+    SFFT_CUDA(cudaFuncSetAttribute(k_fused<Tin, MODE>,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     k_fused<Tin, MODE><<<(unsigned)nitems, kNT, sm, st>>>(p, P, W, out);
     SFFT_CHECK_LAUNCH("k_fused");
     return 0;
