@@ -163,19 +163,24 @@ SFFT_HD double2 unit_root(int64_t n, int64_t e) {
 }
 
 // ----------------------------------------------------------------- loads
+// Permuted signal gathers: ld.global.cg (cache at L2, bypass L1).  The
+// read-only texture path (ld.global.nc) fills L1 at 128-byte granularity,
+// which for a random 8-byte gather quadruples the L2->SM and DRAM sector
+// traffic (measured with ncu: lts sectors 4.3x l1tex sectors); .cg requests
+// single 32-byte sectors.
 template <typename T>
 struct Sample;
 template <>
 struct Sample<float2> {
   static __device__ __forceinline__ double2 load(const float2* p, int64_t i) {
-    float2 v = __ldg(p + i);
+    float2 v = __ldcg(p + i);
     return cmk((double)v.x, (double)v.y);
   }
 };
 template <>
 struct Sample<double2> {
   static __device__ __forceinline__ double2 load(const double2* p, int64_t i) {
-    return __ldg(p + i);
+    return __ldcg(p + i);
   }
 };
 
