@@ -15,6 +15,8 @@
 // the slots directly (no z round trip) and whose row pass writes y.
 #include <cooperative_groups.h>
 
+#include <mutex>
+
 #include "kernels.cuh"
 
 namespace sfft {
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(kNT) k_fused(Prod p, FftPlan P, const double2*
   for (int s = threadIdx.x; s < B; s += kNT) sm[s] = produce<Tin, MODE>(p, c, item, s);
   __syncthreads();
   fft_dif(sm, 1, B, P, W, B, threadIdx.x, kNT);
-  double2* o = out + (int64_t)item * B;
+  double2* o = out + out_row(p, item) * B;
   const double bd = (double)B;
   for (int k = threadIdx.x; k < B; k += kNT) o[k] = cdivr(sm[fft_pos(k, P)], bd);
 }
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(kClNT) k_cluster(Prod p, FftPlan Pm,
   }
   cl.sync();  // remote reads complete before any CTA of the cluster moves on
   fft_dif(bq, 1, M, Pm, W, B, threadIdx.x, kClNT);
-  double2* o = out + (int64_t)item * B + q;
+  double2* o = out + out_row(p, item) * B + q;
   const double bd = (double)B;
   for (int k = threadIdx.x; k < M; k += kClNT) o[(int64_t)CL * k] = cdivr(bq[fft_pos(k, Pm)], bd);
 }
@@ -251,7 +253,8 @@ __global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2
 __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, FftPlan P2, int B1,
                                               int B2, int RG, const double2* __restrict__ W,
                                               const int32_t* item_sig, const int32_t* active,
-                                              double2* __restrict__ out) {
+                                              double2* __restrict__ out, int out_M,
+                                              int64_t out_S) {
   extern __shared__ double2 sm[];
   const int item = blockIdx.y;
   if (active) {
@@ -269,7 +272,8 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
   }
   __syncthreads();
   fft_dif(sm, RG, seg, P2, W, B, threadIdx.x, kNT);
-  double2* o = out + (int64_t)item * B;
+  const int64_t row = out_M > 0 ? (item % out_M) * out_S + item / out_M : item;
+  double2* o = out + row * B;
   const double bd = (double)B;
   for (int t = threadIdx.x; t < RG * B2; t += kNT) {
     const int g = t % RG, k2 = t / RG;
@@ -293,7 +297,8 @@ __global__ void __launch_bounds__(256) k_dft_direct(const double2* __restrict__ 
                                                     const double2* __restrict__ W,
                                                     const int32_t* item_sig,
                                                     const int32_t* active,
-                                                    double2* __restrict__ out) {
+                                                    double2* __restrict__ out, int out_M,
+                                                    int64_t out_S) {
   const int item = blockIdx.y;
   if (active) {
     const int sig = item_sig ? item_sig[item] : item;
@@ -312,7 +317,8 @@ __global__ void __launch_bounds__(256) k_dft_direct(const double2* __restrict__ 
     e += k;
     if (e >= B) e -= B;
   }
-  out[(int64_t)item * B + k] = cdivr(acc, (double)B);
+  const int64_t row = out_M > 0 ? (item % out_M) * out_S + item / out_M : item;
+  out[row * B + k] = cdivr(acc, (double)B);
 }
 
 __global__ void k_twiddle(double2* W, int64_t B) {
@@ -430,14 +436,15 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
     k_cols<Tin, MODE><<<gc, kNT, smc, st>>>(p, P1, (int)B1, (int)B2, CG, W, z);
     SFFT_CHECK_LAUNCH("k_cols");
     dim3 gr((unsigned)cdiv_up(B1, RG), (unsigned)nitems);
-    k_rows<<<gr, kNT, smr, st>>>(z, P2, (int)B1, (int)B2, RG, W, p.item_sig, p.active, out);
+    k_rows<<<gr, kNT, smr, st>>>(z, P2, (int)B1, (int)B2, RG, W, p.item_sig, p.active, out,
+                                 p.out_M, p.out_S);
     SFFT_CHECK_LAUNCH("k_rows");
     return 0;
   }
   dim3 g((unsigned)cdiv_up(B, 256), (unsigned)nitems);
   k_slots<Tin, MODE><<<g, 256, 0, st>>>(p, z);
   SFFT_CHECK_LAUNCH("k_slots");
-  k_dft_direct<<<g, 256, 0, st>>>(z, B, W, p.item_sig, p.active, out);
+  k_dft_direct<<<g, 256, 0, st>>>(z, B, W, p.item_sig, p.active, out, p.out_M, p.out_S);
   SFFT_CHECK_LAUNCH("k_dft_direct");
   return 0;
 }
@@ -492,8 +499,26 @@ int prof_collect() {
 
 // Flat and spike bucketizations of the runners and the C ABI go through here;
 // with profiling on, each launch is bracketed by CUDA events on its stream.
+// Random 8-byte gathers: ask L2 to fetch single 32-byte sectors from HBM
+// instead of the default 64/128-byte promotion (measured: 4 DRAM sectors per
+// gathered sample without this).  Once per device; SFFT_L2_FETCH overrides.
+static void gather_fetch_granularity() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  const char* e = getenv("SFFT_L2_FETCH");
+  const size_t g = e ? (size_t)atoi(e) : 32;
+  if (g > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g);
+  cudaGetLastError();
+  done[dev] = true;
+}
+
 int run_bucketize(int dtype, int mode, const Prod& p0, int64_t nitems, const double2* W,
                   double2* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  gather_fetch_granularity();
   BucketProf& bp = bucket_prof();
   if (!bp.on || (mode != PROD_FLAT && mode != PROD_SPIKE))
     return run_bucketize_inner(dtype, mode, p0, nitems, W, out, ws, ws_bytes, st);

@@ -49,9 +49,11 @@ struct IterArgs {
   int32_t* active;               // [S] main loop gate
   int32_t* gate;                 // [S] secondary gate (residual / polish)
   int32_t* n_active;             // device counter
-  int32_t* item_sig;             // [M*S]
-  int64_t* item_sigma;           // [M*S]
-  int64_t* item_tau;             // [M*S]
+  int32_t* item_sig;             // [S*M] items signal-major (s*M + j)
+  int64_t* item_sigma_it;        // [S*M] per item
+  int64_t* item_tau_it;          // [S*M] per item
+  int64_t* item_sigma;           // [S] shift-0 sigma of each signal's current measurement
+  int64_t* item_tau;             // [S] shift-0 tau
   double2* y;                    // [M][S][B]
   double2* resid;                // [S][B]
   int64_t* rec_pos;              // [S][cap]
@@ -107,17 +109,26 @@ __device__ __forceinline__ void ht_insert(const IterArgs& a, int s, int64_t f, i
 }
 
 // ------------------------------------------------------------------ items
+// Items are signal-major (i = s*nsh + j) so that the shifted measurements of
+// one signal, which re-read most of the same samples, run side by side and
+// share L2 lines; outputs land shift-major (row j*S + s, see Prod::out_M).
 __global__ void k_it_items(IterArgs a, int p, int nsh, const int64_t* shifts_dev,
                            bool use_cursor) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsh * a.S) return;
-  const int j = i / a.S, s = i - j * a.S;
+  const int s = i / nsh, j = i - s * nsh;
   const int pi = use_cursor ? a.st[s].cursor : p;
   const int pp = pi < a.P ? pi : a.P - 1;
   a.item_sig[i] = s;
-  a.item_sigma[i] = a.psig[(int64_t)s * a.P + pp];
+  const int64_t sg = a.psig[(int64_t)s * a.P + pp];
+  const int64_t t0 = a.ptau[(int64_t)s * a.P + pp];
   const int64_t d = shifts_dev ? shifts_dev[j] : (j == 0 ? 0 : a.ladder[j - 1]);
-  a.item_tau[i] = pmod(a.ptau[(int64_t)s * a.P + pp] + d, a.n);
+  a.item_sigma_it[i] = sg;
+  a.item_tau_it[i] = pmod(t0 + d, a.n);
+  if (j == 0) {
+    a.item_sigma[s] = sg;
+    a.item_tau[s] = pmod(t0, a.n);
+  }
 }
 
 // ------------------------------------------------------------------ decide
@@ -639,8 +650,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * S,                   // 2 gate
       sizeof(int32_t) * 8,                   // 3 stats
       sizeof(int32_t) * M * S,               // 4 item_sig
-      sizeof(int64_t) * M * S,               // 5 item_sigma
-      sizeof(int64_t) * M * S,               // 6 item_tau
+      sizeof(int64_t) * M * S * 2,           // 5 item_sigma_it + item_sigma
+      sizeof(int64_t) * M * S * 2,           // 6 item_tau_it + item_tau
       sizeof(double2) * (size_t)M * S * B,   // 7 y
       sizeof(double2) * (size_t)S * B,       // 8 resid
       sizeof(int64_t) * (size_t)S * cap,     // 9 rec_pos
@@ -763,8 +774,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   a.stats = (int32_t*)(w + Lo.off[3]);
   a.n_active = a.stats;
   a.item_sig = (int32_t*)(w + Lo.off[4]);
-  a.item_sigma = (int64_t*)(w + Lo.off[5]);
-  a.item_tau = (int64_t*)(w + Lo.off[6]);
+  a.item_sigma_it = (int64_t*)(w + Lo.off[5]);
+  a.item_sigma = a.item_sigma_it + (size_t)M * S;
+  a.item_tau_it = (int64_t*)(w + Lo.off[6]);
+  a.item_tau = a.item_tau_it + (size_t)M * S;
   a.y = (double2*)(w + Lo.off[7]);
   a.resid = (double2*)(w + Lo.off[8]);
   a.rec_pos = (int64_t*)(w + Lo.off[9]);
@@ -812,9 +825,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   p.omega = omega;
   p.B = B;
   p.item_sig = a.item_sig;
-  p.item_a = a.item_sigma;
-  p.item_b = a.item_tau;
+  p.item_a = a.item_sigma_it;
+  p.item_b = a.item_tau_it;
   p.active = a.active;
+  p.out_S = S;
 
   const size_t dsm = (size_t)kFusedMaxB * (8 + 8 + 4);
   SFFT_CUDA(cudaFuncSetAttribute(k_it_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
@@ -828,6 +842,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   for (int it = 1; it <= max_it; ++it) {
     k_it_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a, it - 1, M, nullptr, false);
     SFFT_CHECK_LAUNCH("k_it_items");
+    p.out_M = M;
     int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
     if (rc) return rc;
     // y0 -= model(recovered), all buckets (tone-split when the lists are long)
@@ -871,6 +886,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
       SFFT_CHECK_LAUNCH("k_it_items(polish)");
       k_po_log<<<sb, 128, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_po_log");
+      p.out_M = 3;
       int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)3 * S, W, a.y, bws, bws_bytes, st);
       if (rc) return rc;
       SFFT_CUDA(cudaMemsetAsync(occ, 0, sizeof(int32_t) * (size_t)S * B, st));

@@ -24,7 +24,13 @@ struct Prod {
   const int32_t* active;     // per-signal gate (null: all active)
   const double2* z;          // PROD_LOAD source [nitems][B]
   unsigned long long* prof_items;  // profiling: count of non-skipped items (null: off)
+  int out_M;                 // > 0: item i writes output row (i % out_M) * out_S + i / out_M
+  int64_t out_S;             //      (items ordered signal-major, rows shift-major)
 };
+
+__host__ __device__ __forceinline__ int64_t out_row(const Prod& p, int64_t item) {
+  return p.out_M > 0 ? (item % p.out_M) * p.out_S + item / p.out_M : item;
+}
 
 // Profiling of the bucketization (gather-fold-FFT) launches: CUDA events on
 // the launching stream around every launch, items counted on the device.
