@@ -33,7 +33,7 @@ template <int MODE>
 __device__ __forceinline__ ItemCtx item_ctx(const Prod& p, int item, int elem_bytes) {
   ItemCtx c;
   const int sig = p.item_sig ? p.item_sig[item] : item;
-  c.skip = p.active && !p.active[sig];
+  c.skip = (p.active && !p.active[sig]) || (p.item_active && !p.item_active[item]);
   c.xs = p.x ? (const char*)p.x + (int64_t)sig * p.xstride * elem_bytes : nullptr;
   c.a = p.item_a ? p.item_a[item] : 0;
   c.b = p.item_b ? p.item_b[item] : 0;
@@ -254,9 +254,10 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
                                               int B2, int RG, const double2* __restrict__ W,
                                               const int32_t* item_sig, const int32_t* active,
                                               double2* __restrict__ out, int out_M,
-                                              int64_t out_S) {
+                                              int64_t out_S, const int32_t* item_active) {
   extern __shared__ double2 sm[];
   const int item = blockIdx.y;
+  if (item_active && !item_active[item]) return;
   if (active) {
     const int sig = item_sig ? item_sig[item] : item;
     if (!active[sig]) return;
@@ -298,8 +299,9 @@ __global__ void __launch_bounds__(256) k_dft_direct(const double2* __restrict__ 
                                                     const int32_t* item_sig,
                                                     const int32_t* active,
                                                     double2* __restrict__ out, int out_M,
-                                                    int64_t out_S) {
+                                                    int64_t out_S, const int32_t* item_active) {
   const int item = blockIdx.y;
+  if (item_active && !item_active[item]) return;
   if (active) {
     const int sig = item_sig ? item_sig[item] : item;
     if (!active[sig]) return;
@@ -437,14 +439,15 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
     SFFT_CHECK_LAUNCH("k_cols");
     dim3 gr((unsigned)cdiv_up(B1, RG), (unsigned)nitems);
     k_rows<<<gr, kNT, smr, st>>>(z, P2, (int)B1, (int)B2, RG, W, p.item_sig, p.active, out,
-                                 p.out_M, p.out_S);
+                                 p.out_M, p.out_S, p.item_active);
     SFFT_CHECK_LAUNCH("k_rows");
     return 0;
   }
   dim3 g((unsigned)cdiv_up(B, 256), (unsigned)nitems);
   k_slots<Tin, MODE><<<g, 256, 0, st>>>(p, z);
   SFFT_CHECK_LAUNCH("k_slots");
-  k_dft_direct<<<g, 256, 0, st>>>(z, B, W, p.item_sig, p.active, out, p.out_M, p.out_S);
+  k_dft_direct<<<g, 256, 0, st>>>(z, B, W, p.item_sig, p.active, out, p.out_M, p.out_S,
+                                  p.item_active);
   SFFT_CHECK_LAUNCH("k_dft_direct");
   return 0;
 }

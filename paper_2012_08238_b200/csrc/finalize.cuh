@@ -26,16 +26,22 @@ struct FinPosKey {  // f+1 of the entries whose |c| bits equal u; else 0
 };
 
 // One CTA per signal; dynamic smem kFusedMaxB * 20 bytes; k <= kFusedMaxB.
+// gate (optional): only slots with gate[s] != 0; rows (optional): output row
+// of slot s (default s).
 static __global__ void __launch_bounds__(kFinNT) k_finalize(const int64_t* rec_pos,
                                                             const double2* rec_coef,
                                                             const int32_t* rec_count, int cap,
                                                             int64_t k, int64_t* out_pos,
-                                                            double2* out_coef, int32_t* out_n) {
+                                                            double2* out_coef, int32_t* out_n,
+                                                            const int32_t* gate = nullptr,
+                                                            const int32_t* rows = nullptr) {
   extern __shared__ unsigned char fsm[];
   __shared__ int redi[32];
   __shared__ unsigned hist[256];
   __shared__ long long sh[4];
   const int s = blockIdx.x;
+  if (gate && !gate[s]) return;
+  const int64_t row = rows ? rows[s] : s;
   const int T = rec_count[s];
   const int64_t* rp = rec_pos + (int64_t)s * cap;
   const double2* rc = rec_coef + (int64_t)s * cap;
@@ -86,10 +92,10 @@ static __global__ void __launch_bounds__(kFinNT) k_finalize(const int64_t* rec_p
   while (capp < cnt) capp <<= 1;
   block_bitonic<kFinNT>(k1, k2, pay, cnt, capp);
   for (int i = threadIdx.x; i < kk; i += kFinNT) {
-    out_pos[(int64_t)s * k + i] = rp[pay[i]];
-    out_coef[(int64_t)s * k + i] = rc[pay[i]];
+    out_pos[row * k + i] = rp[pay[i]];
+    out_coef[row * k + i] = rc[pay[i]];
   }
-  if (threadIdx.x == 0) out_n[s] = kk;
+  if (threadIdx.x == 0) out_n[row] = kk;
 }
 
 }  // namespace sfft

@@ -1,13 +1,16 @@
 // Batched iterative framework with phase location (sfft/frameworks.py:439-516,
 // :556-570) and the residual polish (:573-608), device-resident.
 //
-// S signals advance in lock step; every decision (convergence, heavy set,
-// ladder unwrapping, consistency, merge into the recovered list, the residual
-// test, polish corrections) is taken on the device per signal, and kernels
-// of finished signals exit at once.  The host only loops over iterations and
-// reads one "signals still active" counter per iteration.
+// Continuous batching: S slots work through a queue of Q signals.  Every
+// round advances each busy slot by one step of its own state machine — a
+// loop iteration (LOOP) or a polish pass (POLISH) — and a slot whose signal
+// finishes is refilled from the queue by the device at the start of the next
+// round, so signals that need many iterations never leave the GPU idle.
+// Every decision (convergence, heavy set, ladder unwrapping, consistency,
+// merge, residual test, polish corrections, admission) is taken on the
+// device; the host only issues the rounds and reads one counter per round.
 //
-// Per iteration and signal (perm = perms[s][it-1]):
+// Per loop iteration of a slot (perm = perms[sig][it-1]):
 //   y[j] = bucketize(x, sigma, tau + d_j), d = {0} U ladder       (one launch)
 //   y0  -= model(recovered)                   all B buckets      (k_subtract)
 //   floor, convergence, heavy list (-|y0|, b)                    (k_it_decide)
@@ -20,7 +23,16 @@
 
 namespace sfft {
 
+enum SlotPhase { PH_FREE = 0, PH_LOOP = 1, PH_POLISH = 2, PH_FINISH = 3, PH_IDLE = 4 };
+
 struct IterState {
+  int32_t sig;         // queue index of the signal in this slot
+  int32_t phase;
+  int32_t it;          // loop iterations entered so far
+  int32_t pidx;        // permutation index of this round's measurement
+  int32_t nsh;         // measurements this round (M loop, 3 polish, 0 idle)
+  int32_t epoch, pass; // polish position
+  int32_t newslot;     // admitted this round: hash table needs clearing
   double scale_ref;
   double floor;
   double final_resid;
@@ -38,7 +50,11 @@ struct IterState {
 
 struct IterArgs {
   int64_t n, B, L, omega, k;
-  int S, P, M, max_it, cap;      // cap = recovered capacity per signal
+  int S, P, M, max_it, cap;      // S slots; cap = recovered capacity per slot
+  int Q;                         // signals in the queue
+  int64_t pstride;               // perms row stride per signal (0: shared stream)
+  int32_t* item_active;          // [S*M]
+  int32_t* pgate;                // [S] polish pass this round
   int64_t ladder[kMaxShifts];    // d_1..d_{M-1}
   const int64_t* psig;           // [S][P]
   const int64_t* ptau;           // [S][P]
@@ -69,7 +85,7 @@ struct IterArgs {
   int32_t* pend;                 // [S][cap] polish pending flags
   double2* delta;                // [S][cap] polish corrections
   Group* groups;                 // [S][kMaxGroups]
-  int32_t* stats;                // [4]: n_active, max recovered, max heavy, spare
+  int32_t* stats;                // [8]: -, max recovered, max heavy, done, next
   int64_t* ht_key;               // [S][HT] recovered-position hash (key f+1, 0 empty)
   int32_t* ht_val;               // [S][HT] index into rec_*
   int HT;                        // power of two >= 2*cap
@@ -108,26 +124,110 @@ __device__ __forceinline__ void ht_insert(const IterArgs& a, int s, int64_t f, i
   }
 }
 
-// ------------------------------------------------------------------ items
-// Items are signal-major (i = s*nsh + j) so that the shifted measurements of
-// one signal, which re-read most of the same samples, run side by side and
-// share L2 lines; outputs land shift-major (row j*S + s, see Prod::out_M).
-__global__ void k_it_items(IterArgs a, int p, int nsh, const int64_t* shifts_dev,
-                           bool use_cursor) {
+// ------------------------------------------------------------------ rounds
+// Admission: a free slot takes the next queued signal.
+__global__ void k_cb_admit(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  IterState& S = a.st[s];
+  if (S.phase != PH_FREE) return;
+  const int idx = atomicAdd(a.stats + 4, 1);
+  if (idx >= a.Q) {
+    S.phase = PH_IDLE;
+    return;
+  }
+  S = IterState{};
+  S.sig = idx;
+  S.phase = PH_LOOP;
+  S.newslot = 1;
+  a.rec_count[s] = 0;
+}
+
+__global__ void k_cb_clear(IterArgs a) {
+  const int s = blockIdx.y;
+  if (!a.st[s].newslot) return;
+  int64_t* keys = a.ht_key + (int64_t)s * a.HT;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.HT;
+       i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = 0;
+}
+
+// This round's step of every slot: a loop iteration or a polish pass.
+__global__ void k_cb_step(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  IterState& S = a.st[s];
+  S.newslot = 0;
+  a.active[s] = 0;
+  a.pgate[s] = 0;
+  a.gate[s] = 0;
+  S.nsh = 0;
+  if (S.phase == PH_LOOP) {
+    S.it += 1;
+    S.entries = S.it;
+    S.pidx = S.it - 1;
+    S.nsh = a.M;
+    a.active[s] = 1;
+  } else if (S.phase == PH_POLISH) {
+    if (S.pass == 0) S.pending = S.n_rec;  // epoch start: every tone pending
+    S.pidx = S.cursor;
+    S.cursor += 1;
+    S.nsh = 3;
+    a.pgate[s] = 1;
+  } else {
+    return;
+  }
+  const int pp = S.pidx < a.P ? S.pidx : a.P - 1;
+  const int64_t sg = a.psig[(int64_t)S.sig * a.pstride + pp];
+  const int64_t t0 = pmod(a.ptau[(int64_t)S.sig * a.pstride + pp], a.n);
+  a.item_sigma[s] = sg;
+  a.item_tau[s] = t0;
+  if (S.phase == PH_POLISH) {
+    const int g = S.ngroups;
+    if (g < kMaxGroups) {
+      Group& G = a.groups[(int64_t)s * kMaxGroups + g];
+      G.kind = 0;
+      G.a = sg;
+      G.tau = t0;
+      G.cnt = a.omega;
+      G.nsh = 3;
+      G.sh[0] = 0;
+      G.sh[1] = 1;
+      G.sh[2] = 2;
+      S.ngroups = g + 1;
+    }
+  }
+}
+
+// Items are slot-major (i = s*M + j) so that the shifted measurements of one
+// signal, which re-read most of the same samples, run side by side and share
+// L2 lines; outputs land shift-major (row j*S + s, see Prod::out_M).
+__global__ void k_cb_items(IterArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nsh * a.S) return;
-  const int s = i / nsh, j = i - s * nsh;
-  const int pi = use_cursor ? a.st[s].cursor : p;
-  const int pp = pi < a.P ? pi : a.P - 1;
-  a.item_sig[i] = s;
-  const int64_t sg = a.psig[(int64_t)s * a.P + pp];
-  const int64_t t0 = a.ptau[(int64_t)s * a.P + pp];
-  const int64_t d = shifts_dev ? shifts_dev[j] : (j == 0 ? 0 : a.ladder[j - 1]);
-  a.item_sigma_it[i] = sg;
-  a.item_tau_it[i] = pmod(t0 + d, a.n);
-  if (j == 0) {
-    a.item_sigma[s] = sg;
-    a.item_tau[s] = pmod(t0, a.n);
+  if (i >= a.M * a.S) return;
+  const int s = i / a.M, j = i - s * a.M;
+  const IterState& S = a.st[s];
+  const bool on = j < S.nsh;
+  a.item_active[i] = on;
+  a.item_sig[i] = S.sig > 0 ? S.sig : 0;
+  if (!on) return;
+  const int64_t d = (S.phase == PH_LOOP) ? (j == 0 ? 0 : a.ladder[j - 1]) : j;
+  a.item_sigma_it[i] = a.item_sigma[s];
+  a.item_tau_it[i] = pmod(a.item_tau[s] + d, a.n);
+}
+
+// End of a slot's loop: polish when converged well below the scale, else done
+// (frameworks.py:566-569).
+__device__ __forceinline__ void loop_end(const IterArgs& a, IterState& S, int s) {
+  a.active[s] = 0;
+  const bool pol = S.converged && S.n_rec > 0 && S.final_resid < 0.01 * S.scale_ref;
+  if (pol) {
+    S.phase = PH_POLISH;
+    S.epoch = 0;
+    S.pass = 0;
+    S.cursor = S.entries;
+  } else {
+    S.phase = PH_FINISH;
   }
 }
 
@@ -135,7 +235,7 @@ __global__ void k_it_items(IterArgs a, int p, int nsh, const int64_t* shifts_dev
 constexpr int kDecNT = 512;
 
 // Floor / convergence / heavy list of y0 (sfft/frameworks.py:478-490).
-__global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a, int it) {
+__global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
   extern __shared__ unsigned char dsm[];
   __shared__ unsigned hist[256];
   __shared__ long long sh[4];
@@ -145,6 +245,7 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a, int it) {
   const int s = blockIdx.x;
   if (!a.active[s]) return;
   IterState& S = a.st[s];
+  const int it = S.it;
   const int64_t B = a.B;
   const double2* y0 = a.y + (int64_t)s * B;  // slot 0
   double med, peak;
@@ -169,13 +270,11 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a, int it) {
       for (int j = 1; j < a.M; ++j) G.sh[j] = a.ladder[j - 1];
       S.ngroups = g + 1;
     }
-    S.entries = it;
     if (conv) {
       S.converged = 1;
       S.final_resid = peak;
       S.iterations = it - 1;
-      a.active[s] = 0;
-      atomicSub(a.n_active, 1);
+      loop_end(a, S, s);
     }
   }
   if (conv) return;
@@ -443,11 +542,12 @@ __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
 }
 
 // ------------------------------------------------------------------ residual test
-__global__ void __launch_bounds__(kDecNT) k_it_resid(IterArgs a, int it) {
+__global__ void __launch_bounds__(kDecNT) k_it_resid(IterArgs a) {
   __shared__ double redd[32];
   const int s = blockIdx.x;
   if (!a.active[s]) return;
   IterState& S = a.st[s];
+  const int it = S.it;
   bool conv = false;
   double mx = 0.0;
   if (a.gate[s]) {
@@ -462,63 +562,37 @@ __global__ void __launch_bounds__(kDecNT) k_it_resid(IterArgs a, int it) {
       S.converged = 1;
       S.final_resid = mx;
       S.iterations = it;
-      a.active[s] = 0;
-      atomicSub(a.n_active, 1);
+      loop_end(a, S, s);
     } else if (it == a.max_it) {
       S.iterations = it;
-      a.active[s] = 0;
-      atomicSub(a.n_active, 1);
+      loop_end(a, S, s);
     }
   }
 }
 
 // ------------------------------------------------------------------ polish
-__global__ void k_po_setup(IterArgs a) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
-  IterState& S = a.st[s];
-  S.polish = (S.converged && S.n_rec > 0 && S.final_resid < 0.01 * S.scale_ref) ? 1 : 0;
-  S.cursor = S.entries;
-  S.pending = 0;
-}
-
+// Epoch start: every recovered tone pending again (frameworks.py:586).
 __global__ void k_po_epoch(IterArgs a) {
   const int s = blockIdx.y;
   const IterState& S = a.st[s];
-  if (!S.polish) return;
+  if (!a.pgate[s] || S.pass != 0) return;
   const int T = S.n_rec;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
     a.pend[(int64_t)s * a.cap + t] = 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.st[s].pending = T;
 }
 
-// polish gate + group log; items come from k_it_items with use_cursor
-__global__ void k_po_gate(IterArgs a) {
+// After a pass: at most 3 passes per epoch, an epoch ends when nothing is
+// pending, 2 epochs (frameworks.py:585-589).
+__global__ void k_po_after(IterArgs a) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
+  if (s >= a.S || !a.pgate[s]) return;
   IterState& S = a.st[s];
-  const int on = S.polish && S.pending > 0;
-  a.gate[s] = on;
-}
-
-__global__ void k_po_log(IterArgs a) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.S || !a.gate[s]) return;
-  IterState& S = a.st[s];
-  const int g = S.ngroups;
-  if (g < kMaxGroups) {
-    Group& G = a.groups[(int64_t)s * kMaxGroups + g];
-    G.kind = 0;
-    G.a = a.item_sigma[s];
-    G.tau = a.item_tau[s];
-    G.cnt = a.omega;
-    G.nsh = 3;
-    G.sh[0] = 0;
-    G.sh[1] = 1;
-    G.sh[2] = 2;
-    S.ngroups = g + 1;
+  S.pass += 1;
+  if (S.pending <= 0 || S.pass == 3) {
+    S.epoch += 1;
+    S.pass = 0;
+    if (S.epoch == 2) S.phase = PH_FINISH;
   }
-  S.cursor += 1;
 }
 
 constexpr int kPoNT = 64;
@@ -528,7 +602,7 @@ constexpr int kPoChunk = 128;
 // permutation (frameworks.py:596-598).  occ zeroed by the caller.
 __global__ void k_po_occ(IterArgs a, int32_t* occ) {
   const int s = blockIdx.y;
-  if (!a.gate[s]) return;
+  if (!a.pgate[s]) return;
   const int T = a.rec_count[s];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
@@ -546,7 +620,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
   __shared__ double2 u_c[kPoChunk];
   __shared__ double2 u_ph[kPoChunk][3];
   const int s = blockIdx.y;
-  if (!a.gate[s]) return;
+  if (!a.pgate[s]) return;
   const int64_t n = a.n, B = a.B, L = a.L;
   const int T = a.rec_count[s];
   const int t = blockIdx.x * kPoNT + threadIdx.x;
@@ -606,7 +680,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
 __global__ void k_po_apply(IterArgs a, const int32_t* corr) {
   __shared__ int cnt;
   const int s = blockIdx.y;
-  if (!a.gate[s]) return;
+  if (!a.pgate[s]) return;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
   const int T = a.rec_count[s];
@@ -624,7 +698,7 @@ __global__ void k_po_apply(IterArgs a, const int32_t* corr) {
 // ------------------------------------------------------------------ host driver
 
 struct IterLayout {
-  size_t off[32];
+  size_t off[40];
   size_t total;
 };
 
@@ -667,13 +741,15 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * cap,     // 19 pend
       sizeof(double2) * (size_t)S * cap,     // 20 delta
       sizeof(Group) * (size_t)S * kMaxGroups,// 21 groups
-      sizeof(int64_t) * 3,                   // 22 shifts (polish)
+      sizeof(int32_t) * 2 * S,               // 22 fin + rows
       sizeof(int32_t) * S,                   // 23 ngroups copy
       sizeof(int64_t) * (size_t)S * HT,      // 24 ht_key
       sizeof(int32_t) * (size_t)S * HT,      // 25 ht_val
       sizeof(double2) * (size_t)S * part,    // 26 part
       sizeof(int32_t) * (size_t)S * B,       // 27 occ (polish)
       sizeof(int32_t) * (size_t)S * cap,     // 28 corr (polish)
+      sizeof(int32_t) * (size_t)S * M,       // 29 item_active
+      sizeof(int32_t) * (size_t)S,           // 30 pgate
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -686,18 +762,6 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
 
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap) {
   return iter_layout(n, B, S, M, cap).total + bucketize_ws_bytes(B, (int64_t)M * S);
-}
-
-__global__ void k_copy_ngroups(const IterState* st, int S, int32_t* ng) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < S) ng[s] = st[s].ngroups;
-}
-
-__global__ void k_it_outputs(const IterState* st, int S, int32_t* iters, int32_t* conv) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S) return;
-  iters[s] = st[s].iterations;
-  conv[s] = st[s].converged;
 }
 
 template <int M>
@@ -737,18 +801,43 @@ static int splits(int T, int per, int mx) {
   return z < 1 ? 1 : (z > mx ? mx : z);
 }
 
-int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
+__global__ void k_cb_finish(IterArgs a, int32_t* fin, int32_t* rows, int32_t* ngroups,
+                            int32_t* out_iters, int32_t* out_conv) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  const IterState& S = a.st[s];
+  const bool f = S.phase == PH_FINISH;
+  fin[s] = f;
+  rows[s] = S.sig;
+  ngroups[s] = S.ngroups;
+  if (f) {
+    out_iters[S.sig] = S.iterations;
+    out_conv[S.sig] = S.converged;
+  }
+}
+
+__global__ void k_cb_release(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  IterState& S = a.st[s];
+  if (S.phase != PH_FINISH) return;
+  S.phase = PH_FREE;
+  atomicAdd(a.stats + 3, 1);
+}
+
+int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, int S,
                   const double* taps, int64_t omega, int64_t B, const double2* gt,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
-                  int P, int64_t k, int max_it, const int64_t* ladder, int nlad, int cap,
-                  int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
-                  int32_t* out_conv, int64_t* out_samples, int64_t* out_sched, void* ws,
-                  size_t ws_bytes, cudaStream_t st) {
+                  int P, int64_t pstride, int64_t k, int max_it, const int64_t* ladder, int nlad,
+                  int cap, int64_t* out_pos, double2* out_coef, int32_t* out_n,
+                  int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
+                  int64_t* out_sched, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = 1 + nlad;
   SFFT_REQUIRE(M <= kMaxShifts, "iterative: ladder too long");
   SFFT_REQUIRE(max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
   SFFT_REQUIRE(P >= max_it + 6, "iterative: need max_iterations + 6 permutations");
   SFFT_REQUIRE(k <= kFusedMaxB, "iterative: k must be <= 8192");
+  SFFT_REQUIRE(S >= 1 && Q >= 1, "iterative: need slots and signals");
   SFFT_REQUIRE(ws_bytes >= iterative_ws_bytes(n, B, S, M, cap), "iterative: workspace too small");
   const IterLayout Lo = iter_layout(n, B, S, M, cap);
   char* w = (char*)ws;
@@ -759,7 +848,9 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   a.omega = omega;
   a.k = k;
   a.S = S;
+  a.Q = Q;
   a.P = P;
+  a.pstride = pstride;
   a.M = M;
   a.max_it = max_it;
   a.cap = cap;
@@ -793,29 +884,24 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   a.pend = (int32_t*)(w + Lo.off[19]);
   a.delta = (double2*)(w + Lo.off[20]);
   a.groups = (Group*)(w + Lo.off[21]);
-  int64_t* po_shifts = (int64_t*)(w + Lo.off[22]);
+  int32_t* fin = (int32_t*)(w + Lo.off[22]);
+  int32_t* rows = fin + S;
   int32_t* ngroups = (int32_t*)(w + Lo.off[23]);
   a.HT = ht_size(cap);
   a.ht_key = (int64_t*)(w + Lo.off[24]);
   a.ht_val = (int32_t*)(w + Lo.off[25]);
   a.part = (double2*)(w + Lo.off[26]);
+  int32_t* occ = (int32_t*)(w + Lo.off[27]);
+  int32_t* corr = (int32_t*)(w + Lo.off[28]);
+  a.item_active = (int32_t*)(w + Lo.off[29]);
+  a.pgate = (int32_t*)(w + Lo.off[30]);
   void* bws = w + Lo.total;
   const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
 
-  // state init
+  // all slots free; queue counter 0
   SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
-  SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
   SFFT_CUDA(cudaMemsetAsync(a.stats, 0, sizeof(int32_t) * 8, st));
-  SFFT_CUDA(cudaMemsetAsync(a.ht_key, 0, sizeof(int64_t) * (size_t)S * a.HT, st));
-  {
-    std::vector<int32_t> ones(S, 1);
-    SFFT_CUDA(cudaMemcpyAsync(a.active, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st));
-    const int32_t na = S;
-    SFFT_CUDA(cudaMemcpyAsync(a.n_active, &na, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    const int64_t ps[3] = {0, 1, 2};
-    SFFT_CUDA(cudaMemcpyAsync(po_shifts, ps, sizeof(ps), cudaMemcpyHostToDevice, st));
-    SFFT_CUDA(cudaStreamSynchronize(st));  // host sources above are stack-owned
-  }
+  SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
 
   Prod p{};
   p.x = x;
@@ -827,93 +913,84 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   p.item_sig = a.item_sig;
   p.item_a = a.item_sigma_it;
   p.item_b = a.item_tau_it;
-  p.active = a.active;
+  p.item_active = a.item_active;
+  p.out_M = M;
   p.out_S = S;
 
   const size_t dsm = (size_t)kFusedMaxB * (8 + 8 + 4);
   SFFT_CUDA(cudaFuncSetAttribute(k_it_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   SFFT_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  int32_t* occ = (int32_t*)(w + Lo.off[27]);
-  int32_t* corr = (int32_t*)(w + Lo.off[28]);
 
   const unsigned sb = (unsigned)cdiv_up(S, 128);
-  int t_max = 0;  // largest recovered list (host copy, refreshed every iteration)
-  int h_max = 0;  // largest heavy list so far
-  for (int it = 1; it <= max_it; ++it) {
-    k_it_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a, it - 1, M, nullptr, false);
-    SFFT_CHECK_LAUNCH("k_it_items");
-    p.out_M = M;
+  int t_max = 0;  // largest recovered list seen (host copy, refreshed every round)
+  int h_max = 0;  // largest heavy list seen
+  const int max_rounds = (Q / S + 2) * (max_it + 8) + 16;
+  int round = 0;
+  for (; round < max_rounds; ++round) {
+    k_cb_admit<<<sb, 128, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_cb_admit");
+    k_cb_clear<<<dim3(16, S), 256, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_cb_clear");
+    k_cb_step<<<sb, 128, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_cb_step");
+    k_po_epoch<<<dim3(4, S), 256, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_po_epoch");
+    k_cb_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_cb_items");
     int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
     if (rc) return rc;
-    // y0 -= model(recovered), all buckets (tone-split when the lists are long)
+    // ---- loop slots
     rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st,
                             splits(t_max, 512, kMaxSubSplit), a.part);
     if (rc) return rc;
-    k_it_decide<<<S, kDecNT, dsm, st>>>(a, it);
+    k_it_decide<<<S, kDecNT, dsm, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_decide");
     const int lts = t_max > 256 ? splits(t_max, 256, kMaxLadSplit) : 0;
     rc = launch_locate(a, M, B, S, lts, st);
     if (rc) return rc;
     k_it_merge<<<S, kMrgNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_merge");
-    // residual of y0 after the tones found now (only where gate[s])
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
                             splits(h_max, 512, kMaxSubSplit), a.part);
     if (rc) return rc;
-    k_it_resid<<<S, kDecNT, 0, st>>>(a, it);
+    k_it_resid<<<S, kDecNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_resid");
-    int32_t hs[4] = {0, 0, 0, 0};
+    // ---- polish slots
+    SFFT_CUDA(cudaMemsetAsync(occ, 0, sizeof(int32_t) * (size_t)S * B, st));
+    const unsigned tb = (unsigned)std::max<int64_t>(1, cdiv_up(t_max, 256));
+    k_po_occ<<<dim3(tb, S), 256, 0, st>>>(a, occ);
+    SFFT_CHECK_LAUNCH("k_po_occ");
+    const unsigned td = (unsigned)std::max<int64_t>(1, cdiv_up(t_max, kPoNT));
+    k_po_delta<<<dim3(td, S), kPoNT, 0, st>>>(a, occ, corr);
+    SFFT_CHECK_LAUNCH("k_po_delta");
+    k_po_apply<<<dim3(tb, S), 256, 0, st>>>(a, corr);
+    SFFT_CHECK_LAUNCH("k_po_apply");
+    k_po_after<<<sb, 128, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_po_after");
+    // ---- finished slots: results to their signal's row, then free the slot
+    k_cb_finish<<<sb, 128, 0, st>>>(a, fin, rows, ngroups, out_iters, out_conv);
+    SFFT_CHECK_LAUNCH("k_cb_finish");
+    k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
+                                        out_coef, out_n, fin, rows);
+    SFFT_CHECK_LAUNCH("k_finalize");
+    rc = run_union_count(a.groups, ngroups, S, n, out_samples, st, 64, fin, rows);
+    if (rc) return rc;
+    if (out_sched) {
+      k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched, fin, rows);
+      SFFT_CHECK_LAUNCH("k_export_groups");
+    }
+    k_cb_release<<<sb, 128, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_cb_release");
+    int32_t hs[8];
     SFFT_CUDA(cudaMemcpyAsync(hs, a.stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
     SFFT_CUDA(cudaStreamSynchronize(st));
     t_max = hs[1];
     h_max = hs[2];
-    if (hs[0] <= 0) break;
+    if (hs[3] >= Q) break;
   }
-
-  // polish (2 epochs x <= 3 passes x shifts 0,1,2)
-  k_po_setup<<<sb, 128, 0, st>>>(a);
-  SFFT_CHECK_LAUNCH("k_po_setup");
-  p.active = a.gate;
-  for (int epoch = 0; epoch < 2; ++epoch) {
-    k_po_epoch<<<dim3(4, S), 256, 0, st>>>(a);
-    SFFT_CHECK_LAUNCH("k_po_epoch");
-    for (int pass = 0; pass < 3; ++pass) {
-      k_po_gate<<<sb, 128, 0, st>>>(a);
-      SFFT_CHECK_LAUNCH("k_po_gate");
-      k_it_items<<<(unsigned)cdiv_up((int64_t)3 * S, 256), 256, 0, st>>>(a, 0, 3, po_shifts, true);
-      SFFT_CHECK_LAUNCH("k_it_items(polish)");
-      k_po_log<<<sb, 128, 0, st>>>(a);
-      SFFT_CHECK_LAUNCH("k_po_log");
-      p.out_M = 3;
-      int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)3 * S, W, a.y, bws, bws_bytes, st);
-      if (rc) return rc;
-      SFFT_CUDA(cudaMemsetAsync(occ, 0, sizeof(int32_t) * (size_t)S * B, st));
-      const unsigned tb = (unsigned)std::max<int64_t>(1, cdiv_up(t_max, 256));
-      k_po_occ<<<dim3(tb, S), 256, 0, st>>>(a, occ);
-      SFFT_CHECK_LAUNCH("k_po_occ");
-      const unsigned td = (unsigned)std::max<int64_t>(1, cdiv_up(t_max, kPoNT));
-      k_po_delta<<<dim3(td, S), kPoNT, 0, st>>>(a, occ, corr);
-      SFFT_CHECK_LAUNCH("k_po_delta");
-      k_po_apply<<<dim3(tb, S), 256, 0, st>>>(a, corr);
-      SFFT_CHECK_LAUNCH("k_po_apply");
-    }
-  }
-
-  k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
-                                      out_coef, out_n);
-  SFFT_CHECK_LAUNCH("k_finalize");
-  k_it_outputs<<<sb, 128, 0, st>>>(a.st, S, out_iters, out_conv);
-  SFFT_CHECK_LAUNCH("k_it_outputs");
-  k_copy_ngroups<<<sb, 128, 0, st>>>(a.st, S, ngroups);
-  SFFT_CHECK_LAUNCH("k_copy_ngroups");
-  int rc = run_union_count(a.groups, ngroups, S, n, out_samples, st, 128);
-  if (rc) return rc;
-  if (out_sched) {
-    k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched);
-    SFFT_CHECK_LAUNCH("k_export_groups");
-  }
+  SFFT_REQUIRE(round < max_rounds, "iterative: round limit reached (internal error)");
   return 0;
 }
 

@@ -22,6 +22,7 @@ struct Prod {
   const int64_t* item_b;     // flat: tau_tot
   const int64_t* item_c;     // flat: b'*sigma mod n (null: 0)
   const int32_t* active;     // per-signal gate (null: all active)
+  const int32_t* item_active;  // per-item gate (null: all)
   const double2* z;          // PROD_LOAD source [nitems][B]
   unsigned long long* prof_items;  // profiling: count of non-skipped items (null: off)
   int out_M;                 // > 0: item i writes output row (i % out_M) * out_S + i / out_M
@@ -111,12 +112,12 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
 
 // iterative.cu
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap);
-int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int S,
+int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, int S,
                   const double* taps, int64_t omega, int64_t B, const double2* gt,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
-                  int P, int64_t k, int max_it, const int64_t* ladder, int nlad, int cap,
-                  int64_t* out_pos, double2* out_coef, int32_t* out_n, int32_t* out_iters,
-                  int32_t* out_conv, int64_t* out_samples, int64_t* out_sched, void* ws,
-                  size_t ws_bytes, cudaStream_t st);
+                  int P, int64_t pstride, int64_t k, int max_it, const int64_t* ladder, int nlad,
+                  int cap, int64_t* out_pos, double2* out_coef, int32_t* out_n,
+                  int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
+                  int64_t* out_sched, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace sfft

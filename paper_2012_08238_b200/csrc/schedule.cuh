@@ -117,11 +117,14 @@ constexpr int kSchedWords = 5 + kMaxShifts;  // kind, a, tau, cnt, nsh, sh[]
 
 // Export the groups as int64 records [S][kMaxGroups][kSchedWords].
 static __global__ void k_export_groups(const Group* __restrict__ groups, const int32_t* ngroups,
-                                int S, int64_t* out) {
+                                       int S, int64_t* out, const int32_t* gate = nullptr,
+                                       const int32_t* rows = nullptr) {
   const int s = blockIdx.x;
+  if (gate && !gate[s]) return;
+  const int64_t row = rows ? rows[s] : s;
   const int G = min(ngroups[s], kMaxGroups);
   for (int g = threadIdx.x; g < kMaxGroups; g += blockDim.x) {
-    int64_t* o = out + ((int64_t)s * kMaxGroups + g) * kSchedWords;
+    int64_t* o = out + (row * kMaxGroups + g) * kSchedWords;
     if (g >= G) {
       o[0] = -1;
       continue;
@@ -182,12 +185,14 @@ namespace sfft {
 // samples[s] (zeroed by the caller), so the result is exact and deterministic.
 static __global__ void __launch_bounds__(kUnionNT) k_union_count_mc(
     const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
-    unsigned long long* samples) {
+    unsigned long long* samples, const int32_t* gate, const int32_t* rows) {
   __shared__ Group sg[kMaxGroups];
   __shared__ GroupSh sp[kMaxGroups];
   __shared__ int64_t gstart[kMaxGroups + 1];
   __shared__ unsigned long long red[32];
   const int s = blockIdx.y;
+  if (gate && !gate[s]) return;
+  const int64_t row = rows ? rows[s] : s;
   const int G = min(ngroups[s], kMaxGroups);
   const Group* gs = groups + (int64_t)s * gstride;
   for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
@@ -224,17 +229,29 @@ static __global__ void __launch_bounds__(kUnionNT) k_union_count_mc(
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
     for (int i = 0; i < kUnionNT / 32; ++i) t += red[i];
-    if (t) atomicAdd(samples + s, t);
+    if (t) atomicAdd(samples + row, t);
   }
 }
 
 // samples[s] = |union of read sets| for every signal (exact, multi-CTA).
+static __global__ void k_zero_rows(int64_t* v, int S, const int32_t* gate, const int32_t* rows) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S || (gate && !gate[s])) return;
+  v[rows ? rows[s] : s] = 0;
+}
+
 inline int run_union_count(const Group* groups, const int32_t* ngroups, int S, int64_t n,
-                           int64_t* samples, cudaStream_t st, int chunks = 48) {
-  SFFT_CUDA(cudaMemsetAsync(samples, 0, sizeof(int64_t) * S, st));
+                           int64_t* samples, cudaStream_t st, int chunks = 48,
+                           const int32_t* gate = nullptr, const int32_t* rows = nullptr) {
+  if (gate || rows) {
+    k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
+    SFFT_CHECK_LAUNCH("k_zero_rows");
+  } else {
+    SFFT_CUDA(cudaMemsetAsync(samples, 0, sizeof(int64_t) * S, st));
+  }
   dim3 g(chunks, S);
   k_union_count_mc<<<g, kUnionNT, 0, st>>>(groups, ngroups, kMaxGroups, n,
-                                           (unsigned long long*)samples);
+                                           (unsigned long long*)samples, gate, rows);
   SFFT_CHECK_LAUNCH("k_union_count_mc");
   return 0;
 }

@@ -240,8 +240,15 @@ class _WS:
 
 # ------------------------------------------------------------------ iterative
 
-def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
-    """run_iterative (phase location) for every row of ``xs`` at once."""
+DEFAULT_SLOTS = 128
+
+
+def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = None) -> BatchResult:
+    """run_iterative (phase location) for every row of ``xs``.
+
+    The device engine keeps ``slots`` signals in flight (default
+    min(len(xs), 128)) and refills a slot from the queue as soon as its signal
+    finishes, so long-running signals never idle the GPU."""
     import torch
     cfg = cfg.validated()
     if cfg.framework != "iterative":
@@ -260,8 +267,9 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
     M = 1 + len(ladder)
     P = cfg.max_iterations + 6
     sig, tau = draw_perms(n, cfg.seed, P)
-    psig = torch.as_tensor(np.tile(sig, (S, 1)), device=dev)
-    ptau = torch.as_tensor(np.tile(tau, (S, 1)), device=dev)
+    psig = torch.as_tensor(sig, device=dev)    # one stream shared by all signals
+    ptau = torch.as_tensor(tau, device=dev)
+    nslots = min(S, slots or DEFAULT_SLOTS)
     cap = cfg.max_iterations * b
     out_pos = torch.zeros((S, k), dtype=torch.int64, device=dev)
     out_coef = torch.zeros((S, k), dtype=torch.complex128, device=dev)
@@ -271,15 +279,16 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
     out_sm = torch.zeros(S, dtype=torch.int64, device=dev)
     sched = _sched_buffer(S, dev)
     L = lib()
-    wsb = L.sfft_iterative_ws_bytes(n, b, S, M, cap)
+    wsb = L.sfft_iterative_ws_bytes(n, b, nslots, M, cap)
     ws = _WS.get(wsb, dev)
     import ctypes
     lad = (ctypes.c_int64 * len(ladder))(*ladder)
     dt = 0 if X.dtype == torch.complex64 else 1
     gmax = torch.tensor([filt.peak], dtype=torch.float64, device=dev)
-    check(L.sfft_run_iterative(dt, ptr(X), n, X.stride(0), S, ptr(filt.taps), filt.support, b,
-                               ptr(filt.gtable), ptr(gmax), ptr(twiddles(b, dev)), ptr(psig),
-                               ptr(ptau), P, k, cfg.max_iterations, lad, len(ladder), cap,
+    check(L.sfft_run_iterative(dt, ptr(X), n, X.stride(0), S, nslots, ptr(filt.taps),
+                               filt.support, b, ptr(filt.gtable), ptr(gmax),
+                               ptr(twiddles(b, dev)), ptr(psig), ptr(ptau), P, 0, k,
+                               cfg.max_iterations, lad, len(ladder), cap,
                                ptr(out_pos), ptr(out_coef), ptr(out_n), ptr(out_it), ptr(out_cv),
                                ptr(out_sm), ptr(sched), ptr(ws), wsb, stream_of(dev)),
           "sfft_run_iterative")

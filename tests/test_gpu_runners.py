@@ -163,3 +163,22 @@ PEEL_SMALL = [c for c in PEEL if not c[0]["name"].startswith("C4")]
 @pytest.mark.parametrize("case", PEEL_SMALL, ids=[c[0]["name"] for c in PEEL_SMALL])
 def test_peeling_rounded(sb, case):
     check_rounded(sb, *case)
+
+
+@pytest.mark.parametrize("slots", [1, 2, 3])
+def test_iterative_continuous_batching(sb, slots):
+    """A queue of signals through fewer device slots gives every signal the
+    reference's result (C1 seeds; slots refilled as signals finish)."""
+    import torch
+    cases = [c for c in CASES if c[0]["name"].startswith("C1")]
+    X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).cuda()
+    cfg = _cfg(sb, cases[0][0])
+    res = sb.run_iterative_batch(X, 16, cfg, slots=slots).to_results()
+    for (rec, arr), got in zip(cases, res):
+        want = dict(zip(arr["pos"].tolist(), arr["coef"].tolist()))
+        assert set(got.spectrum.entries) == set(want), rec["name"]
+        err = max(abs(got.spectrum.entries[f] - c) / abs(c) for f, c in want.items())
+        assert err <= 1e-10
+        assert got.samples_read == rec["samples_read"]
+        assert got.iterations == rec["iterations"]
+        assert got.converged == rec["converged"]
