@@ -89,13 +89,18 @@ __device__ inline void merge_pieces(const Group& g, int64_t n, GroupSh* out) {
   out->ainv = modinv(g.a, n);
 }
 
+// (a * b) mod n with a, b < n < 2^31; a mask when n is a power of two.
+__device__ __forceinline__ int64_t mulmod_n(int64_t a, int64_t b, int64_t n, int64_t mask) {
+  return mask >= 0 ? ((a * b) & mask) : (a * b) % n;
+}
+
 __device__ __forceinline__ bool group_has(const Group& g, const GroupSh& gs, int64_t n,
-                                          int64_t e) {
+                                          int64_t e, int64_t mask) {
   if (g.kind == 1) {
     const int64_t v = pmod(e + g.tau, n);
     return (v % g.a) == 0 && (v / g.a) < g.cnt;
   }
-  const int64_t t = mulmod(gs.ainv, e, n);
+  const int64_t t = mulmod_n(gs.ainv, e, n, mask);
   for (int i = 0; i < gs.np; ++i)
     if (t >= gs.lo[i] && t < gs.hi[i]) return true;
   return false;
@@ -103,11 +108,11 @@ __device__ __forceinline__ bool group_has(const Group& g, const GroupSh& gs, int
 
 // e of element j of group g (j < gs.total)
 __device__ __forceinline__ int64_t group_elem(const Group& g, const GroupSh& gs, int64_t n,
-                                              int64_t j) {
+                                              int64_t j, int64_t mask) {
   if (g.kind == 1) return pmod(g.a * j - g.tau, n);
   for (int i = 0; i < gs.np; ++i) {
     const int64_t len = gs.hi[i] - gs.lo[i];
-    if (j < len) return mulmod(g.a, gs.lo[i] + j, n);
+    if (j < len) return mulmod_n(g.a, gs.lo[i] + j, n, mask);
     j -= len;
   }
   return 0;
@@ -145,6 +150,7 @@ constexpr int kUnionNT = 512;
 static __global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __restrict__ groups,
                                                           const int32_t* ngroups, int gstride,
                                                           int64_t n, int64_t* samples) {
+  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
   __shared__ Group sg[kMaxGroups];
   __shared__ GroupSh sp[kMaxGroups];
   __shared__ unsigned long long red[32];
@@ -159,9 +165,9 @@ static __global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __
   for (int g = 0; g < G; ++g) {
     const int64_t tot = sp[g].total;
     for (int64_t j = threadIdx.x; j < tot; j += kUnionNT) {
-      const int64_t e = group_elem(sg[g], sp[g], n, j);
+      const int64_t e = group_elem(sg[g], sp[g], n, j, mask);
       bool fresh = true;
-      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e);
+      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e, mask);
       cnt += fresh;
     }
   }
@@ -193,6 +199,7 @@ static __global__ void __launch_bounds__(kUnionNT) k_union_count_mc(
   const int s = blockIdx.y;
   if (gate && !gate[s]) return;
   const int64_t row = rows ? rows[s] : s;
+  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
   const int G = min(ngroups[s], kMaxGroups);
   const Group* gs = groups + (int64_t)s * gstride;
   for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
@@ -216,9 +223,9 @@ static __global__ void __launch_bounds__(kUnionNT) k_union_count_mc(
   for (int g = 0; g < G; ++g) {
     const int64_t lo = max(c0, gstart[g]), hi = min(c1, gstart[g + 1]);
     for (int64_t j = lo + threadIdx.x; j < hi; j += kUnionNT) {
-      const int64_t e = group_elem(sg[g], sp[g], n, j - gstart[g]);
+      const int64_t e = group_elem(sg[g], sp[g], n, j - gstart[g], mask);
       bool fresh = true;
-      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e);
+      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e, mask);
       cnt += fresh;
     }
   }
