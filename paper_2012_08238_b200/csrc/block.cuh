@@ -168,15 +168,33 @@ struct MagKey {
   }
 };
 
+template <int NT, typename KeyF>
+__device__ void median_and_peak_k(KeyF key, int64_t B, double* med, double* peak, unsigned* hist,
+                                  long long* sh, double* redd, unsigned long long* redu);
+
+struct SmemKey {
+  const unsigned long long* k;
+  __device__ __forceinline__ unsigned long long operator()(int64_t i) const { return k[i]; }
+};
+
 // median of |v| (numpy: mean of the two middle values for even counts) and max.
 template <int NT>
 __device__ void median_and_peak(const double2* v, int64_t B, double* med, double* peak,
                                 unsigned* hist, long long* sh, double* redd,
                                 unsigned long long* redu) {
-  double m = 0.0;
-  for (int64_t i = threadIdx.x; i < B; i += NT) m = fmax(m, cabs_(v[i]));
-  *peak = block_max<NT>(m, redd);
   MagKey key{v};
+  median_and_peak_k<NT>(key, B, med, peak, hist, sh, redd, redu);
+}
+
+template <int NT, typename KeyF>
+__device__ void median_and_peak_k(KeyF key, int64_t B, double* med, double* peak, unsigned* hist,
+                                  long long* sh, double* redd, unsigned long long* redu) {
+  unsigned long long mx = 0;
+  for (int64_t i = threadIdx.x; i < B; i += NT) {
+    const unsigned long long u = key(i);
+    mx = u > mx ? u : mx;
+  }
+  *peak = __longlong_as_double((long long)(~block_min_u64<NT>(~mx, redu)));
   const int64_t k1 = (B - 1) / 2;
   long long below, equal;
   const unsigned long long u1 = block_radix_select<NT>(key, B, 0ull, k1, hist, sh, &below, &equal);

@@ -404,7 +404,20 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
     __syncthreads();
     if (live) {
       const int64_t tn = (T - t0 < kSubChunk) ? (T - t0) : kSubChunk;
-      for (int64_t j = 0; j < tn; ++j) {
+      // 8 table reads in flight, then the ordered subtraction
+      int64_t j = 0;
+      for (; j + 8 <= tn; j += 8) {
+        double2 w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          int64_t col = bk - s_q[j + u];
+          col += (col < 0) ? B : 0;
+          w[u] = __ldg(gt + s_row[j + u] * B + col);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = csub(acc, cmul(cmul(s_c[j + u], w[u]), s_ph[j + u]));
+      }
+      for (; j < tn; ++j) {
         int64_t col = bk - s_q[j];
         col += (col < 0) ? B : 0;
         const double2 w = __ldg(gt + s_row[j] * B + col);

@@ -248,8 +248,20 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
   const int it = S.it;
   const int64_t B = a.B;
   const double2* y0 = a.y + (int64_t)s * B;  // slot 0
+  unsigned long long* k1 = (unsigned long long*)dsm;
+  long long* k2 = (long long*)(k1 + kFusedMaxB);
+  int* pay = (int*)(k2 + kFusedMaxB);
+  const bool cached = B <= kFusedMaxB;
+  // |y0| bits cached in shared memory (k2) for the radix passes
+  unsigned long long* mg = (unsigned long long*)k2;
   double med, peak;
-  median_and_peak<kDecNT>(y0, B, &med, &peak, hist, sh, redd, redu);
+  if (cached) {
+    for (int64_t i = threadIdx.x; i < B; i += kDecNT) mg[i] = dbits(cabs_(y0[i]));
+    __syncthreads();
+    median_and_peak_k<kDecNT>(SmemKey{mg}, B, &med, &peak, hist, sh, redd, redu);
+  } else {
+    median_and_peak<kDecNT>(y0, B, &med, &peak, hist, sh, redd, redu);
+  }
   const double robust = fmax(fmax(fmin(3.0 * med, 0.25 * peak), 1e-9 * peak), 1e-300);
   const double sref = fmax(S.scale_ref, peak);
   const double fl = fmax(robust, 1e-9 * sref);
@@ -279,22 +291,24 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
   }
   if (conv) return;
   // heavy = {b : |y0[b]| >= floor} in (-|y0|, b) order
-  unsigned long long* k1 = (unsigned long long*)dsm;
-  long long* k2 = (long long*)(k1 + kFusedMaxB);
-  int* pay = (int*)(k2 + kFusedMaxB);
   const unsigned long long ufl = dbits(fl);
+  constexpr int kPer = kFusedMaxB / kDecNT;
   const int64_t per = (B + kDecNT - 1) / kDecNT;
   const int64_t i0 = threadIdx.x * per, i1 = min(B, i0 + per);
+  unsigned long long mine_u[kPer];
   int mine = 0;
-  for (int64_t i = i0; i < i1; ++i) mine += dbits(cabs_(y0[i])) >= ufl;
+  for (int64_t i = i0; i < i1; ++i) {
+    const unsigned long long u = cached ? mg[i] : dbits(cabs_(y0[i]));
+    if (cached) mine_u[i - i0] = u;
+    mine += u >= ufl;
+  }
   int total;
-  int off = block_exscan<kDecNT>(mine, redi, &total);
-  const bool sortable = B <= kFusedMaxB;
+  int off = block_exscan<kDecNT>(mine, redi, &total);  // also orders the mg reads before reuse
   int32_t* hv = a.heavy + (int64_t)s * B;
   for (int64_t i = i0; i < i1; ++i) {
-    const unsigned long long u = dbits(cabs_(y0[i]));
+    const unsigned long long u = cached ? mine_u[i - i0] : dbits(cabs_(y0[i]));
     if (u >= ufl) {
-      if (sortable) {
+      if (cached) {
         k1[off] = ~u;
         k2[off] = i;
         pay[off] = (int)i;
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
     }
   }
   __syncthreads();
-  if (sortable) {
+  if (cached) {
     int cap = 1;
     while (cap < total) cap <<= 1;
     block_bitonic<kDecNT>(k1, k2, pay, total, cap);
@@ -350,7 +364,23 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
     __syncthreads();
     if (live) {
       const int tn = (int)((te - t0 < kLocChunk) ? te - t0 : kLocChunk);
-      for (int tt = 0; tt < tn; ++tt) {
+      int tt = 0;
+      for (; tt + 4 <= tn; tt += 4) {
+        double2 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int64_t col = b - t_q[tt + u];
+          col += (col < 0) ? B : 0;
+          w[u] = __ldg(a.gt + t_row[tt + u] * B + col);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 cw = cmul(t_c[tt + u], w[u]);
+#pragma unroll
+          for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cmul(cw, t_ph[tt + u][j]));
+        }
+      }
+      for (; tt < tn; ++tt) {
         int64_t col = b - t_q[tt];
         col += (col < 0) ? B : 0;
         const double2 cw = cmul(t_c[tt], __ldg(a.gt + t_row[tt] * B + col));
@@ -657,11 +687,27 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
     __syncthreads();
     if (mine) {
       const int un = min(kPoChunk, T - u0);
-#pragma unroll 4
-      for (int q = 0; q < un; ++q) {
+      int q = 0;
+      for (; q + 8 <= un; q += 8) {
+        double2 w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          int64_t col = bi - u_q[q + u];
+          col += (col < 0) ? B : 0;
+          w[u] = __ldg(a.gt + u_row[q + u] * B + col);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 cw = cmul(u_c[q + u], w[u]);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q + u][d]));
+        }
+      }
+      for (; q < un; ++q) {
         int64_t col = bi - u_q[q];
         col += (col < 0) ? B : 0;
         const double2 cw = cmul(u_c[q], __ldg(a.gt + u_row[q] * B + col));
+#pragma unroll
         for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q][d]));
       }
     }

@@ -88,11 +88,25 @@ __global__ void __launch_bounds__(kVoNT) k_vo_est(VoteArgs a, int refine) {
       __syncthreads();
       if (live) {
         const int un = min(kVoChunk, C - u0);
-        for (int q = 0; q < un; ++q) {
+        // (c * w) * phase, subtracted in model order (frameworks.py:432-435);
+        // 8 table reads in flight
+        int q = 0;
+        for (; q + 8 <= un; q += 8) {
+          double2 wq[8], pq[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            int64_t col = b - u_q[q + u];
+            col += (col < 0) ? B : 0;
+            wq[u] = __ldg(a.gt + u_row[q + u] * B + col);
+            pq[u] = a.ph[base + u0 + q + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v = csub(v, cmul(cmul(u_cp[q + u], wq[u]), pq[u]));
+        }
+        for (; q < un; ++q) {
           int64_t col = b - u_q[q];
           col += (col < 0) ? B : 0;
           const double2 wq = __ldg(a.gt + u_row[q] * B + col);
-          // (c * w) * phase, subtracted in model order (frameworks.py:432-435)
           v = csub(v, cmul(cmul(u_cp[q], wq), a.ph[base + u0 + q]));
         }
       }
