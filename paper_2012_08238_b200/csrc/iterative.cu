@@ -796,6 +796,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * cap,     // 28 corr (polish)
       sizeof(int32_t) * (size_t)S * M,       // 29 item_active
       sizeof(int32_t) * (size_t)S,           // 30 pgate
+      sizeof(uint32_t) * (size_t)S * ((n + 31) / 32),  // 31 read bitmap (samples_read)
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -941,6 +942,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   int32_t* corr = (int32_t*)(w + Lo.off[28]);
   a.item_active = (int32_t*)(w + Lo.off[29]);
   a.pgate = (int32_t*)(w + Lo.off[30]);
+  uint32_t* bitmap = (uint32_t*)(w + Lo.off[31]);
   void* bws = w + Lo.total;
   const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
 
@@ -948,6 +950,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
   SFFT_CUDA(cudaMemsetAsync(a.stats, 0, sizeof(int32_t) * 8, st));
   SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
+  SFFT_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)S * ((n + 31) / 32), st));
 
   Prod p{};
   p.x = x;
@@ -1021,7 +1024,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
                                         out_coef, out_n, fin, rows);
     SFFT_CHECK_LAUNCH("k_finalize");
-    rc = run_union_count(a.groups, ngroups, S, n, out_samples, st, 64, fin, rows);
+    rc = run_union_bitmap(a.groups, ngroups, S, n, bitmap, out_samples, fin, rows, st);
     if (rc) return rc;
     if (out_sched) {
       k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched, fin, rows);

@@ -264,3 +264,91 @@ inline int run_union_count(const Group* groups, const int32_t* ngroups, int S, i
 }
 
 }  // namespace sfft
+
+namespace sfft {
+
+// Bitmap variant for the continuous engine: every read index of a finishing
+// slot is OR-ed into the slot's N-bit map (L2 atomics), then the map is
+// popcounted and cleared for the slot's next signal.  O(total reads) instead
+// of O(reads x groups) membership tests.
+static __global__ void __launch_bounds__(kUnionNT) k_mark_bits(
+    const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
+    uint32_t* bits, int64_t words, const int32_t* gate) {
+  __shared__ Group sg[kMaxGroups];
+  __shared__ GroupSh sp[kMaxGroups];
+  __shared__ int64_t gstart[kMaxGroups + 1];
+  const int s = blockIdx.y;
+  if (gate && !gate[s]) return;
+  const int G = min(ngroups[s], kMaxGroups);
+  const Group* gs = groups + (int64_t)s * gstride;
+  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
+  for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += kUnionNT) merge_pieces(sg[i], n, &sp[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int g = 0; g < G; ++g) {
+      gstart[g] = acc;
+      acc += sp[g].total;
+    }
+    gstart[G] = acc;
+  }
+  __syncthreads();
+  const int64_t all = gstart[G];
+  const int64_t per = (all + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = (int64_t)blockIdx.x * per;
+  const int64_t c1 = min(all, c0 + per);
+  uint32_t* b = bits + (int64_t)s * words;
+  for (int g = 0; g < G; ++g) {
+    const int64_t lo = max(c0, gstart[g]), hi = min(c1, gstart[g + 1]);
+    for (int64_t j = lo + threadIdx.x; j < hi; j += kUnionNT) {
+      const int64_t e = group_elem(sg[g], sp[g], n, j - gstart[g], mask);
+      atomicOr(&b[e >> 5], 1u << (e & 31));
+    }
+  }
+}
+
+static __global__ void k_popcount_clear(uint32_t* bits, int64_t words, const int32_t* gate,
+                                        const int32_t* rows, unsigned long long* samples) {
+  __shared__ unsigned long long red[32];
+  const int s = blockIdx.y;
+  if (gate && !gate[s]) return;
+  uint32_t* b = bits + (int64_t)s * words;
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = b[i];
+    if (v) {
+      c += __popc(v);
+      b[i] = 0u;
+    }
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += red[i];
+    if (t) atomicAdd(samples + (rows ? rows[s] : s), t);
+  }
+}
+
+// bits: [S][ceil(n/32)] zero on entry, zero again on return.
+inline int run_union_bitmap(const Group* groups, const int32_t* ngroups, int S, int64_t n,
+                            uint32_t* bits, int64_t* samples, const int32_t* gate,
+                            const int32_t* rows, cudaStream_t st) {
+  const int64_t words = (n + 31) / 32;
+  k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
+  SFFT_CHECK_LAUNCH("k_zero_rows");
+  k_mark_bits<<<dim3(64, S), kUnionNT, 0, st>>>(groups, ngroups, kMaxGroups, n, bits, words,
+                                                gate);
+  SFFT_CHECK_LAUNCH("k_mark_bits");
+  k_popcount_clear<<<dim3(32, S), 512, 0, st>>>(bits, words, gate, rows,
+                                                (unsigned long long*)samples);
+  SFFT_CHECK_LAUNCH("k_popcount_clear");
+  return 0;
+}
+
+}  // namespace sfft
