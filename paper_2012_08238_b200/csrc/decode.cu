@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
         for (int u = 0; u < 8; ++u) {
           int64_t col = bk - s_q[j + u];
           col += (col < 0) ? B : 0;
-          w[u] = __ldg(gt + s_row[j + u] * B + col);
+          w[u] = ld_table(gt + s_row[j + u] * B + col);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = csub(acc, cmul(cmul(s_c[j + u], w[u]), s_ph[j + u]));
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
       for (; j < tn; ++j) {
         int64_t col = bk - s_q[j];
         col += (col < 0) ? B : 0;
-        const double2 w = __ldg(gt + s_row[j] * B + col);
+        const double2 w = ld_table(gt + s_row[j] * B + col);
         acc = csub(acc, cmul(cmul(s_c[j], w), s_ph[j]));
       }
     }

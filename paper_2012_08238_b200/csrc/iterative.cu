@@ -371,7 +371,7 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
         for (int u = 0; u < 4; ++u) {
           int64_t col = b - t_q[tt + u];
           col += (col < 0) ? B : 0;
-          w[u] = __ldg(a.gt + t_row[tt + u] * B + col);
+          w[u] = ld_table(a.gt + t_row[tt + u] * B + col);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -383,7 +383,7 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
       for (; tt < tn; ++tt) {
         int64_t col = b - t_q[tt];
         col += (col < 0) ? B : 0;
-        const double2 cw = cmul(t_c[tt], __ldg(a.gt + t_row[tt] * B + col));
+        const double2 cw = cmul(t_c[tt], ld_table(a.gt + t_row[tt] * B + col));
 #pragma unroll
         for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cmul(cw, t_ph[tt][j]));
       }
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
         for (int u = 0; u < 8; ++u) {
           int64_t col = bi - u_q[q + u];
           col += (col < 0) ? B : 0;
-          w[u] = __ldg(a.gt + u_row[q + u] * B + col);
+          w[u] = ld_table(a.gt + u_row[q + u] * B + col);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
       for (; q < un; ++q) {
         int64_t col = bi - u_q[q];
         col += (col < 0) ? B : 0;
-        const double2 cw = cmul(u_c[q], __ldg(a.gt + u_row[q] * B + col));
+        const double2 cw = cmul(u_c[q], ld_table(a.gt + u_row[q] * B + col));
 #pragma unroll
         for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q][d]));
       }

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kVoNT) k_vo_est(VoteArgs a, int refine) {
           for (int u = 0; u < 8; ++u) {
             int64_t col = b - u_q[q + u];
             col += (col < 0) ? B : 0;
-            wq[u] = __ldg(a.gt + u_row[q + u] * B + col);
+            wq[u] = ld_table(a.gt + u_row[q + u] * B + col);
             pq[u] = a.ph[base + u0 + q + u];
           }
 #pragma unroll
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kVoNT) k_vo_est(VoteArgs a, int refine) {
         for (; q < un; ++q) {
           int64_t col = b - u_q[q];
           col += (col < 0) ? B : 0;
-          const double2 wq = __ldg(a.gt + u_row[q] * B + col);
+          const double2 wq = ld_table(a.gt + u_row[q] * B + col);
           v = csub(v, cmul(cmul(u_cp[q], wq), a.ph[base + u0 + q]));
         }
       }
