@@ -173,7 +173,6 @@ SFFT_HD double2 unit_root(int64_t n, int64_t e) {
 // reused only by the concurrently running shifted measurements), the flat
 // response table evict_last (every subtraction re-reads it), so the
 // streaming gathers do not push the table out of L2.
-#ifdef __CUDA_ARCH__
 __device__ __forceinline__ unsigned long long policy_evict_first() {
   unsigned long long p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -192,7 +191,6 @@ __device__ __forceinline__ double2 ld_table(const double2* p) {
                : "l"(p), "l"(policy_evict_last()));
   return v;
 }
-#endif
 
 template <typename T>
 struct Sample;
