@@ -169,10 +169,10 @@ SFFT_HD double2 unit_root(int64_t n, int64_t e) {
 // traffic (measured with ncu: lts sectors 4.3x l1tex sectors); .cg requests
 // single 32-byte sectors.
 //
-// L2 eviction policy: gathered signal lines are marked evict_first (they are
-// reused only by the concurrently running shifted measurements), the flat
-// response table evict_last (every subtraction re-reads it), so the
-// streaming gathers do not push the table out of L2.
+// L2 eviction policy: the flat response table is read with evict_last (every
+// subtraction re-reads it) so the streaming gathers do not push it out of L2.
+// (evict_first on the gathers was measured slower: it cuts the L2 reuse
+// between the concurrently running shifted measurements.)
 __device__ __forceinline__ unsigned long long policy_evict_first() {
   unsigned long long p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -197,21 +197,14 @@ struct Sample;
 template <>
 struct Sample<float2> {
   static __device__ __forceinline__ double2 load(const float2* p, int64_t i) {
-    float x, y;
-    asm volatile("ld.global.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
-                 : "=f"(x), "=f"(y)
-                 : "l"(p + i), "l"(policy_evict_first()));
-    return cmk((double)x, (double)y);
+    const float2 v = __ldcg(p + i);
+    return cmk((double)v.x, (double)v.y);
   }
 };
 template <>
 struct Sample<double2> {
   static __device__ __forceinline__ double2 load(const double2* p, int64_t i) {
-    double x, y;
-    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(x), "=d"(y)
-                 : "l"(p + i), "l"(policy_evict_first()));
-    return cmk(x, y);
+    return __ldcg(p + i);
   }
 };
 
