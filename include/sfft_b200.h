@@ -163,7 +163,8 @@ size_t sfft_iterative_ws_bytes(int64_t n, int64_t B, int64_t nslots, int64_t nsh
  * ladder_host (HOST int64[nladder]) is _phase_ladder(n).  Outputs per signal:
  * out_pos/out_coef [nsig][k] the top-k entries in (-|c|, f) order,
  * out_count, out_iterations, out_converged, out_samples (samples_read);
- * out_sched (optional) receives the read schedule, see sfft_schedule_layout.
+ * out_sched (optional) receives the read schedule, see sfft_schedule_layout;
+ * avail (optional) enables streaming admission, see sfft_set_avail.
  * Synchronises the stream once per round (one step of every busy slot). */
 int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
                        int64_t nslots, const double* taps, int64_t omega, int64_t B,
@@ -172,8 +173,14 @@ int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int
                        int64_t perm_stride, int64_t k, int64_t max_iterations,
                        const int64_t* ladder_host, int64_t nladder, int64_t cap, int64_t* out_pos,
                        void* out_coef, int32_t* out_count, int32_t* out_iterations,
-                       int32_t* out_converged, int64_t* out_samples, int64_t* out_sched, void* ws,
-                       size_t ws_bytes, void* stream);
+                       int32_t* out_converged, int64_t* out_samples, int64_t* out_sched,
+                       const int32_t* avail, void* ws, size_t ws_bytes, void* stream);
+
+/* Streaming admission for sfft_run_iterative: with avail != NULL the engine
+ * only admits signals [0, *avail); a copy stream publishes progress with
+ * sfft_set_avail after each chunk's host-to-device copy, so transfers overlap
+ * the compute of earlier signals. */
+int sfft_set_avail(int32_t* avail, int32_t value, void* stream);
 
 /* Workspace bytes of sfft_run_voting. */
 size_t sfft_voting_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t rounds, int64_t k,

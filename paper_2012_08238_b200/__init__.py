@@ -20,5 +20,6 @@ from .bucketize import (BucketSet, HashMapView, bucketize_flat, bucketize_flat_b
 __version__ = "0.1.0"
 from .reconstruct import VoteTable, robust_noise_floor, select_by_votes, vote_tally
 from .frameworks import (FRAMEWORKS, AlgorithmConfig, BatchResult, RecoveryResult,
-                         run_algorithm, run_iterative, run_iterative_batch, run_peeling,
+                         run_algorithm, run_iterative, run_iterative_batch,
+                         run_iterative_stream, run_peeling,
                          run_peeling_batch, run_voting, run_voting_batch)

@@ -108,7 +108,7 @@ SIGNATURES.update({
     "sfft_iterative_ws_bytes": (sz, [i64, i64, i64, i64, i64]),
     "sfft_run_iterative": (C.c_int, [C.c_int, vp, i64, i64, i64, i64, P_f64, i64, i64, vp, P_f64,
                                      vp, P_i64, P_i64, i64, i64, i64, i64, vp, i64, i64, P_i64,
-                                     vp, P_i32, P_i32, P_i32, P_i64, P_i64, vp, sz, vp]),
+                                     vp, P_i32, P_i32, P_i32, P_i64, P_i64, P_i32, vp, sz, vp]),
     "sfft_schedule_layout": (C.c_int, [vp, vp]),
 })
 SIGNATURES.update({
@@ -126,4 +126,7 @@ SIGNATURES.update({
     "sfft_peeling_ws_bytes": (sz, [i64, i64, vp, i64, i64]),
     "sfft_run_peeling": (C.c_int, [C.c_int, vp, i64, i64, i64, vp, i64, vp, i64, P_i64, vp,
                                    P_i32, P_i32, P_i32, P_i32, P_i64, P_i64, vp, sz, vp]),
+})
+SIGNATURES.update({
+    "sfft_set_avail": (C.c_int, [P_i32, C.c_int32, vp]),
 })

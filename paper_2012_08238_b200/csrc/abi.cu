@@ -256,8 +256,8 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
                                 const int64_t* ladder_host, int64_t nladder, int64_t cap,
                                 int64_t* out_pos, void* out_coef, int32_t* out_count,
                                 int32_t* out_iterations, int32_t* out_converged,
-                                int64_t* out_samples, int64_t* out_sched, void* ws,
-                                size_t ws_bytes, void* stream) {
+                                int64_t* out_samples, int64_t* out_sched,
+                                const int32_t* avail, void* ws, size_t ws_bytes, void* stream) {
   SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_iterative: dtype must be 0 or 1");
   SFFT_REQUIRE(x && taps && gtable && gmax && W && perm_sigma && perm_tau && ladder_host,
                "sfft_run_iterative: null pointer");
@@ -270,8 +270,8 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
                        B, (const double2*)gtable, gmax, (const double2*)W, perm_sigma, perm_tau,
                        (int)nperm, perm_stride, k, (int)max_iterations, ladder_host,
                        (int)nladder, (int)cap, out_pos, (double2*)out_coef, out_count,
-                       out_iterations, out_converged, out_samples, out_sched, ws, ws_bytes,
-                       (cudaStream_t)stream);
+                       out_iterations, out_converged, out_samples, out_sched, avail, ws,
+                       ws_bytes, (cudaStream_t)stream);
 }
 
 SFFT_API size_t sfft_voting_ws_bytes(int64_t n, int64_t B, int64_t nsig, int64_t rounds,
@@ -331,4 +331,15 @@ SFFT_API int sfft_run_peeling(int dtype, const void* x, int64_t n, int64_t xstri
                      (const double2* const*)W_stages_host, k, out_pos, (double2*)out_coef,
                      out_count, out_iterations, out_converged, out_error, out_samples, out_sched,
                      ws, ws_bytes, (cudaStream_t)stream);
+}
+
+// Publish "signals [0, value) have arrived" for streaming admission (run on
+// the copy stream after each chunk's host-to-device copy).
+__global__ void k_set_avail(int32_t* avail, int32_t value) { *avail = value; }
+
+SFFT_API int sfft_set_avail(int32_t* avail, int32_t value, void* stream) {
+  SFFT_REQUIRE(avail, "sfft_set_avail: null pointer");
+  k_set_avail<<<1, 1, 0, (cudaStream_t)stream>>>(avail, value);
+  SFFT_CHECK_LAUNCH("k_set_avail");
+  return 0;
 }

@@ -52,6 +52,7 @@ struct IterArgs {
   int64_t n, B, L, omega, k;
   int S, P, M, max_it, cap;      // S slots; cap = recovered capacity per slot
   int Q;                         // signals in the queue
+  const int32_t* avail;          // optional: signals [0, *avail) have arrived in HBM
   int64_t pstride;               // perms row stride per signal (0: shared stream)
   int32_t* item_active;          // [S*M]
   int32_t* pgate;                // [S] polish pass this round
@@ -131,9 +132,12 @@ __global__ void k_cb_admit(IterArgs a) {
   if (s >= a.S) return;
   IterState& S = a.st[s];
   if (S.phase != PH_FREE) return;
+  // signals still being copied in (streaming admission) are not taken yet
+  const int lim = a.avail ? min(a.Q, *(volatile const int32_t*)a.avail) : a.Q;
   const int idx = atomicAdd(a.stats + 4, 1);
-  if (idx >= a.Q) {
-    S.phase = PH_IDLE;
+  if (idx >= lim) {
+    atomicSub(a.stats + 4, 1);
+    if (lim >= a.Q) S.phase = PH_IDLE;
     return;
   }
   S = IterState{};
@@ -878,7 +882,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
                   int P, int64_t pstride, int64_t k, int max_it, const int64_t* ladder, int nlad,
                   int cap, int64_t* out_pos, double2* out_coef, int32_t* out_n,
                   int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
-                  int64_t* out_sched, void* ws, size_t ws_bytes, cudaStream_t st) {
+                  int64_t* out_sched, const int32_t* avail, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
   const int M = 1 + nlad;
   SFFT_REQUIRE(M <= kMaxShifts, "iterative: ladder too long");
   SFFT_REQUIRE(max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
@@ -896,6 +901,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.k = k;
   a.S = S;
   a.Q = Q;
+  a.avail = avail;
   a.P = P;
   a.pstride = pstride;
   a.M = M;
@@ -973,7 +979,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   const unsigned sb = (unsigned)cdiv_up(S, 128);
   int t_max = 0;  // largest recovered list seen (host copy, refreshed every round)
   int h_max = 0;  // largest heavy list seen
-  const int max_rounds = (Q / S + 2) * (max_it + 8) + 16;
+  // streaming admission may spend rounds waiting for data: no round cap then
+  const int max_rounds = avail ? (1 << 30) : (Q / S + 2) * (max_it + 8) + 16;
   int round = 0;
   for (; round < max_rounds; ++round) {
     k_cb_admit<<<sb, 128, 0, st>>>(a);

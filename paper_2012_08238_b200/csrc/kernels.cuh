@@ -118,6 +118,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
                   int P, int64_t pstride, int64_t k, int max_it, const int64_t* ladder, int nlad,
                   int cap, int64_t* out_pos, double2* out_coef, int32_t* out_n,
                   int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
-                  int64_t* out_sched, void* ws, size_t ws_bytes, cudaStream_t st);
+                  int64_t* out_sched, const int32_t* avail, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
 
 }  // namespace sfft

@@ -243,12 +243,14 @@ class _WS:
 DEFAULT_SLOTS = 128
 
 
-def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = None) -> BatchResult:
+def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = None,
+                        avail=None) -> BatchResult:
     """run_iterative (phase location) for every row of ``xs``.
 
     The device engine keeps ``slots`` signals in flight (default
     min(len(xs), 128)) and refills a slot from the queue as soon as its signal
-    finishes, so long-running signals never idle the GPU."""
+    finishes, so long-running signals never idle the GPU.  ``avail`` (device
+    int32 scalar) enables streaming admission (see run_iterative_stream)."""
     import torch
     cfg = cfg.validated()
     if cfg.framework != "iterative":
@@ -290,9 +292,34 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
                                ptr(twiddles(b, dev)), ptr(psig), ptr(ptau), P, 0, k,
                                cfg.max_iterations, lad, len(ladder), cap,
                                ptr(out_pos), ptr(out_coef), ptr(out_n), ptr(out_it), ptr(out_cv),
-                               ptr(out_sm), ptr(sched), ptr(ws), wsb, stream_of(dev)),
-          "sfft_run_iterative")
+                               ptr(out_sm), ptr(sched), ptr(avail), ptr(ws), wsb,
+                               stream_of(dev)), "sfft_run_iterative")
     return BatchResult(n, k, out_pos, out_coef, out_n, out_it, out_cv, out_sm, sched)
+
+
+def run_iterative_stream(host_x, k: int, cfg: AlgorithmConfig, slots: int | None = None,
+                         chunk: int = 64, out=None) -> BatchResult:
+    """End-to-end batch from host memory: rows of ``host_x`` (pinned CPU tensor
+    [Q][N], complex64/complex128) are copied to the device chunk by chunk on a
+    side stream while the engine already works on the rows that arrived
+    (streaming admission), so the transfer overlaps the compute."""
+    import torch
+    from ._lib import require_cuda
+    dev = require_cuda()
+    Q, n = host_x.shape
+    X = out if out is not None else torch.empty((Q, n), dtype=host_x.dtype, device=dev)
+    avail = torch.zeros(1, dtype=torch.int32, device=dev)
+    cs = torch.cuda.Stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    L = lib()
+    with torch.cuda.stream(cs):
+        for c0 in range(0, Q, chunk):
+            c1 = min(Q, c0 + chunk)
+            X[c0:c1].copy_(host_x[c0:c1], non_blocking=True)
+            check(L.sfft_set_avail(ptr(avail), c1, cs.cuda_stream), "sfft_set_avail")
+    br = run_iterative_batch(X, k, cfg, slots=slots, avail=avail)
+    torch.cuda.current_stream(dev).wait_stream(cs)
+    return br
 
 
 def run_iterative(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:

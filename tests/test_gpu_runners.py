@@ -182,3 +182,18 @@ def test_iterative_continuous_batching(sb, slots):
         assert got.samples_read == rec["samples_read"]
         assert got.iterations == rec["iterations"]
         assert got.converged == rec["converged"]
+
+
+def test_iterative_stream_from_host(sb):
+    """Streaming admission: rows copied from pinned host memory chunk by chunk
+    while the engine runs give the same results as the resident batch."""
+    import torch
+    cases = [c for c in CASES if c[0]["name"].startswith("C1")]
+    Xh = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).pin_memory()
+    cfg = _cfg(sb, cases[0][0])
+    res = sb.run_iterative_stream(Xh, 16, cfg, slots=2, chunk=1).to_results()
+    for (rec, arr), got in zip(cases, res):
+        want = dict(zip(arr["pos"].tolist(), arr["coef"].tolist()))
+        assert set(got.spectrum.entries) == set(want), rec["name"]
+        assert got.samples_read == rec["samples_read"]
+        assert got.iterations == rec["iterations"]
