@@ -359,19 +359,23 @@ int run_energy_est(const double2* y, int64_t B, const double2* gt, const double*
 constexpr int kSubNT = 256;
 constexpr int kSubChunk = 256;
 
+// Two buckets per thread (consecutive for full subtractions, so a warp reads
+// 1 KB contiguous of each table row); a_t = c_t * w^{tau m_t} is formed once
+// per tone in shared memory (the reference forms (c*w)*phase: same value up
+// to rounding).
+constexpr int kSubBPT = 2;
+
 __global__ void __launch_bounds__(kSubNT) k_subtract(
     const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
     const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
     const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
     const int32_t* tcount, int64_t tstride, const int32_t* gate, double2* __restrict__ part) {
-  __shared__ int64_t s_row[kSubChunk];
-  __shared__ int64_t s_q[kSubChunk];
-  __shared__ double2 s_c[kSubChunk];
-  __shared__ double2 s_ph[kSubChunk];
+  __shared__ int32_t s_row[kSubChunk];
+  __shared__ int32_t s_q[kSubChunk];
+  __shared__ double2 s_a[kSubChunk];
   const int item = blockIdx.y;
   const int sig = item_sig ? item_sig[item] : item;
   if (gate && !gate[sig]) return;
-  const int64_t i = (int64_t)blockIdx.x * kSubNT + threadIdx.x;
   const int64_t L = n / B;
   const int64_t sg = sigma[item];
   const int64_t tt = tau_tot[item];
@@ -385,49 +389,66 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
   const int64_t T = te > tb ? te - tb : 0;
   const int64_t* tp = tpos + (int64_t)sig * tstride + tb;
   const double2* tc = tcoef + (int64_t)sig * tstride + tb;
-  int64_t bk = 0;
-  double2 acc = cmk(0.0, 0.0);
-  const bool live = i < nb;
-  if (live) {
-    bk = blist ? blist[(int64_t)item * nb + i] : i;
-    if (TS == 1) acc = y[(int64_t)item * B + bk];
+  const int64_t i0 = ((int64_t)blockIdx.x * kSubNT + threadIdx.x) * kSubBPT;
+  int bk[kSubBPT];
+  bool live[kSubBPT];
+  double2 acc[kSubBPT];
+#pragma unroll
+  for (int u = 0; u < kSubBPT; ++u) {
+    const int64_t i = i0 + u;
+    live[u] = i < nb;
+    bk[u] = live[u] ? (int)(blist ? blist[(int64_t)item * nb + i] : i) : 0;
+    acc[u] = (live[u] && TS == 1) ? y[(int64_t)item * B + bk[u]] : cmk(0.0, 0.0);
   }
+  const int Bi = (int)B;
   for (int64_t t0 = 0; t0 < T; t0 += kSubChunk) {
     __syncthreads();
     for (int j = threadIdx.x; j < kSubChunk && t0 + j < T; j += kSubNT) {
       const int64_t m = mulmod(sg, pmod(tp[t0 + j], n), n);
-      s_row[j] = (L - m % L) % L;
-      s_q[j] = (m + L - 1) / L;
-      s_c[j] = tc[t0 + j];
-      s_ph[j] = unit_root(n, mulmod(tt, m, n));
+      s_row[j] = (int)((L - m % L) % L);
+      s_q[j] = (int)((m + L - 1) / L);
+      s_a[j] = cmul(tc[t0 + j], unit_root(n, mulmod(tt, m, n)));
     }
     __syncthreads();
-    if (live) {
-      const int64_t tn = (T - t0 < kSubChunk) ? (T - t0) : kSubChunk;
-      // 8 table reads in flight, then the ordered subtraction
-      int64_t j = 0;
-      for (; j + 8 <= tn; j += 8) {
-        double2 w[8];
+    if (live[0]) {
+      const int tn = (int)((T - t0 < kSubChunk) ? (T - t0) : kSubChunk);
+      // 4 tones x 2 buckets of table reads in flight, then the ordered updates
+      int j = 0;
+      for (; j + 4 <= tn; j += 4) {
+        double2 w[4][kSubBPT];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          int64_t col = bk - s_q[j + u];
-          col += (col < 0) ? B : 0;
-          w[u] = ld_table(gt + s_row[j + u] * B + col);
+        for (int v = 0; v < 4; ++v) {
+          const double2* row = gt + (int64_t)s_row[j + v] * B;
+#pragma unroll
+          for (int u = 0; u < kSubBPT; ++u) {
+            int col = bk[u] - s_q[j + v];
+            col += (col < 0) ? Bi : 0;
+            w[v][u] = ld_table(row + col);
+          }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = csub(acc, cmul(cmul(s_c[j + u], w[u]), s_ph[j + u]));
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int u = 0; u < kSubBPT; ++u) acc[u] = csub(acc[u], cmul(s_a[j + v], w[v][u]));
       }
       for (; j < tn; ++j) {
-        int64_t col = bk - s_q[j];
-        col += (col < 0) ? B : 0;
-        const double2 w = ld_table(gt + s_row[j] * B + col);
-        acc = csub(acc, cmul(cmul(s_c[j], w), s_ph[j]));
+        const double2* row = gt + (int64_t)s_row[j] * B;
+#pragma unroll
+        for (int u = 0; u < kSubBPT; ++u) {
+          int col = bk[u] - s_q[j];
+          col += (col < 0) ? Bi : 0;
+          acc[u] = csub(acc[u], cmul(s_a[j], ld_table(row + col)));
+        }
       }
     }
   }
-  if (!live) return;
-  if (TS == 1) out[(int64_t)item * nb + i] = acc;
-  else part[((int64_t)item * TS + blockIdx.z) * nb + i] = acc;
+#pragma unroll
+  for (int u = 0; u < kSubBPT; ++u) {
+    if (!live[u]) continue;
+    const int64_t i = i0 + u;
+    if (TS == 1) out[(int64_t)item * nb + i] = acc[u];
+    else part[((int64_t)item * TS + blockIdx.z) * nb + i] = acc[u];
+  }
 }
 
 // out = y + sum of the (negated) split partial sums, in split order.
@@ -453,7 +474,7 @@ int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        double2* part) {
   if (nitems <= 0 || nb <= 0) return 0;
   if (TS < 1 || !part) TS = 1;
-  dim3 g((unsigned)cdiv_up(nb, kSubNT), (unsigned)nitems, (unsigned)TS);
+  dim3 g((unsigned)cdiv_up(nb, (int64_t)kSubNT * kSubBPT), (unsigned)nitems, (unsigned)TS);
   k_subtract<<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma, tau_tot, tpos,
                                    tcoef, tcount, tstride, gate, part);
   SFFT_CHECK_LAUNCH("k_subtract");
