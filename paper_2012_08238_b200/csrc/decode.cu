@@ -364,6 +364,12 @@ constexpr int kSubChunk = 256;
 // per tone in shared memory (the reference forms (c*w)*phase: same value up
 // to rounding).
 constexpr int kSubBPT = 2;
+constexpr int kSubPerSplit = 512;  // tones per split
+
+__device__ __forceinline__ int sub_splits(int64_t T, int maxTS) {
+  const int64_t z = (T + kSubPerSplit - 1) / kSubPerSplit;
+  return (int)(z < 1 ? 1 : (z > maxTS ? maxTS : z));
+}
 
 __global__ void __launch_bounds__(kSubNT) k_subtract(
     const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
@@ -380,9 +386,11 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
   const int64_t sg = sigma[item];
   const int64_t tt = tau_tot[item];
   const int64_t Tall = tcount[sig];
-  // tone split z of gridDim.z: tones [tb, te); with one split the running
-  // value starts at y and the tones are subtracted in order (reference order)
-  const int TS = gridDim.z;
+  // tone split z < TS of this item's own tone count (gridDim.z = the largest
+  // split count); with one split the running value starts at y and the tones
+  // are subtracted in order (reference order)
+  const int TS = sub_splits(Tall, gridDim.z);
+  if ((int)blockIdx.z >= TS) return;
   const int64_t per = (Tall + TS - 1) / TS;
   const int64_t tb = (int64_t)blockIdx.z * per;
   const int64_t te = (tb + per < Tall) ? tb + per : Tall;
@@ -447,22 +455,25 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
     if (!live[u]) continue;
     const int64_t i = i0 + u;
     if (TS == 1) out[(int64_t)item * nb + i] = acc[u];
-    else part[((int64_t)item * TS + blockIdx.z) * nb + i] = acc[u];
+    else part[((int64_t)item * gridDim.z + blockIdx.z) * nb + i] = acc[u];
   }
 }
 
 // out = y + sum of the (negated) split partial sums, in split order.
 __global__ void k_sub_reduce(const double2* __restrict__ y, double2* __restrict__ out, int64_t B,
                              int64_t nb, const int32_t* blist, const int32_t* item_sig,
-                             const int32_t* gate, const double2* __restrict__ part, int TS) {
+                             const int32_t* gate, const double2* __restrict__ part, int maxTS,
+                             const int32_t* tcount) {
   const int item = blockIdx.y;
   const int sig = item_sig ? item_sig[item] : item;
   if (gate && !gate[sig]) return;
+  const int TS = sub_splits(tcount[sig], maxTS);
+  if (TS == 1) return;  // written in place by k_subtract
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nb) return;
   const int64_t bk = blist ? blist[(int64_t)item * nb + i] : i;
   double2 acc = cmk(0.0, 0.0);
-  for (int t = 0; t < TS; ++t) acc = cadd(acc, part[((int64_t)item * TS + t) * nb + i]);
+  for (int t = 0; t < TS; ++t) acc = cadd(acc, part[((int64_t)item * maxTS + t) * nb + i]);
   out[(int64_t)item * nb + i] = cadd(y[(int64_t)item * B + bk], acc);
 }
 
@@ -480,7 +491,7 @@ int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
   SFFT_CHECK_LAUNCH("k_subtract");
   if (TS > 1) {
     dim3 g2((unsigned)cdiv_up(nb, 256), (unsigned)nitems);
-    k_sub_reduce<<<g2, 256, 0, st>>>(y, out, B, nb, blist, item_sig, gate, part, TS);
+    k_sub_reduce<<<g2, 256, 0, st>>>(y, out, B, nb, blist, item_sig, gate, part, TS, tcount);
     SFFT_CHECK_LAUNCH("k_sub_reduce");
   }
   return 0;

@@ -395,6 +395,15 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
   }
 }
 
+constexpr int kLadPerSplit = 256;  // tones per split
+
+// splits of a slot's ladder model (0: small list, subtracted inline)
+__device__ __forceinline__ int lad_splits(int64_t T, int maxTS) {
+  if (T <= kLadPerSplit || maxTS <= 0) return 0;
+  const int64_t z = (T + kLadPerSplit - 1) / kLadPerSplit;
+  return (int)(z > maxTS ? maxTS : z);
+}
+
 // Tone-split partial ladder sums for large recovered lists:
 // part[s][z][h][j-1] = -sum_{tones of split z} c w ph_j.
 template <int M>
@@ -409,8 +418,9 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   if (h0 >= nh) return;
   const int h = h0 + threadIdx.x;
   const bool live = h < nh;
-  const int TS = gridDim.z;
   const int64_t T = a.rec_count[s];
+  const int TS = lad_splits(T, gridDim.z);
+  if ((int)blockIdx.z >= TS) return;  // TS == 0: k_it_locate subtracts inline
   const int64_t per = (T + TS - 1) / TS;
   const int64_t tb = (int64_t)blockIdx.z * per;
   const int64_t te = (tb + per < T) ? tb + per : T;
@@ -420,7 +430,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   for (int j = 0; j < M; ++j) ys[j] = cmk(0.0, 0.0);
   ladder_model<M>(a, s, b, live, tb, te, ys, t_row, t_q, t_c, t_ph);
   if (!live) return;
-  double2* o = a.part + (((int64_t)s * TS + blockIdx.z) * a.B + h) * (M - 1);
+  double2* o = a.part + (((int64_t)s * gridDim.z + blockIdx.z) * a.B + h) * (M - 1);
 #pragma unroll
   for (int j = 1; j < M; ++j) o[j - 1] = ys[j];
 }
@@ -430,7 +440,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
 // TS == 0: the model is subtracted here in tone order; TS > 0: summed from
 // k_it_ladder_part's splits.
 template <int M>
-__global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
+__global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
   __shared__ double2 t_ph[kLocChunk][kMaxShifts];
@@ -449,11 +459,12 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int TS) {
   double2 ys[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
+  const int TS = lad_splits(a.rec_count[s], maxTS);
   if (TS == 0) {
     ladder_model<M>(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_c, t_ph);
   } else if (live) {
     for (int z = 0; z < TS; ++z) {
-      const double2* p = a.part + (((int64_t)s * TS + z) * B + h) * (M - 1);
+      const double2* p = a.part + (((int64_t)s * maxTS + z) * B + h) * (M - 1);
 #pragma unroll
       for (int j = 1; j < M; ++j) ys[j] = cadd(ys[j], p[j - 1]);
     }
