@@ -76,7 +76,9 @@ struct IterArgs {
   int64_t* rec_pos;              // [S][cap]
   double2* rec_coef;             // [S][cap]
   int32_t* rec_count;            // [S]
-  int32_t* heavy;                // [S][B]
+  int32_t* heavy;                // [S][B] heavy buckets in (-|y0|, b) order (merge order)
+  int32_t* heavy_b;              // [S][B] heavy buckets in bucket order (coalesced table reads)
+  int32_t* hrank;                // [S][B] position of bucket b in the (-|y0|, b) order
   int64_t* f_pos;                // [S][B] per heavy index
   double2* f_coef;               // [S][B]
   int32_t* f_ok;                 // [S][B]
@@ -309,9 +311,11 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
   int total;
   int off = block_exscan<kDecNT>(mine, redi, &total);  // also orders the mg reads before reuse
   int32_t* hv = a.heavy + (int64_t)s * B;
+  int32_t* hb = a.heavy_b + (int64_t)s * B;
   for (int64_t i = i0; i < i1; ++i) {
     const unsigned long long u = cached ? mine_u[i - i0] : dbits(cabs_(y0[i]));
     if (u >= ufl) {
+      hb[off] = (int)i;
       if (cached) {
         k1[off] = ~u;
         k2[off] = i;
@@ -327,7 +331,12 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
     int cap = 1;
     while (cap < total) cap <<= 1;
     block_bitonic<kDecNT>(k1, k2, pay, total, cap);
-    for (int i = threadIdx.x; i < total; i += kDecNT) hv[i] = pay[i];
+    for (int i = threadIdx.x; i < total; i += kDecNT) {
+      hv[i] = pay[i];
+      a.hrank[(int64_t)s * B + pay[i]] = i;
+    }
+  } else {
+    for (int i = threadIdx.x; i < total; i += kDecNT) a.hrank[(int64_t)s * B + hv[i]] = i;
   }
   if (threadIdx.x == 0) {
     S.nheavy = total;
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   const int64_t per = (T + TS - 1) / TS;
   const int64_t tb = (int64_t)blockIdx.z * per;
   const int64_t te = (tb + per < T) ? tb + per : T;
-  const int b = live ? a.heavy[(int64_t)s * a.B + h] : 0;
+  const int b = live ? a.heavy_b[(int64_t)s * a.B + h] : 0;
   double2 ys[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) ys[j] = cmk(0.0, 0.0);
@@ -455,7 +464,9 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   const int64_t n = a.n, B = a.B, L = a.L;
   const int64_t sigma = a.item_sigma[s];
   const int64_t tau = a.item_tau[s];  // shift 0 item
-  const int b = live ? a.heavy[(int64_t)s * B + h] : 0;
+  // heavy buckets are visited in bucket order (coalesced table rows); the
+  // result goes to the bucket's rank in the (-|y0|, b) order used by merge
+  const int b = live ? a.heavy_b[(int64_t)s * B + h] : 0;
   double2 ys[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
@@ -470,7 +481,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
     }
   }
   if (!live) return;
-  const int64_t fi = (int64_t)s * B + h;
+  const int64_t fi = (int64_t)s * B + a.hrank[(int64_t)s * B + b];
   a.f_ok[fi] = 0;
   const double2 y0 = ys[0];
   // _unwrap_position (frameworks.py:179-196): ladder[0] == 1
@@ -812,6 +823,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * M,       // 29 item_active
       sizeof(int32_t) * (size_t)S,           // 30 pgate
       sizeof(uint32_t) * (size_t)S * ((n + 31) / 32),  // 31 read bitmap (samples_read)
+      sizeof(int32_t) * (size_t)S * B,       // 32 heavy_b
+      sizeof(int32_t) * (size_t)S * B,       // 33 hrank
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -960,6 +973,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.item_active = (int32_t*)(w + Lo.off[29]);
   a.pgate = (int32_t*)(w + Lo.off[30]);
   uint32_t* bitmap = (uint32_t*)(w + Lo.off[31]);
+  a.heavy_b = (int32_t*)(w + Lo.off[32]);
+  a.hrank = (int32_t*)(w + Lo.off[33]);
   void* bws = w + Lo.total;
   const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
 
