@@ -40,8 +40,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256, help="signals per step (queue length)")
-    ap.add_argument("--slots", type=int, default=128, help="device slots kept in flight")
+    ap.add_argument("--batch", type=int, default=2048, help="signals per step (queue length)")
+    ap.add_argument("--slots", type=int, default=512, help="device slots kept in flight")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="signals in the CPU-baseline sample (0: one per host core, max 32)")
