@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=2048, help="signals per step (queue length)")
     ap.add_argument("--slots", type=int, default=512, help="device slots kept in flight")
+    ap.add_argument("--engines", type=int, default=1, help="concurrent engines (streams)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="signals in the CPU-baseline sample (0: one per host core, max 32)")
@@ -230,7 +231,7 @@ def main():
     st = torch.cuda.current_stream(dev)
 
     def step(xs):
-        return sb.run_iterative_batch(xs, K, cfg, slots=args.slots)
+        return sb.run_iterative_batch(xs, K, cfg, slots=args.slots, engines=args.engines)
 
     for _ in range(args.warmup):
         br = step(X)
@@ -313,7 +314,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c64",
             "data": "synthetic (seeded gen_signal positions/phases, device AWGN)",
-            "config": {"workload": WORKLOAD, "batch_per_gpu": S, "slots": args.slots, "n": N, "k": K,
+            "config": {"workload": WORKLOAD, "batch_per_gpu": S, "slots": args.slots, "engines": args.engines, "n": N, "k": K,
                        "num_buckets": B, "omega": omega, "parallelism": f"replicas{world}",
                        "l2": "inputs larger than L2 (%.1f GB per GPU)" % (S * N * 8 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -481,6 +481,7 @@ int prof_end(cudaStream_t st, cudaEvent_t ev0) {
   cudaEvent_t ev1;
   SFFT_CUDA(cudaEventCreate(&ev1));
   SFFT_CUDA(cudaEventRecord(ev1, st));
+  std::lock_guard<std::mutex> lk(bucket_prof().mu);
   bucket_prof().pending.push_back({ev0, ev1});
   bucket_prof().launches += 1;
   return 0;
@@ -488,6 +489,7 @@ int prof_end(cudaStream_t st, cudaEvent_t ev0) {
 
 int prof_collect() {
   BucketProf& p = bucket_prof();
+  std::lock_guard<std::mutex> lk(p.mu);
   for (auto& e : p.pending) {
     SFFT_CUDA(cudaEventSynchronize(e.second));
     float ms = 0.f;

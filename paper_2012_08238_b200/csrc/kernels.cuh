@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "fft.cuh"
@@ -41,6 +42,7 @@ struct BucketProf {
   double ms = 0.0;
   long long launches = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;  // read at prof_collect
+  std::mutex mu;
 };
 BucketProf& bucket_prof();
 int prof_collect();

@@ -227,9 +227,9 @@ class _WS:
     buf: dict = {}
 
     @classmethod
-    def get(cls, nbytes, device):
+    def get(cls, nbytes, device, tag: str = ""):
         import torch
-        key = str(device)
+        key = str(device) + tag
         t = cls.buf.get(key)
         if t is None or t.numel() < nbytes:
             cls.buf.pop(key, None)
@@ -244,13 +244,18 @@ DEFAULT_SLOTS = 128
 
 
 def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = None,
-                        avail=None) -> BatchResult:
+                        avail=None, engines: int = 1) -> BatchResult:
     """run_iterative (phase location) for every row of ``xs``.
 
     The device engine keeps ``slots`` signals in flight (default
     min(len(xs), 128)) and refills a slot from the queue as soon as its signal
     finishes, so long-running signals never idle the GPU.  ``avail`` (device
-    int32 scalar) enables streaming admission (see run_iterative_stream)."""
+    int32 scalar) enables streaming admission (see run_iterative_stream).
+    ``engines`` > 1 splits the queue over that many engines on their own CUDA
+    streams (host threads; ctypes releases the GIL), so one engine's
+    memory-bound gathers overlap another's FP64 subtraction kernels."""
+    if engines > 1 and avail is None:
+        return _iterative_engines(xs, k, cfg, slots, engines)
     import torch
     cfg = cfg.validated()
     if cfg.framework != "iterative":
@@ -282,7 +287,7 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
     sched = _sched_buffer(S, dev)
     L = lib()
     wsb = L.sfft_iterative_ws_bytes(n, b, nslots, M, cap)
-    ws = _WS.get(wsb, dev)
+    ws = _WS.get(wsb, dev, tag=f"it{torch.cuda.current_stream(dev).cuda_stream}")
     import ctypes
     lad = (ctypes.c_int64 * len(ladder))(*ladder)
     dt = 0 if X.dtype == torch.complex64 else 1
@@ -295,6 +300,45 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
                                ptr(out_sm), ptr(sched), ptr(avail), ptr(ws), wsb,
                                stream_of(dev)), "sfft_run_iterative")
     return BatchResult(n, k, out_pos, out_coef, out_n, out_it, out_cv, out_sm, sched)
+
+
+def _iterative_engines(xs, k, cfg, slots, engines):
+    import threading
+
+    import torch
+    X, _ = _as_batch(xs)
+    S = X.shape[0]
+    dev = X.device
+    parts = [(i * S // engines, (i + 1) * S // engines) for i in range(engines)]
+    parts = [p for p in parts if p[1] > p[0]]
+    per_slots = max(1, (slots or DEFAULT_SLOTS) // len(parts))
+    main = torch.cuda.current_stream(dev)
+    streams = [torch.cuda.Stream(dev) for _ in parts]
+    out = [None] * len(parts)
+    err = []
+
+    def work(i):
+        try:
+            with torch.cuda.device(dev), torch.cuda.stream(streams[i]):
+                streams[i].wait_stream(main)
+                lo, hi = parts[i]
+                out[i] = run_iterative_batch(X[lo:hi], k, cfg, slots=per_slots)
+        except Exception as e:  # re-raised on the caller's thread
+            err.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(parts))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    for s in streams:
+        main.wait_stream(s)
+    cat = lambda f: torch.cat([getattr(o, f) for o in out])
+    return BatchResult(out[0].n, out[0].k, cat("pos"), cat("coef"), cat("count"),
+                       cat("iterations"), cat("converged"), cat("samples_read"),
+                       cat("schedule"))
 
 
 def run_iterative_stream(host_x, k: int, cfg: AlgorithmConfig, slots: int | None = None,
