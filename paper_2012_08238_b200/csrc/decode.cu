@@ -364,7 +364,7 @@ constexpr int kSubChunk = 256;
 // per tone in shared memory (the reference forms (c*w)*phase: same value up
 // to rounding).
 constexpr int kSubBPT = 2;
-constexpr int kSubPerSplit = 512;  // tones per split
+constexpr int kSubPerSplit = 128;  // tones per split
 
 __device__ __forceinline__ int sub_splits(int64_t T, int maxTS) {
   const int64_t z = (T + kSubPerSplit - 1) / kSubPerSplit;

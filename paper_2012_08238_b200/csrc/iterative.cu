@@ -1024,7 +1024,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     // ---- loop slots
     rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st,
-                            splits(t_max, 512, kMaxSubSplit), a.part);
+                            splits(t_max, 128, kMaxSubSplit), a.part);
     if (rc) return rc;
     k_it_decide<<<S, kDecNT, dsm, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_decide");
@@ -1035,7 +1035,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CHECK_LAUNCH("k_it_merge");
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
-                            splits(h_max, 512, kMaxSubSplit), a.part);
+                            splits(h_max, 128, kMaxSubSplit), a.part);
     if (rc) return rc;
     k_it_resid<<<S, kDecNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_resid");
