@@ -118,7 +118,8 @@ def run_reference(args):
     cb["value"] = value
     line = {"metric": "sFFT transforms/s (N=2^22, K=256, C3)", "value": value,
             "unit": "transforms/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * (args.cpu_sample or min(
+                len(os.sched_getaffinity(0)), 32)) / value, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": WORKLOAD, "n": N, "k": K, "num_buckets": B},
