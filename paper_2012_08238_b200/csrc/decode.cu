@@ -269,6 +269,240 @@ __global__ void __launch_bounds__(kVoteNT) k_votes_emit(VoteRounds vr, const int
   (void)cand_count;
 }
 
+// ---------------------------------------------------------------- fast path
+
+__device__ __forceinline__ int64_t modinv_dev(int64_t a, int64_t n) {
+  int64_t t = 0, nt = 1, r = n, nr = pmod(a, n);
+  while (nr) {
+    const int64_t q = r / nr;
+    int64_t tmp = t - q * nt; t = nt; nt = tmp;
+    tmp = r - q * nr; r = nr; nr = tmp;
+  }
+  return t < 0 ? t + n : t;
+}
+
+constexpr int kVoteCap = 8192;  // candidates sorted in shared memory per signal
+
+struct FastVote {
+  int64_t nmask;  // n - 1 when n is a power of two, else -1
+  int logL;       // log2 L when L is a power of two, else -1
+};
+
+__device__ __forceinline__ int64_t vbucket(const VoteRounds& vr, const FastVote& fv,
+                                           int64_t sg, int64_t bp, int64_t f) {
+  if (fv.nmask >= 0 && fv.logL >= 0 && bp == 0 && vr.cs == 0) {
+    const int64_t m = (sg * f) & fv.nmask;
+    return ((m + (vr.L >> 1)) & fv.nmask) >> fv.logL;
+  }
+  const int64_t m = mulmod(sg, pmod(f - bp, vr.n), vr.n);
+  int64_t b = pmod(m - vr.cs + vr.L / 2, vr.n) / vr.L;
+  return b >= vr.B ? b - vr.B : b;
+}
+
+__device__ __forceinline__ bool vheavy(const uint32_t* bits_r, int64_t b) {
+  return (bits_r[b >> 5] >> (b & 31)) & 1u;
+}
+
+// Per (signal, round): heavy bucket list from the bitmap, and sigma^-1.
+__global__ void k_vote_lists(VoteRounds vr, int64_t hc, int32_t* hl, int32_t* nh,
+                             int64_t* sinv) {
+  __shared__ int cnt;
+  const int s = blockIdx.y, r = blockIdx.x;
+  const int64_t sr = (int64_t)s * vr.R + r;
+  const uint32_t* bw = vr.bits + sr * vr.words;
+  if (threadIdx.x == 0) {
+    cnt = 0;
+    sinv[sr] = modinv_dev(vr.sigma[sr], vr.n);
+  }
+  __syncthreads();
+  for (int64_t w = threadIdx.x; w < vr.words; w += blockDim.x) {
+    uint32_t v = bw[w];
+    while (v) {
+      const int bit = __ffs(v) - 1;
+      v &= v - 1;
+      const int idx = atomicAdd(&cnt, 1);
+      if (idx < hc) hl[sr * hc + idx] = (int32_t)(w * 32 + bit);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) nh[sr] = cnt < hc ? cnt : (int)hc;
+}
+
+// Warp-aggregated append of (R - score, f) keys.
+__device__ __forceinline__ void vappend(bool take, unsigned long long key, int s,
+                                        int32_t* cnt, unsigned long long* buf) {
+  const unsigned mask = __ballot_sync(0xffffffffu, take);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(cnt + s, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (take) {
+    const int idx = base + __popc(mask & ((1u << lane) - 1));
+    if (idx < kVoteCap) buf[(int64_t)s * kVoteCap + idx] = key;
+  }
+}
+
+// mode 0: every position; mode 1: preimages of the heavy buckets of rounds
+// 0..R-need (every position with >= need votes is heavy in one of them),
+// each position counted from its first heavy round only.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_vote_collect(VoteRounds vr, FastVote fv, int need,
+                                                      int64_t hc, const int32_t* hl,
+                                                      const int32_t* nh, const int64_t* sinv,
+                                                      int32_t* cnt, unsigned long long* buf) {
+  extern __shared__ uint32_t sb[];
+  __shared__ int64_t ssig[64];
+  const int s = blockIdx.y;
+  const int R = vr.R;
+  const uint32_t* gb = vr.bits + (int64_t)s * R * vr.words;
+  for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += blockDim.x) sb[i] = gb[i];
+  for (int r = threadIdx.x; r < R; r += blockDim.x) ssig[r] = vr.sigma[(int64_t)s * R + r];
+  __syncthreads();
+  const int64_t* bps = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
+  if (MODE == 0) {
+    for (int64_t f0 = (int64_t)blockIdx.x * blockDim.x; f0 < vr.n;
+         f0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t f = f0 + threadIdx.x;
+      int c = 0;
+      if (f < vr.n)
+        for (int r = 0; r < R; ++r)
+          c += vheavy(sb + (int64_t)r * vr.words, vbucket(vr, fv, ssig[r], bps ? bps[r] : 0, f));
+      vappend(f < vr.n && c >= need, ((unsigned long long)(R - c) << 40) | (unsigned long long)f,
+              s, cnt, buf);
+    }
+  } else {
+    const int R0 = R - need + 1;
+    const int64_t per_round = hc * vr.L;
+    const int64_t total = (int64_t)R0 * per_round;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < total;
+         e0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t e = e0 + threadIdx.x;
+      bool take = false;
+      unsigned long long key = 0;
+      if (e < total) {
+        const int r0 = (int)(e / per_round);
+        const int64_t rem = e - (int64_t)r0 * per_round;
+        const int64_t hi = rem / vr.L, j = rem - hi * vr.L;
+        const int64_t sr = (int64_t)s * R + r0;
+        if (hi < nh[sr]) {
+          const int64_t b = hl[sr * hc + hi];
+          const int64_t m = pmod(b * vr.L + vr.cs - vr.L / 2 + j, vr.n);
+          const int64_t f = pmod(mulmod(sinv[sr], m, vr.n) + (bps ? bps[r0] : 0), vr.n);
+          bool first = true;
+          for (int r = 0; r < r0 && first; ++r)
+            first = !vheavy(sb + (int64_t)r * vr.words, vbucket(vr, fv, ssig[r], bps ? bps[r] : 0, f));
+          if (first) {
+            int c = 1;
+            for (int r = r0 + 1; r < R; ++r)
+              c += vheavy(sb + (int64_t)r * vr.words, vbucket(vr, fv, ssig[r], bps ? bps[r] : 0, f));
+            take = c >= need;
+            key = ((unsigned long long)(R - c) << 40) | (unsigned long long)f;
+          }
+        }
+      }
+      vappend(take, key, s, cnt, buf);
+    }
+  }
+}
+
+// Per signal: sort the (R - score, f) keys, keep the first `keep`.
+__global__ void __launch_bounds__(1024) k_vote_sort(const int32_t* cnt,
+                                                    const unsigned long long* buf, int keep,
+                                                    int64_t* cand, int32_t* ncand,
+                                                    int32_t* overflow) {
+  extern __shared__ unsigned long long ks[];
+  const int s = blockIdx.x;
+  const int c = cnt[s];
+  if (c > kVoteCap) {
+    if (threadIdx.x == 0) {
+      *overflow = 1;
+      ncand[s] = 0;
+    }
+    return;
+  }
+  int capp = 1;
+  while (capp < c) capp <<= 1;
+  for (int i = threadIdx.x; i < capp; i += blockDim.x)
+    ks[i] = i < c ? buf[(int64_t)s * kVoteCap + i] : ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= capp; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < capp / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        if ((ks[lo] > ks[hi]) == up) {
+          const unsigned long long x = ks[lo];
+          ks[lo] = ks[hi];
+          ks[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  const int kk = c < keep ? c : keep;
+  for (int i = threadIdx.x; i < kk; i += blockDim.x)
+    cand[(int64_t)s * keep + i] = (int64_t)(ks[i] & ((1ull << 40) - 1));
+  if (threadIdx.x == 0) ncand[s] = kk;
+}
+
+size_t votes_fast_ws_bytes(int S, int R, int64_t hc) {
+  return (size_t)S * kVoteCap * 8 + (size_t)S * 4 + 256 + (size_t)S * R * hc * 4 +
+         (size_t)S * R * 4 + (size_t)S * R * 8 + 1024;
+}
+
+int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, int64_t* cand,
+                   int32_t* ncand, void* ws, size_t ws_bytes, int* overflow_host,
+                   cudaStream_t st) {
+  SFFT_REQUIRE(vr.R >= 1 && vr.R <= 64 && need >= 1, "votes_fast: bad rounds");
+  SFFT_REQUIRE(ws_bytes >= votes_fast_ws_bytes(S, vr.R, hc), "votes_fast: workspace too small");
+  char* w = (char*)ws;
+  unsigned long long* buf = (unsigned long long*)w;
+  w += (size_t)S * kVoteCap * 8;
+  int32_t* cnt = (int32_t*)w;
+  w += (size_t)S * 4;
+  int32_t* ovf = (int32_t*)w;
+  w += 256;
+  int32_t* hl = (int32_t*)w;
+  w += (size_t)S * vr.R * hc * 4;
+  int32_t* nh = (int32_t*)w;
+  w += (size_t)S * vr.R * 4;
+  w = (char*)(((uintptr_t)w + 7) & ~(uintptr_t)7);
+  int64_t* sinv = (int64_t*)w;
+  SFFT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * S, st));
+  SFFT_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int32_t), st));
+  FastVote fv;
+  fv.nmask = (vr.n & (vr.n - 1)) == 0 ? vr.n - 1 : -1;
+  fv.logL = (vr.L & (vr.L - 1)) == 0 ? __builtin_ctzll((unsigned long long)vr.L) : -1;
+  const size_t sm = (size_t)vr.R * vr.words * sizeof(uint32_t);
+  SFFT_REQUIRE(sm <= 200 * 1024, "votes_fast: heavy bitmaps exceed shared memory");
+  const int R0 = vr.R - need + 1;
+  const bool pre = R0 >= 1 && (double)R0 * hc * vr.L < 0.5 * (double)vr.n;
+  if (pre) {
+    k_vote_lists<<<dim3(vr.R, S), 256, 0, st>>>(vr, hc, hl, nh, sinv);
+    SFFT_CHECK_LAUNCH("k_vote_lists");
+    SFFT_CUDA(cudaFuncSetAttribute(k_vote_collect<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sm ? sm : 1)));
+    const int64_t total = (int64_t)R0 * hc * vr.L;
+    const unsigned gx = (unsigned)std::min<int64_t>(cdiv_up(total, 256), 512);
+    k_vote_collect<1><<<dim3(gx, S), 256, sm, st>>>(vr, fv, need, hc, hl, nh, sinv, cnt, buf);
+    SFFT_CHECK_LAUNCH("k_vote_collect<pre>");
+  } else {
+    SFFT_CUDA(cudaFuncSetAttribute(k_vote_collect<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sm ? sm : 1)));
+    const unsigned gx = (unsigned)std::min<int64_t>(cdiv_up(vr.n, 256), 1024);
+    k_vote_collect<0><<<dim3(gx, S), 256, sm, st>>>(vr, fv, need, hc, hl, nh, sinv, cnt, buf);
+    SFFT_CHECK_LAUNCH("k_vote_collect<scan>");
+  }
+  SFFT_CUDA(cudaFuncSetAttribute(k_vote_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kVoteCap * 8));
+  k_vote_sort<<<S, 1024, kVoteCap * 8, st>>>(cnt, buf, keep, cand, ncand, ovf);
+  SFFT_CHECK_LAUNCH("k_vote_sort");
+  SFFT_CUDA(cudaMemcpyAsync(overflow_host, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int run_votes(const VoteRounds& vr, int S, const int64_t* counts_in, int64_t* counts_out,
               int need, int keep, int64_t* cand, int32_t* ncand, int* chist, bool emit,
               cudaStream_t st) {

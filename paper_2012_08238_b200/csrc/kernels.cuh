@@ -75,6 +75,14 @@ struct VoteRounds {
   int64_t n, B, L, words, cs;
   int R;
 };
+// Runner fast path: candidates (score >= need) of every signal in (-score, pos)
+// order, first keep, without materialising per-position scores.  Returns 1 in
+// *overflow_host when a signal has more than the sort capacity of candidates
+// (the caller then uses run_votes).
+size_t votes_fast_ws_bytes(int S, int R, int64_t hc);
+int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, int64_t* cand,
+                   int32_t* ncand, void* ws, size_t ws_bytes, int* overflow_host,
+                   cudaStream_t st);
 int run_votes(const VoteRounds& vr, int S, const int64_t* counts_in, int64_t* counts_out,
               int need, int keep, int64_t* cand, int32_t* ncand, int* chist, bool emit,
               cudaStream_t st);

@@ -221,6 +221,7 @@ static VoteLayout vote_layout(int64_t n, int64_t B, int S, int R, int C, int64_t
       sizeof(uint32_t) * (size_t)S * ((Bpre > 0 ? Bpre : 1) + 31) / 32 + 64,  // 17 pre bits
       sizeof(double) * (size_t)S,                 // 18 pre thr
       sizeof(int64_t) * (size_t)S,                // 19 pre tau (zeros)
+      votes_fast_ws_bytes(S, R, 2 * (int64_t)(C / 2)),  // 20 fast vote workspace
   };
   size_t o = 0;
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
@@ -279,6 +280,7 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   Group* groups = (Group*)(w + Lo.off[13]);
   int32_t* ngroups = (int32_t*)(w + Lo.off[14]);
   int32_t* item_sig = (int32_t*)(w + Lo.off[15]);
+  void* fastws = w + Lo.off[20];
   void* bws = w + Lo.total;
   const size_t bws_bytes = ws_bytes - Lo.total;
 
@@ -310,8 +312,16 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   vr.words = (B + 31) / 32;
   vr.cs = 0;
   vr.R = R;
-  rc = run_votes(vr, S, nullptr, nullptr, need, C, a.cand, a.ncand, chist, true, st);
-  if (rc) return rc;
+  {
+    int overflow = 0;
+    rc = run_votes_fast(vr, S, need, C, 2 * k, a.cand, a.ncand, fastws, votes_fast_ws_bytes(S, R, 2 * k),
+                        &overflow, st);
+    if (rc) return rc;
+    if (overflow) {  // some signal has > 8192 candidates: exact chunked ranking
+      rc = run_votes(vr, S, nullptr, nullptr, need, C, a.cand, a.ncand, chist, true, st);
+      if (rc) return rc;
+    }
+  }
 
   int64_t pre_L = 0;
   if (Bpre > 0) {
