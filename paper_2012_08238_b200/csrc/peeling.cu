@@ -61,11 +61,12 @@ struct Verdict {
 };
 
 // classify_bucket with a_max = 1 (sfft/reconstruct.py:412-440) after the
-// peeling pre-check (sfft/frameworks.py:653-658).  Warp-cooperative: the
-// nearest-candidate search (_nearest_candidate, reconstruct.py:136-140) is
-// split over the lanes; every lane returns the same verdict.
-__device__ Verdict classify_warp(const PeelArgs& a, int s, int j, int64_t b, int lane,
-                                 int32_t* err) {
+// peeling pre-check (sfft/frameworks.py:653-658), one thread.  The
+// candidates {b + B i} are evenly spaced, so the nearest one under circular
+// distance (_nearest_candidate, reconstruct.py:136-140) is among the four
+// around (raw - b)/B; the reference distance formula and its tie rule (smaller
+// candidate) are applied to those.
+__device__ Verdict classify_one(const PeelArgs& a, int s, int j, int64_t b, int32_t* err) {
   Verdict v{0, 0, cmk(0.0, 0.0)};
   const int ns = (int)a.sh[j];
   const int64_t n = a.n, B = a.Bs[j], L = a.p[j];
@@ -78,7 +79,7 @@ __device__ Verdict classify_warp(const PeelArgs& a, int s, int j, int64_t b, int
   }
   if (sabs / ns < fl) return v;  // zero
   if (ns < 2) {                  // MomentSequence raises InvalidParameter
-    if (lane == 0) atomicExch(err, 1);
+    atomicExch(err, 1);
     v.kind = 2;
     return v;
   }
@@ -91,25 +92,17 @@ __device__ Verdict classify_warp(const PeelArgs& a, int s, int j, int64_t b, int
   double raw = fmod(atan2(r.y, r.x) * (-nd / (2.0 * 3.141592653589793)), nd);
   if (raw != 0.0 && raw < 0.0) raw += nd;
   if (raw == 0.0) raw = 0.0;
-  // nearest admissible candidate (bucket + B*i) mod n, ties to the smaller
+  const int64_t i0 = (int64_t)floor((raw - (double)b) / (double)B);
   double bd = CUDART_INF;
   int64_t bc = 0x7fffffffffffffffll;
-  for (int64_t i = lane; i < L; i += 32) {
-    const int64_t cnd = pmod(b + B * i, n);
+  for (int64_t di = -1; di <= 2; ++di) {
+    const int64_t cnd = pmod(b + B * pmod(i0 + di, L), n);
     double d = fmod(((double)cnd - raw) + nd / 2.0, nd);
     if (d != 0.0 && d < 0.0) d += nd;
     d = fabs(d - nd / 2.0);
     if (d < bd || (d == bd && cnd < bc)) {
       bd = d;
       bc = cnd;
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-    const long long oc = __shfl_xor_sync(0xffffffffu, (long long)bc, o);
-    if (od < bd || (od == bd && oc < bc)) {
-      bd = od;
-      bc = oc;
     }
   }
   const int64_t f = bc;
@@ -131,21 +124,18 @@ __device__ Verdict classify_warp(const PeelArgs& a, int s, int j, int64_t b, int
   return v;
 }
 
-// Initial classification of every bucket of every stage (warp per bucket).
+// Initial classification of every bucket of every stage (thread per bucket).
 __global__ void k_pe_classify_all(PeelArgs a) {
   const int s = blockIdx.y;
-  const int lane = threadIdx.x & 31;
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.sumB) return;
   const int j = stage_of(a, g);
   const int64_t b = g - a.boff[j];
-  const Verdict v = classify_warp(a, s, j, b, lane, a.err + s);
-  if (lane == 0) {
-    const int64_t i = (int64_t)s * a.sumB + g;
-    a.kind[i] = v.kind;
-    a.cf[i] = v.f;
-    a.cc[i] = v.c;
-  }
+  const Verdict v = classify_one(a, s, j, b, a.err + s);
+  const int64_t i = (int64_t)s * a.sumB + g;
+  a.kind[i] = v.kind;
+  a.cf[i] = v.f;
+  a.cc[i] = v.c;
 }
 
 // Singles in (stage, bucket) order into the two tier queues.
@@ -229,31 +219,35 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget) {
     }
     nrec += __shfl_sync(0xffffffffu, grew, 0);
     ++peels;
-    for (int j = 0; j < a.nst; ++j) {
+    // every stage in its own lane: subtract c w^{t f} from bucket f mod B_j,
+    // reclassify; new single-tons are queued in stage order
+    Verdict v{0, 0, cmk(0.0, 0.0)};
+    int64_t gi = 0;
+    int tier = 0;
+    if (lane < a.nst) {
+      const int j = lane;
       const int64_t b = f % a.Bs[j];
-      if (lane < a.sh[j]) {
-        const int t = lane;
+      for (int t = 0; t < a.sh[j]; ++t) {
         double2* mp = a.meas + a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b;
         *mp = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
       }
-      __syncwarp();
-      const Verdict v = classify_warp(a, s, j, b, lane, a.err + s);
-      const int64_t gi = a.boff[j] + b;
-      if (lane == 0) {
-        kind[gi] = v.kind;
-        cfs[gi] = v.f;
-        ccs[gi] = v.c;
-        if (v.kind == 1) {
-          const int tier = a.sh[j] >= 3 ? 0 : 1;
-          if (tail[tier] < a.qcap) q[tier][tail[tier]] = gi;
-        }
-      }
-      if (v.kind == 1) {
-        const int tier = a.sh[j] >= 3 ? 0 : 1;
-        if (tail[tier] < a.qcap) ++tail[tier];
-      }
-      __syncwarp();
+      v = classify_one(a, s, j, b, a.err + s);
+      gi = a.boff[j] + b;
+      kind[gi] = v.kind;
+      cfs[gi] = v.f;
+      ccs[gi] = v.c;
+      tier = a.sh[j] >= 3 ? 0 : 1;
     }
+    for (int tr = 0; tr < 2; ++tr) {
+      const unsigned push = __ballot_sync(0xffffffffu, lane < a.nst && v.kind == 1 && tier == tr);
+      if (lane < a.nst && v.kind == 1 && tier == tr) {
+        const int64_t pos = tail[tr] + __popc(push & ((1u << lane) - 1));
+        if (pos < a.qcap) q[tr][pos] = gi;
+      }
+      const int64_t nt = (int64_t)tail[tr] + __popc(push);
+      tail[tr] = (int32_t)(nt < a.qcap ? nt : a.qcap);
+    }
+    __syncwarp();
   }
   if (lane == 0) {
     a.rec_count[s] = nrec;
@@ -448,7 +442,8 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
                    nullptr, st);
     if (rc) return rc;
   }
-  dim3 gc((unsigned)cdiv_up(d.sumB, 8), S);
+  SFFT_REQUIRE(nst <= 32, "peeling: at most 32 stages");
+  dim3 gc((unsigned)cdiv_up(d.sumB, 256), S);
   k_pe_classify_all<<<gc, 256, 0, st>>>(a);
   SFFT_CHECK_LAUNCH("k_pe_classify_all");
   k_pe_queue_init<<<S, 1024, 0, st>>>(a);
