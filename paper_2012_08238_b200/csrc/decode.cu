@@ -20,10 +20,15 @@ namespace sfft {
 constexpr int kFloorNT = 256;
 
 // One CTA per bucket set: floor[i] and peak[i] of values[i][0..B).
-__global__ void __launch_bounds__(kFloorNT) k_floor(const double2* __restrict__ values, int64_t B,
-                                                    double mult, const int32_t* item_sig,
-                                                    const int32_t* active, double* floor_out,
-                                                    double* peak_out) {
+constexpr int kFloorBigNT = 1024;
+constexpr int64_t kFloorCache = 24576;  // |v| bits cached in shared memory up to this B
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_floor(const double2* __restrict__ values, int64_t B,
+                                              double mult, const int32_t* item_sig,
+                                              const int32_t* active, double* floor_out,
+                                              double* peak_out) {
+  extern __shared__ unsigned long long fcache[];
   __shared__ unsigned hist[256];
   __shared__ long long sh[4];
   __shared__ double redd[32];
@@ -34,7 +39,14 @@ __global__ void __launch_bounds__(kFloorNT) k_floor(const double2* __restrict__ 
     if (!active[sig]) return;
   }
   double med, peak;
-  median_and_peak<kFloorNT>(values + (int64_t)item * B, B, &med, &peak, hist, sh, redd, redu);
+  const double2* v = values + (int64_t)item * B;
+  if (B <= kFloorCache) {
+    for (int64_t i = threadIdx.x; i < B; i += NT) fcache[i] = dbits(cabs_(v[i]));
+    __syncthreads();
+    median_and_peak_k<NT>(SmemKey{fcache}, B, &med, &peak, hist, sh, redd, redu);
+  } else {
+    median_and_peak<NT>(v, B, &med, &peak, hist, sh, redd, redu);
+  }
   if (threadIdx.x == 0) {
     const double fl = fmax(fmax(fmin(mult * med, 0.25 * peak), 1e-9 * peak), 1e-300);
     floor_out[item] = fl;
@@ -46,8 +58,16 @@ int run_floor(const double2* values, int64_t nsets, int64_t B, double mult,
               const int32_t* item_sig, const int32_t* active, double* floor_out, double* peak_out,
               cudaStream_t st) {
   if (nsets <= 0) return 0;
-  k_floor<<<(unsigned)nsets, kFloorNT, 0, st>>>(values, B, mult, item_sig, active, floor_out,
-                                                peak_out);
+  const size_t sm = B <= kFloorCache ? (size_t)B * 8 : 0;
+  if (B > 2048) {
+    SFFT_CUDA(cudaFuncSetAttribute(k_floor<kFloorBigNT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sm ? sm : 1)));
+    k_floor<kFloorBigNT><<<(unsigned)nsets, kFloorBigNT, sm, st>>>(values, B, mult, item_sig,
+                                                                   active, floor_out, peak_out);
+  } else {
+    k_floor<kFloorNT><<<(unsigned)nsets, kFloorNT, sm, st>>>(values, B, mult, item_sig, active,
+                                                             floor_out, peak_out);
+  }
   SFFT_CHECK_LAUNCH("k_floor");
   return 0;
 }
