@@ -118,6 +118,63 @@ __device__ __forceinline__ double2 produce(const Prod& p, const ItemCtx& c, int 
   }
 }
 
+// Two flat slots at once (8 gathers in flight per thread); each slot's rows
+// are still summed in row order without FMA contraction.
+template <typename Tin>
+__device__ __forceinline__ void produce_flat2(const Prod& p, const ItemCtx& c, int64_t s0,
+                                              int64_t s1, double2* o0, double2* o1) {
+  const int64_t n = p.n;
+  const Tin* xs = (const Tin*)c.xs;
+  int64_t ia = mulmod(c.a, pmod(s0 - c.b, n), n);
+  int64_t ib = mulmod(c.a, pmod(s1 - c.b, n), n);
+  double2 aa = cmk(0.0, 0.0), ab = cmk(0.0, 0.0);
+  int64_t i = s0, k = s1;
+  const int64_t B = p.B;
+  // s1 > s0, so slot s1 runs out of rows first or at the same time
+  for (; k + 3 * B < p.omega; i += 4 * B, k += 4 * B) {
+    int64_t ia1 = ia + c.step; ia1 -= (ia1 >= n) ? n : 0;
+    int64_t ia2 = ia1 + c.step; ia2 -= (ia2 >= n) ? n : 0;
+    int64_t ia3 = ia2 + c.step; ia3 -= (ia3 >= n) ? n : 0;
+    int64_t ib1 = ib + c.step; ib1 -= (ib1 >= n) ? n : 0;
+    int64_t ib2 = ib1 + c.step; ib2 -= (ib2 >= n) ? n : 0;
+    int64_t ib3 = ib2 + c.step; ib3 -= (ib3 >= n) ? n : 0;
+    const double2 va0 = Sample<Tin>::load(xs, ia), va1 = Sample<Tin>::load(xs, ia1);
+    const double2 va2 = Sample<Tin>::load(xs, ia2), va3 = Sample<Tin>::load(xs, ia3);
+    const double2 vb0 = Sample<Tin>::load(xs, ib), vb1 = Sample<Tin>::load(xs, ib1);
+    const double2 vb2 = Sample<Tin>::load(xs, ib2), vb3 = Sample<Tin>::load(xs, ib3);
+    const double ga0 = __ldg(p.taps + i), ga1 = __ldg(p.taps + i + B);
+    const double ga2 = __ldg(p.taps + i + 2 * B), ga3 = __ldg(p.taps + i + 3 * B);
+    const double gb0 = __ldg(p.taps + k), gb1 = __ldg(p.taps + k + B);
+    const double gb2 = __ldg(p.taps + k + 2 * B), gb3 = __ldg(p.taps + k + 3 * B);
+    aa = cadd_rn(aa, cmk(__dmul_rn(ga0, va0.x), __dmul_rn(ga0, va0.y)));
+    aa = cadd_rn(aa, cmk(__dmul_rn(ga1, va1.x), __dmul_rn(ga1, va1.y)));
+    aa = cadd_rn(aa, cmk(__dmul_rn(ga2, va2.x), __dmul_rn(ga2, va2.y)));
+    aa = cadd_rn(aa, cmk(__dmul_rn(ga3, va3.x), __dmul_rn(ga3, va3.y)));
+    ab = cadd_rn(ab, cmk(__dmul_rn(gb0, vb0.x), __dmul_rn(gb0, vb0.y)));
+    ab = cadd_rn(ab, cmk(__dmul_rn(gb1, vb1.x), __dmul_rn(gb1, vb1.y)));
+    ab = cadd_rn(ab, cmk(__dmul_rn(gb2, vb2.x), __dmul_rn(gb2, vb2.y)));
+    ab = cadd_rn(ab, cmk(__dmul_rn(gb3, vb3.x), __dmul_rn(gb3, vb3.y)));
+    ia = ia3 + c.step; ia -= (ia >= n) ? n : 0;
+    ib = ib3 + c.step; ib -= (ib >= n) ? n : 0;
+  }
+  for (; i < p.omega; i += B) {
+    const double2 v = Sample<Tin>::load(xs, ia);
+    const double g = __ldg(p.taps + i);
+    aa = cadd_rn(aa, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
+    ia += c.step;
+    ia -= (ia >= n) ? n : 0;
+  }
+  for (; k < p.omega; k += B) {
+    const double2 v = Sample<Tin>::load(xs, ib);
+    const double g = __ldg(p.taps + k);
+    ab = cadd_rn(ab, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
+    ib += c.step;
+    ib -= (ib >= n) ? n : 0;
+  }
+  *o0 = aa;
+  *o1 = ab;
+}
+
 constexpr int kNT = 512;
 
 template <typename Tin, int MODE>
@@ -162,8 +219,14 @@ __global__ void __launch_bounds__(kClNT) k_cluster(Prod p, FftPlan Pm,
   const int M = B / CL;
   double2* a = sm;
   double2* bq = sm + M;
-  for (int j = threadIdx.x; j < M; j += kClNT)
-    a[j] = produce<Tin, MODE>(p, c, item, (int64_t)q * M + j);
+  if (MODE == PROD_FLAT && c.c == 0 && M % (2 * kClNT) == 0) {
+    for (int j = threadIdx.x; j < M; j += 2 * kClNT)
+      produce_flat2<Tin>(p, c, (int64_t)q * M + j, (int64_t)q * M + j + kClNT, &a[j],
+                         &a[j + kClNT]);
+  } else {
+    for (int j = threadIdx.x; j < M; j += kClNT)
+      a[j] = produce<Tin, MODE>(p, c, item, (int64_t)q * M + j);
+  }
   cl.sync();
   const double2* rem[CL];
 #pragma unroll
