@@ -270,6 +270,18 @@ def main():
     kern_ms = pm.value
     achieved = (pi.value * item_bytes) / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
     peak, peak_kind = peaks()
+    # DRAM traffic of the same kernel from the committed ncu --set full capture
+    # (profiles/r1_k_cluster_ncu_raw.json: first C3 loop round, 1024 items)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_k_cluster_ncu_raw.json")) as f:
+            raw = json.load(f)
+        unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        rd = float(raw["dram__bytes_read.sum"][0]) * unit[raw["dram__bytes_read.sum"][1]]
+        wr = float(raw["dram__bytes_write.sum"][0]) * unit[raw["dram__bytes_write.sum"][1]]
+        traffic = (rd + wr) / 1024.0  # per item, like bytes_per_item
+    except Exception:
+        traffic = None
 
     value = total / (ms * 1e-3)
 
@@ -319,7 +331,8 @@ def main():
                        "num_buckets": B, "omega": omega, "parallelism": f"replicas{world}",
                        "l2": "inputs larger than L2 (%.1f GB per GPU)" % (S * N * 8 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": traffic, "traffic_unit": "DRAM bytes per item (ncu)",
                          "kernel": "k_cluster<float2,FLAT,8> (gather+window+fold, DSMEM radix-8 stage, FFT_512)",
                          "bytes_per_item": item_bytes, "items": pi.value,
                          "launches": pl.value, "kernel_ms": kern_ms,
