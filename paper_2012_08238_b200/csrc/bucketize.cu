@@ -203,8 +203,15 @@ __global__ void __launch_bounds__(kNT) k_fused(Prod p, FftPlan P, const double2*
 // spread over 8 SMs instead of one.
 constexpr int kClNT = 256;
 
+// the complex64 flat gather is latency bound: cap registers at 64 so that 4
+// CTAs (1024 threads) share an SM; other instantiations keep their registers
+template <typename Tin, int MODE>
+constexpr int cluster_min_blocks() {
+  return (MODE == PROD_FLAT && sizeof(Tin) == 8) ? 4 : 1;
+}
+
 template <typename Tin, int MODE, int CL>
-__global__ void __launch_bounds__(kClNT) k_cluster(Prod p, FftPlan Pm,
+__global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>()) k_cluster(Prod p, FftPlan Pm,
                                                    const double2* __restrict__ W,
                                                    double2* __restrict__ out) {
   namespace cg = cooperative_groups;
