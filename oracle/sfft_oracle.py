@@ -273,6 +273,7 @@ class Cfg:
     num_buckets: int | None = None
     coprime_factors: tuple | None = None
     location_method: str | None = None
+    branching: int = 2
     rounds: int = 10
     max_iterations: int = 10
     spike_prestage: bool = False
@@ -400,13 +401,36 @@ def unwrap(y0, ys: dict, n: int):
     return int(np.round(q)) % n
 
 
+class Ambiguous(Exception):
+    """AmbiguousSplit (sfft/errors.py)."""
+
+
+def split_search(sub, bucket: int, width: int, branching: int, noise_floor: float) -> int:
+    """Iterated class splits of the in-bucket offset (sfft/reconstruct.py:197-215):
+    digit by digit, the `branching` class sums mod step = scale*branching are
+    compared by magnitude; a top-two gap below the noise floor is ambiguous."""
+    digits = round(np.log(width) / np.log(branching))
+    if branching < 2 or branching ** digits != width:
+        raise OracleError("InvalidParameter", f"width {width} is not a power of {branching}")
+    r, scale = 0, 1
+    for _ in range(digits):
+        step = scale * branching
+        mags = np.array([abs(sub(bucket, r + d * scale, step)) for d in range(branching)])
+        top = np.sort(mags)[::-1]
+        if top[0] - top[1] < noise_floor:
+            raise Ambiguous(f"{top[0]:.3g} vs {top[1]:.3g}")
+        r += scale * int(np.argmax(mags))
+        scale = step
+    return r
+
+
 def iterative(acc: Access, k: int, cfg: Cfg) -> Outcome:
-    """Phase-location iterative framework (sfft/frameworks.py:439-516, :556-570)
-    plus the residual polish (:573-608).  Binary/multiscale location is out of
-    the hot-path scope (SURVEY.md §8(f) #1)."""
+    """Iterative framework (sfft/frameworks.py:439-570) with phase location
+    (:493-516) or binary / multiscale class-split location (:517-554), plus the
+    residual polish (:573-608)."""
     loc = cfg.location_method or "phase"
-    if loc != "phase":
-        raise OracleError("ConfigMismatch", f"oracle covers phase location only, got {loc}")
+    if loc not in ("phase", "binary", "multiscale"):
+        raise OracleError("ConfigMismatch", f"iterative cannot use location {loc}")
     n = acc.n
     if k <= 0:
         return _finish(acc, {}, 0, 0, True)
@@ -441,26 +465,58 @@ def iterative(acc: Access, k: int, cfg: Cfg) -> Outcome:
             break
         hv = np.flatnonzero(mag >= fl)
         hv = hv[np.lexsort((hv, -mag[hv]))]
-        ys = {d: meas(d) for d in rungs}
         new: dict = {}
-        for bi in hv:
-            q = unwrap(y0[bi], {d: ys[d][bi] for d in rungs}, n)
-            if q is None:
-                continue
-            lo = (bi * L - L // 2) % n
-            if (q - lo) % n >= L:
-                continue
-            tol = max(3.0 * fl, 0.15 * abs(y0[bi]))
-            if any(abs(ys[d][bi] - y0[bi] * unit_root(n, d * q)) > tol for d in rungs):
-                continue
-            w = win.response[(bi * L - q) % n]
-            if abs(w) < 0.05 * peak:
-                continue
-            sh = np.array([0] + rungs, dtype=np.int64)
-            v = np.array([y0[bi]] + [ys[d][bi] for d in rungs])
-            c = complex(np.mean(v * unit_root(n, -(t + sh) * q)) / w)
-            f = int((sinv * q + bp) % n)
-            new[f] = new.get(f, 0.0) + c
+        if loc == "phase":
+            ys = {d: meas(d) for d in rungs}
+            for bi in hv:
+                q = unwrap(y0[bi], {d: ys[d][bi] for d in rungs}, n)
+                if q is None:
+                    continue
+                lo = (bi * L - L // 2) % n
+                if (q - lo) % n >= L:
+                    continue
+                tol = max(3.0 * fl, 0.15 * abs(y0[bi]))
+                if any(abs(ys[d][bi] - y0[bi] * unit_root(n, d * q)) > tol for d in rungs):
+                    continue
+                w = win.response[(bi * L - q) % n]
+                if abs(w) < 0.05 * peak:
+                    continue
+                sh = np.array([0] + rungs, dtype=np.int64)
+                v = np.array([y0[bi]] + [ys[d][bi] for d in rungs])
+                c = complex(np.mean(v * unit_root(n, -(t + sh) * q)) / w)
+                f = int((sinv * q + bp) % n)
+                new[f] = new.get(f, 0.0) + c
+        else:
+            br = 2 if loc == "binary" else cfg.branching
+            digits = round(math.log(L, br))
+            if br ** digits != L:
+                raise OracleError("ConfigMismatch", f"bucket width {L} is not a power of {br}")
+
+            def sub(bi, off, step):
+                # class-sum measurement from `step` shifted bucketizations
+                base = (bi * L - L // 2) % n
+                qc = (base + off) % step
+                dd = np.arange(step, dtype=np.int64)
+                vals = np.array([meas(int(tt))[bi] for tt in dd * (n // step)])
+                return complex(np.mean(vals * np.exp(2j * np.pi * dd * qc / step)))
+
+            for bi in hv:
+                try:
+                    r = split_search(sub, int(bi), L, br, fl / 2)
+                except Ambiguous:
+                    continue
+                q = (bi * L - L // 2 + r) % n
+                meas(1), meas(3)  # whole-window alias check shifts
+                tol = max(3.0 * fl, 0.15 * abs(y0[bi]))
+                checks = [tt for tt in sorted(memo) if tt != 0]
+                if any(abs(memo[tt][bi] - y0[bi] * unit_root(n, tt * q)) > tol for tt in checks):
+                    continue
+                w = win.response[(bi * L - q) % n]
+                if abs(w) < 0.05 * peak:
+                    continue
+                c = complex(y0[bi] * unit_root(n, -t * q) / w)
+                f = int((sinv * q + bp) % n)
+                new[f] = new.get(f, 0.0) + c
         for f, c in new.items():
             rec[f] = rec.get(f, 0.0) + c
         if len(rec) >= k and new:

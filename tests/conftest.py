@@ -32,9 +32,9 @@ def sig_checksum(x):
                     dtype=np.complex128)
 
 
-def runner_cases():
+def runner_cases(name="runners"):
     import json
-    z = load_golden("runners")
+    z = load_golden(name)
     index = json.loads(str(z["index_json"]))
     out = []
     for rec in index:

@@ -115,3 +115,33 @@ def test_runner_golden(case):
 @pytest.mark.parametrize("case", SLOW, ids=[c[0]["name"] for c in SLOW])
 def test_runner_golden_full_size(case):
     _check_runner(*case)
+
+
+SPLIT = runner_cases("split")
+SPLIT_FAST = [c for c in SPLIT if c[0]["n"] <= (1 << 14)]
+SPLIT_SLOW = [c for c in SPLIT if c[0]["n"] > (1 << 14)]
+
+
+@pytest.mark.parametrize("case", SPLIT_FAST, ids=[c[0]["name"] for c in SPLIT_FAST])
+def test_split_location_golden(case):
+    """Binary / multiscale location (sfft/frameworks.py:517-554) pinned bit-exactly."""
+    _check_runner(*case)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", SPLIT_SLOW, ids=[c[0]["name"] for c in SPLIT_SLOW])
+def test_split_location_golden_large(case):
+    _check_runner(*case)
+
+
+def test_split_search_unit():
+    """Known answers of the split search (reference tests/test_reconstruct.py:125-160)."""
+    def sub_for(coeffs):
+        return lambda b, off, step: sum(c for r, c in coeffs.items() if (r - off) % step == 0)
+    assert O.split_search(sub_for({5: 1.0}), 0, 8, 2, 1e-12) == 5
+    assert O.split_search(sub_for({11: 1.0}), 0, 16, 4, 1e-12) == 11
+    assert O.split_search(sub_for({13: 2.0, 4: 0.5}), 0, 16, 16, 1e-12) == 13
+    for off in range(16):
+        assert O.split_search(sub_for({off: 1 + 0.5j}), 0, 16, 2, 1e-12) == off
+    with pytest.raises(O.Ambiguous):
+        O.split_search(sub_for({}), 0, 8, 2, 1e-12)
