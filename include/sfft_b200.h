@@ -150,17 +150,21 @@ int sfft_subtract_flat(const void* y, void* out, int64_t B, int64_t nb, const in
 /* ---- runners (device-resident frameworks) ---------------------------------- */
 
 /* Workspace bytes of sfft_run_iterative for nslots slots (nshifts = 1 +
- * ladder length, cap = recovered-tone capacity per slot; max_iterations * B
- * suffices). */
+ * ladder length for phase location, n/B + 2 for split location; cap =
+ * recovered-tone capacity per slot, max_iterations * B suffices). */
 size_t sfft_iterative_ws_bytes(int64_t n, int64_t B, int64_t nslots, int64_t nshifts, int64_t cap);
 
-/* A16 run_iterative with phase location + _polish_flat_estimates
- * (sfft/frameworks.py:439-608) for nsig signals (rows of x), continuously
+/* A16 run_iterative + _polish_flat_estimates (sfft/frameworks.py:439-608)
+ * with phase location (location 0, :493-516) or binary / multiscale
+ * class-split location (location 1, :517-554; branching 2 for binary,
+ * AlgorithmConfig.branching for multiscale; n/B must be a power of it) for
+ * nsig signals (rows of x), continuously
  * batched over nslots device slots: a slot whose signal finishes takes the
  * next queued signal.  perm_sigma/perm_tau hold each signal's permutation
  * stream (PermutationParams.random draws in order; nperm >= max_iterations
  * + 6) at row stride perm_stride (0: one stream shared by all signals).
- * ladder_host (HOST int64[nladder]) is _phase_ladder(n).  Outputs per signal:
+ * ladder_host (HOST int64[nladder]) is _phase_ladder(n) (unused, may be NULL,
+ * for split location).  Outputs per signal:
  * out_pos/out_coef [nsig][k] the top-k entries in (-|c|, f) order,
  * out_count, out_iterations, out_converged, out_samples (samples_read);
  * out_sched (optional) receives the read schedule, see sfft_schedule_layout;
@@ -171,7 +175,8 @@ int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int
                        const void* gtable, const double* gmax, const void* W,
                        const int64_t* perm_sigma, const int64_t* perm_tau, int64_t nperm,
                        int64_t perm_stride, int64_t k, int64_t max_iterations,
-                       const int64_t* ladder_host, int64_t nladder, int64_t cap, int64_t* out_pos,
+                       const int64_t* ladder_host, int64_t nladder, int32_t location,
+                       int32_t branching, int64_t cap, int64_t* out_pos,
                        void* out_coef, int32_t* out_count, int32_t* out_iterations,
                        int32_t* out_converged, int64_t* out_samples, int64_t* out_sched,
                        const int32_t* avail, void* ws, size_t ws_bytes, void* stream);

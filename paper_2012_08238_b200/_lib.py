@@ -107,7 +107,8 @@ SIGNATURES.update({
 SIGNATURES.update({
     "sfft_iterative_ws_bytes": (sz, [i64, i64, i64, i64, i64]),
     "sfft_run_iterative": (C.c_int, [C.c_int, vp, i64, i64, i64, i64, P_f64, i64, i64, vp, P_f64,
-                                     vp, P_i64, P_i64, i64, i64, i64, i64, vp, i64, i64, P_i64,
+                                     vp, P_i64, P_i64, i64, i64, i64, i64, vp, i64, i32, i32,
+                                     i64, P_i64,
                                      vp, P_i32, P_i32, P_i32, P_i64, P_i64, P_i32, vp, sz, vp]),
     "sfft_schedule_layout": (C.c_int, [vp, vp]),
 })

@@ -253,13 +253,15 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
                                 int64_t B, const void* gtable, const double* gmax, const void* W,
                                 const int64_t* perm_sigma, const int64_t* perm_tau, int64_t nperm,
                                 int64_t perm_stride, int64_t k, int64_t max_iterations,
-                                const int64_t* ladder_host, int64_t nladder, int64_t cap,
+                                const int64_t* ladder_host, int64_t nladder, int32_t location,
+                                int32_t branching, int64_t cap,
                                 int64_t* out_pos, void* out_coef, int32_t* out_count,
                                 int32_t* out_iterations, int32_t* out_converged,
                                 int64_t* out_samples, int64_t* out_sched,
                                 const int32_t* avail, void* ws, size_t ws_bytes, void* stream) {
   SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_iterative: dtype must be 0 or 1");
-  SFFT_REQUIRE(x && taps && gtable && gmax && W && perm_sigma && perm_tau && ladder_host,
+  SFFT_REQUIRE(x && taps && gtable && gmax && W && perm_sigma && perm_tau &&
+                   (ladder_host || location == 1),
                "sfft_run_iterative: null pointer");
   SFFT_REQUIRE(n > 0 && B > 0 && n % B == 0 && nsig >= 1 && nslots >= 1 && k >= 1 &&
                    max_iterations >= 1, "sfft_run_iterative: bad sizes");
@@ -269,7 +271,8 @@ SFFT_API int sfft_run_iterative(int dtype, const void* x, int64_t n, int64_t xst
   return run_iterative(dtype, x, n, xstride, (int)nsig, (int)std::min(nslots, nsig), taps, omega,
                        B, (const double2*)gtable, gmax, (const double2*)W, perm_sigma, perm_tau,
                        (int)nperm, perm_stride, k, (int)max_iterations, ladder_host,
-                       (int)nladder, (int)cap, out_pos, (double2*)out_coef, out_count,
+                       (int)nladder, (int)location, (int)branching, (int)cap, out_pos,
+                       (double2*)out_coef, out_count,
                        out_iterations, out_converged, out_samples, out_sched, avail, ws,
                        ws_bytes, (cudaStream_t)stream);
 }

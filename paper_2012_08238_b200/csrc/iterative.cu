@@ -17,6 +17,15 @@
 //   y[j>0] - model(recovered) at heavy buckets; unwrap; checks   (k_it_locate)
 //   merge found into recovered (insertion order = heavy order)   (k_it_merge)
 //   |y0 - model(found)| < 1.3 floor ?                            (k_subtract, k_it_resid)
+//
+// Binary / multiscale location (sfft/frameworks.py:517-554) replaces the
+// ladder by the class-split measurements: the loop items of a slot are the
+// L = N/B shifts d*B (d < L, every d*(n/step) the split search can ask for)
+// plus the alias-check shifts 1 and 3; k_sp_model subtracts the recovered
+// model from them at the heavy buckets, k_sp_search runs the digit-by-digit
+// split per heavy bucket (one warp each) and k_sp_check applies the
+// consistency checks against the shifts the reference would have cached by
+// then (a prefix over the heavy order), the weight check and the estimate.
 #include "kernels.cuh"
 #include "schedule.cuh"
 #include "finalize.cuh"
@@ -56,7 +65,13 @@ struct IterArgs {
   int64_t pstride;               // perms row stride per signal (0: shared stream)
   int32_t* item_active;          // [S*M]
   int32_t* pgate;                // [S] polish pass this round
-  int64_t ladder[kMaxShifts];    // d_1..d_{M-1}
+  int64_t ladder[kMaxShifts];    // d_1..d_{M-1} (phase location)
+  const int64_t* shifts;         // [M] shift of loop item j (device)
+  int loc;                       // 0 phase, 1 class-split (binary / multiscale)
+  int branching, digits;         // split search: L = branching^digits
+  int32_t* sp_r;                 // [S][B] split offset per heavy rank
+  int32_t* sp_ok;                // [S][B] 1 located, 0 ambiguous
+  int32_t* sp_depth;             // [S][B] largest step the search measured
   const int64_t* psig;           // [S][P]
   const int64_t* ptau;           // [S][P]
   const double2* gt;             // [L][B]
@@ -217,7 +232,7 @@ __global__ void k_cb_items(IterArgs a) {
   a.item_active[i] = on;
   a.item_sig[i] = S.sig > 0 ? S.sig : 0;
   if (!on) return;
-  const int64_t d = (S.phase == PH_LOOP) ? (j == 0 ? 0 : a.ladder[j - 1]) : j;
+  const int64_t d = (S.phase == PH_LOOP) ? a.shifts[j] : j;
   a.item_sigma_it[i] = a.item_sigma[s];
   a.item_tau_it[i] = pmod(a.item_tau[s] + d, a.n);
 }
@@ -277,7 +292,8 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
     S.scale_ref = sref;
     S.floor = fl;
     const int g = S.ngroups;
-    if (g < kMaxGroups) {
+    // split location logs its (data-dependent) shifts in k_sp_check
+    if (g < kMaxGroups && (conv || a.loc == 0)) {
       Group& G = a.groups[(int64_t)s * kMaxGroups + g];
       G.kind = 0;
       G.a = a.item_sigma[s];
@@ -285,7 +301,8 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
       G.cnt = a.omega;
       G.nsh = conv ? 1 : a.M;
       G.sh[0] = 0;
-      for (int j = 1; j < a.M; ++j) G.sh[j] = a.ladder[j - 1];
+      if (!conv)
+        for (int j = 1; j < a.M; ++j) G.sh[j] = a.ladder[j - 1];
       S.ngroups = g + 1;
     }
     if (conv) {
@@ -532,6 +549,258 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   a.f_pos[fi] = f;
   a.f_coef[fi] = coeff;
   a.f_ok[fi] = 1;
+}
+
+
+// ------------------------------------------------------------------ split location
+// y[j][s][b] -= sum_t (c_t * G[(bL - m_t) mod N]) * w^{(tau + d_j) m_t} for
+// the loop items j >= 1 at the heavy buckets, tones in order (the running
+// subtraction of _subtract_flat, frameworks.py:423-436).  Tile: 32 heavy
+// buckets (lanes) x 32 shifts (8 warps x 4), tones staged 16 at a time.
+constexpr int kSpNT = 256;
+constexpr int kSpH = 32, kSpJ = 32, kSpT = 16;
+
+__global__ void __launch_bounds__(kSpNT) k_sp_model(IterArgs a) {
+  __shared__ double2 cw[kSpT][kSpH];
+  __shared__ double2 ph[kSpT][kSpJ];
+  __shared__ int64_t tm[kSpT], trow[kSpT], tq[kSpT];
+  __shared__ double2 tc[kSpT];
+  const int s = blockIdx.z;
+  if (!a.active[s]) return;
+  const int nh = a.st[s].nheavy;
+  const int h0 = blockIdx.x * kSpH;
+  const int j0 = 1 + blockIdx.y * kSpJ;
+  if (h0 >= nh || j0 >= a.M) return;
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int64_t sigma = a.item_sigma[s], tau = a.item_tau[s];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int h = h0 + lane;
+  const bool hl = h < nh;
+  const int b = hl ? a.heavy_b[(int64_t)s * B + h] : 0;
+  double2 acc[4];
+  bool jl[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = j0 + wq * 4 + u;
+    jl[u] = hl && j < a.M;
+    acc[u] = jl[u] ? a.y[((int64_t)j * a.S + s) * B + b] : cmk(0.0, 0.0);
+  }
+  const int T = a.rec_count[s];
+  const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  const double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  for (int t0 = 0; t0 < T; t0 += kSpT) {
+    const int tn = min(kSpT, T - t0);
+    __syncthreads();
+    if (threadIdx.x < tn) {
+      const int64_t m = mulmod(sigma, pmod(rp[t0 + threadIdx.x], n), n);
+      tm[threadIdx.x] = m;
+      trow[threadIdx.x] = (L - m % L) % L;
+      tq[threadIdx.x] = (m + L - 1) / L;
+      tc[threadIdx.x] = rc[t0 + threadIdx.x];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSpT * kSpH; e += kSpNT) {
+      const int t = e / kSpH, hh = e - t * kSpH;
+      if (t >= tn || h0 + hh >= nh) continue;
+      const int bb = a.heavy_b[(int64_t)s * B + h0 + hh];
+      int64_t col = bb - tq[t];
+      col += (col < 0) ? B : 0;
+      cw[t][hh] = cmul(tc[t], ld_table(a.gt + trow[t] * B + col));
+    }
+    for (int e = threadIdx.x; e < kSpT * kSpJ; e += kSpNT) {
+      const int t = e / kSpJ, jj = e - t * kSpJ;
+      if (t >= tn || j0 + jj >= a.M) continue;
+      ph[t][jj] = unit_root(n, mulmod(pmod(tau + a.shifts[j0 + jj], n), tm[t], n));
+    }
+    __syncthreads();
+    for (int t = 0; t < tn; ++t) {
+      const double2 c = cw[t][lane];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = csub(acc[u], cmul(c, ph[t][wq * 4 + u]));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = j0 + wq * 4 + u;
+    if (jl[u]) a.y[((int64_t)j * a.S + s) * B + b] = acc[u];
+  }
+}
+
+// measurement of loop shift d*B (d < L) at bucket b (d = 0: y0)
+__device__ __forceinline__ double2 sp_val(const IterArgs& a, int s, int64_t d, int b) {
+  return a.y[(d * a.S + s) * a.B + b];
+}
+
+// _split_search (sfft/reconstruct.py:197-215) with the class sums of
+// sub_bucketizer (frameworks.py:524-529): one warp per heavy bucket.
+constexpr int kSrNT = 128;
+__global__ void __launch_bounds__(kSrNT) k_sp_search(IterArgs a) {
+  const int s = blockIdx.y;
+  if (!a.active[s]) return;
+  const IterState& S = a.st[s];
+  const int h = blockIdx.x * (kSrNT / 32) + (threadIdx.x >> 5);
+  if (h >= S.nheavy) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = a.n, L = a.L;
+  const int b = a.heavy[(int64_t)s * a.B + h];
+  const int64_t base = pmod((int64_t)b * L - L / 2, n);
+  const double noise = S.floor / 2.0;
+  const double twopi = 6.283185307179586;
+  int64_t r = 0, scale = 1, depth = 1;
+  int ok = 1;
+  for (int dg = 0; dg < a.digits; ++dg) {
+    const int64_t step = scale * a.branching;
+    depth = step;
+    const int64_t jstep = L / step;
+    const double inv = 1.0 / (double)step;
+    double m1 = -1.0, m2 = -1.0;
+    int64_t i1 = 0;
+    for (int64_t dd = 0; dd < a.branching; ++dd) {
+      const int64_t qc = (base + r + dd * scale) % step;
+      double2 acc = cmk(0.0, 0.0);
+      for (int64_t d = lane; d < step; d += 32) {
+        // exp(2j*pi*d*qc/step) formed as numpy forms it
+        const double th = ((twopi * (double)d) * (double)qc) * inv;
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        acc = cadd(acc, cmul(sp_val(a, s, d * jstep, b), cmk(cs, sn)));
+      }
+      for (int o = 16; o; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      const double mg = cabs_scalar(cmk(acc.x * inv, acc.y * inv));
+      if (mg > m1) {
+        m2 = m1;
+        m1 = mg;
+        i1 = dd;
+      } else if (mg > m2) {
+        m2 = mg;
+      }
+    }
+    if (m1 - m2 < noise) {
+      ok = 0;
+      break;
+    }
+    r += scale * i1;
+    scale = step;
+  }
+  if (lane == 0) {
+    const int64_t i = (int64_t)s * a.B + h;
+    a.sp_r[i] = (int32_t)r;
+    a.sp_ok[i] = ok;
+    a.sp_depth[i] = (int32_t)depth;
+  }
+}
+
+// Prefix over the heavy order of the shifts measured so far (the reference's
+// lazy cache), consistency / weight checks and the estimate
+// y0 * w^{-tau q} / G (frameworks.py:538-554); logs the iteration's reads.
+constexpr int kSckNT = 256;
+__global__ void __launch_bounds__(kSckNT) k_sp_check(IterArgs a) {
+  __shared__ int red[32];
+  __shared__ int smax_tot, ok_tot;
+  const int s = blockIdx.x;
+  if (!a.active[s]) return;
+  IterState& S = a.st[s];
+  const int nh = S.nheavy;
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int64_t sigma = a.item_sigma[s], tau = a.item_tau[s];
+  const int per = (nh + kSckNT - 1) / kSckNT;
+  const int hb = threadIdx.x * per, he = min(nh, hb + per);
+  int32_t* dep = a.sp_depth + (int64_t)s * B;
+  const int32_t* okv = a.sp_ok + (int64_t)s * B;
+  // inclusive prefix max of the depth (steps are powers of the branching, so
+  // the max of a prefix is its largest exponent) and prefix count of located
+  int lm = 0, lc = 0;
+  for (int h = hb; h < he; ++h) {
+    lm = max(lm, (int)dep[h]);
+    lc += okv[h];
+  }
+  // exclusive max-scan of the thread maxima (warp shuffles + warp totals)
+  int xm = lm;
+  const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, xm, o);
+    if (ln >= o) xm = max(xm, t);
+  }
+  __syncthreads();
+  if (ln == 31) red[w] = xm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < kSckNT / 32; ++i) {
+      const int v = red[i];
+      red[i] = run;
+      run = max(run, v);
+    }
+    smax_tot = run;
+  }
+  __syncthreads();
+  int pm = max(red[w], __shfl_up_sync(0xffffffffu, xm, 1));
+  if (ln == 0) pm = red[w];
+  int tot;
+  int pc = block_exscan<kSckNT>(lc, red, &tot);
+  if (threadIdx.x == 0) ok_tot = tot;
+  for (int h = hb; h < he; ++h) {
+    pm = max(pm, (int)dep[h]);
+    pc += okv[h];
+    const int64_t fi = (int64_t)s * B + h;
+    a.f_ok[fi] = 0;
+    if (!okv[h]) continue;
+    const int b = a.heavy[(int64_t)s * B + h];
+    const int64_t q = pmod((int64_t)b * L - L / 2 + a.sp_r[fi], n);
+    const double2 y0 = sp_val(a, s, 0, b);
+    const double tol = fmax(3.0 * S.floor, 0.15 * cabs_scalar(y0));
+    // cached shifts: k * (n / pm) for 1 <= k < pm, and 1, 3 (pc >= 1 here)
+    bool bad = false;
+    const int64_t jst = L / pm;
+    for (int64_t kk = 1; kk < pm && !bad; ++kk) {
+      const int64_t t = kk * (n / pm);
+      const double2 pred = cmul(y0, unit_root(n, mulmod(t % n, q, n)));
+      bad = cabs_scalar(csub(sp_val(a, s, kk * jst, b), pred)) > tol;
+    }
+    for (int u = 0; u < 2 && !bad; ++u) {
+      const int64_t t = u == 0 ? 1 : 3;
+      const double2 pred = cmul(y0, unit_root(n, mulmod(t, q, n)));
+      bad = cabs_scalar(csub(sp_val(a, s, L + u, b), pred)) > tol;
+    }
+    if (bad) continue;
+    const int64_t e = pmod((int64_t)b * L - q, n);
+    const double2 gw = a.gt[(e % L) * B + e / L];
+    if (cabs_scalar(gw) < 0.05 * a.gmax[0]) continue;
+    const double2 coeff = cdiv(cmul(y0, unit_root(n, pmod(-mulmod(tau, q, n), n))), gw);
+    a.f_pos[fi] = mulmod(modinv(sigma, n), q, n);
+    a.f_coef[fi] = coeff;
+    a.f_ok[fi] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // reads of this iteration: shifts k*(n/Smax), k < Smax, then 1 and 3
+    const int smax = max(1, smax_tot);
+    int g = S.ngroups;
+    if (g < kMaxGroups) {
+      Group& G = a.groups[(int64_t)s * kMaxGroups + g];
+      G.kind = 2;
+      G.a = sigma;
+      G.tau = tau;
+      G.cnt = a.omega;
+      G.nsh = smax;
+      G.sh[0] = n / smax;
+      S.ngroups = ++g;
+    }
+    if (ok_tot > 0 && g < kMaxGroups) {
+      Group& G = a.groups[(int64_t)s * kMaxGroups + g];
+      G.kind = 0;
+      G.a = sigma;
+      G.tau = tau;
+      G.cnt = a.omega;
+      G.nsh = 2;
+      G.sh[0] = 1;
+      G.sh[1] = 3;
+      S.ngroups = ++g;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ merge
@@ -825,6 +1094,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(uint32_t) * (size_t)S * ((n + 31) / 32),  // 31 read bitmap (samples_read)
       sizeof(int32_t) * (size_t)S * B,       // 32 heavy_b
       sizeof(int32_t) * (size_t)S * B,       // 33 hrank
+      sizeof(int64_t) * (size_t)M,           // 34 loop shift of each item
+      sizeof(int32_t) * (size_t)S * B * 3,   // 35 split search r / ok / depth
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -904,12 +1175,26 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
                   const double* taps, int64_t omega, int64_t B, const double2* gt,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
                   int P, int64_t pstride, int64_t k, int max_it, const int64_t* ladder, int nlad,
-                  int cap, int64_t* out_pos, double2* out_coef, int32_t* out_n,
-                  int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
+                  int loc, int branching, int cap, int64_t* out_pos, double2* out_coef,
+                  int32_t* out_n, int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
                   int64_t* out_sched, const int32_t* avail, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
-  const int M = 1 + nlad;
-  SFFT_REQUIRE(M <= kMaxShifts, "iterative: ladder too long");
+  SFFT_REQUIRE(loc == 0 || loc == 1, "iterative: location must be 0 (phase) or 1 (split)");
+  const int64_t Lw = B > 0 ? n / B : 0;
+  int digits = 0;
+  if (loc == 1) {
+    SFFT_REQUIRE(B >= 4 && n % B == 0, "iterative: split location needs 4 <= B, B | n");
+    SFFT_REQUIRE(branching >= 2, "iterative: branching must be >= 2");
+    int64_t p = 1;
+    while (p < Lw) {
+      p *= branching;
+      ++digits;
+    }
+    SFFT_REQUIRE(p == Lw, "iterative: bucket width is not a power of the branching factor");
+    SFFT_REQUIRE(2 * max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
+  }
+  const int M = loc == 1 ? (int)Lw + 2 : 1 + nlad;
+  SFFT_REQUIRE(loc == 1 || M <= kMaxShifts, "iterative: ladder too long");
   SFFT_REQUIRE(max_it + 7 <= kMaxGroups, "iterative: max_iterations too large");
   SFFT_REQUIRE(P >= max_it + 6, "iterative: need max_iterations + 6 permutations");
   SFFT_REQUIRE(k <= kFusedMaxB, "iterative: k must be <= 8192");
@@ -931,7 +1216,11 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.M = M;
   a.max_it = max_it;
   a.cap = cap;
-  for (int j = 0; j < nlad; ++j) a.ladder[j] = ladder[j];
+  a.loc = loc;
+  a.branching = branching;
+  a.digits = digits;
+  if (loc == 0)
+    for (int j = 0; j < nlad; ++j) a.ladder[j] = ladder[j];
   a.psig = psig;
   a.ptau = ptau;
   a.gt = gt;
@@ -975,7 +1264,26 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   uint32_t* bitmap = (uint32_t*)(w + Lo.off[31]);
   a.heavy_b = (int32_t*)(w + Lo.off[32]);
   a.hrank = (int32_t*)(w + Lo.off[33]);
+  int64_t* shifts = (int64_t*)(w + Lo.off[34]);
+  a.shifts = shifts;
+  a.sp_r = (int32_t*)(w + Lo.off[35]);
+  a.sp_ok = a.sp_r + (size_t)S * B;
+  a.sp_depth = a.sp_ok + (size_t)S * B;
   void* bws = w + Lo.total;
+  {
+    // loop shifts: phase {0} + ladder; split {d*B : d < L} + {1, 3}
+    std::vector<int64_t> sh(M);
+    if (loc == 0) {
+      sh[0] = 0;
+      for (int j = 1; j < M; ++j) sh[j] = ladder[j - 1];
+    } else {
+      for (int64_t d = 0; d < Lw; ++d) sh[d] = d * B;
+      sh[Lw] = 1;
+      sh[Lw + 1] = 3;
+    }
+    SFFT_CUDA(cudaMemcpyAsync(shifts, sh.data(), sizeof(int64_t) * M, cudaMemcpyHostToDevice, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));  // sh is a host temporary
+  }
   const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
 
   // all slots free; queue counter 0
@@ -1028,9 +1336,19 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     if (rc) return rc;
     k_it_decide<<<S, kDecNT, dsm, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_decide");
-    const int lts = t_max > 256 ? splits(t_max, 256, kMaxLadSplit) : 0;
-    rc = launch_locate(a, M, B, S, lts, st);
-    if (rc) return rc;
+    if (loc == 0) {
+      const int lts = t_max > 256 ? splits(t_max, 256, kMaxLadSplit) : 0;
+      rc = launch_locate(a, M, B, S, lts, st);
+      if (rc) return rc;
+    } else {
+      const unsigned hb = (unsigned)cdiv_up(B, kSpH);
+      k_sp_model<<<dim3(hb, (unsigned)cdiv_up(M - 1, kSpJ), S), kSpNT, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_sp_model");
+      k_sp_search<<<dim3((unsigned)cdiv_up(B, kSrNT / 32), S), kSrNT, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_sp_search");
+      k_sp_check<<<S, kSckNT, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_sp_check");
+    }
     k_it_merge<<<S, kMrgNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_merge");
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,

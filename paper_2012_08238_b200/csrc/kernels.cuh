@@ -126,8 +126,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
                   const double* taps, int64_t omega, int64_t B, const double2* gt,
                   const double* gmax, const double2* W, const int64_t* psig, const int64_t* ptau,
                   int P, int64_t pstride, int64_t k, int max_it, const int64_t* ladder, int nlad,
-                  int cap, int64_t* out_pos, double2* out_coef, int32_t* out_n,
-                  int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
+                  int loc, int branching, int cap, int64_t* out_pos, double2* out_coef,
+                  int32_t* out_n, int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
                   int64_t* out_sched, const int32_t* avail, void* ws, size_t ws_bytes,
                   cudaStream_t st);
 

@@ -20,12 +20,15 @@ constexpr int kMaxShifts = 16;
 constexpr int kMaxGroups = 64;
 constexpr int kMaxPieces = 2 * kMaxShifts;
 
+// kind 2 (flat, arithmetic shifts): the split-location measurements of one
+// loop iteration, shifts k*sh[0] for k < nsh (sfft/frameworks.py:524-529:
+// d*(n/step) for d < step); nsh may exceed kMaxShifts.
 struct Group {
   int64_t a;     // flat: sigma | spike: stride L
   int64_t tau;   // base shift
   int64_t cnt;   // flat: Omega | spike: number of samples
-  int32_t kind;  // 0 flat, 1 spike
-  int32_t nsh;   // extra shifts (flat)
+  int32_t kind;  // 0 flat, 1 spike, 2 flat with shifts k*sh[0], k < nsh
+  int32_t nsh;   // extra shifts (flat) | shift count (kind 2)
   int64_t sh[kMaxShifts];
 };
 
@@ -59,6 +62,13 @@ __device__ inline void merge_pieces(const Group& g, int64_t n, GroupSh* out) {
     return;
   }
   const int64_t w = g.cnt >= n ? n : g.cnt;
+  if (g.kind == 2) {  // arcs [-tau - k*step, +w): disjoint when step >= w, else one run
+    const int64_t step = g.sh[0], c = g.nsh;
+    out->np = 0;
+    out->total = step >= w ? min(n, c * w) : min(n, (c - 1) * step + w);
+    out->ainv = modinv(g.a, n);
+    return;
+  }
   for (int d = 0; d < g.nsh; ++d) {
     const int64_t s = pmod(-g.tau - g.sh[d], n);
     if (w >= n) { lo[m] = 0; hi[m] = n; ++m; continue; }
@@ -101,6 +111,18 @@ __device__ __forceinline__ bool group_has(const Group& g, const GroupSh& gs, int
     return (v % g.a) == 0 && (v / g.a) < g.cnt;
   }
   const int64_t t = mulmod_n(gs.ainv, e, n, mask);
+  if (g.kind == 2) {
+    // (v + k*step) mod n in [0, w) for some k < c, v = t + tau; step | n
+    const int64_t w = g.cnt >= n ? n : g.cnt;
+    if (w >= n) return true;
+    const int64_t step = g.sh[0], c = g.nsh, S = n / step;
+    const int64_t v = pmod(t + g.tau, n);
+    const int64_t r = v % step, j0 = v / step;
+    if (r >= w) return false;
+    int64_t jm = (w - r + step - 1) / step;
+    jm = jm < S ? jm : S;
+    return j0 < jm || j0 + c - 1 >= S;
+  }
   for (int i = 0; i < gs.np; ++i)
     if (t >= gs.lo[i] && t < gs.hi[i]) return true;
   return false;
@@ -110,6 +132,15 @@ __device__ __forceinline__ bool group_has(const Group& g, const GroupSh& gs, int
 __device__ __forceinline__ int64_t group_elem(const Group& g, const GroupSh& gs, int64_t n,
                                               int64_t j, int64_t mask) {
   if (g.kind == 1) return pmod(g.a * j - g.tau, n);
+  if (g.kind == 2) {
+    const int64_t w = g.cnt >= n ? n : g.cnt;
+    const int64_t step = g.sh[0], c = g.nsh;
+    int64_t u;
+    if (w >= n) u = j;
+    else if (step >= w) u = -g.tau - (j / w) * step + (j % w);
+    else u = -g.tau - (c - 1) * step + j;
+    return mulmod_n(g.a, pmod(u, n), n, mask);
+  }
   for (int i = 0; i < gs.np; ++i) {
     const int64_t len = gs.hi[i] - gs.lo[i];
     if (j < len) return mulmod_n(g.a, gs.lo[i] + j, n, mask);
@@ -140,7 +171,8 @@ static __global__ void k_export_groups(const Group* __restrict__ groups, const i
     o[2] = q.tau;
     o[3] = q.cnt;
     o[4] = q.nsh;
-    for (int i = 0; i < kMaxShifts; ++i) o[5 + i] = i < q.nsh ? q.sh[i] : 0;
+    const int ns = q.kind == 2 ? 1 : q.nsh;
+    for (int i = 0; i < kMaxShifts; ++i) o[5 + i] = i < ns ? q.sh[i] : 0;
   }
 }
 

@@ -150,6 +150,10 @@ class BatchResult:
             if kind == 0:
                 for d in row[5:5 + nsh]:
                     out.append(("flat", a, (tau + int(d)) % self.n, cnt))
+            elif kind == 2:  # split location: shifts j * row[5], j < nsh
+                step = int(row[5])
+                for j in range(nsh):
+                    out.append(("flat", a, (tau + j * step) % self.n, cnt))
             else:
                 out.append(("spike", a, tau % self.n, cnt))
         return out
@@ -245,7 +249,7 @@ DEFAULT_SLOTS = 128
 
 def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = None,
                         avail=None, engines: int = 1) -> BatchResult:
-    """run_iterative (phase location) for every row of ``xs``.
+    """run_iterative (phase, binary or multiscale location) for every row of ``xs``.
 
     The device engine keeps ``slots`` signals in flight (default
     min(len(xs), 128)) and refills a slot from the queue as soon as its signal
@@ -265,18 +269,29 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
     dev = X.device
     if k <= 0:
         return _empty_batch(n, S, 0, dev, 0, True)
-    if cfg.location_method != "phase":
-        raise NotImplementedError(
-            "binary/multiscale location is outside the device hot path (SURVEY.md §8(f) #1)")
     b = cfg.resolve_buckets(n, k)
+    split = cfg.location_method in ("binary", "multiscale")
+    if split:
+        # class-split location (frameworks.py:517-522): n/B = branching^digits
+        br = 2 if cfg.location_method == "binary" else cfg.branching
+        width = n // b
+        digits = round(math.log(width, br)) if br >= 2 and width >= 1 else 0
+        if br < 2 or br ** digits != width:
+            raise ConfigMismatch(f"bucket width {width} is not a power of branching {br}")
+        ladder, M = [], width + 2
+        # every loop keeps n/B + 2 bucketizations per slot: bound the slots by memory
+        slot_cap = max(1, (8 << 30) // (M * b * 16))
+    else:
+        br = 0
+        ladder = phase_ladder(n)
+        M = 1 + len(ladder)
+        slot_cap = S
     filt = make_flat_filter(n, b, device=dev)
-    ladder = phase_ladder(n)
-    M = 1 + len(ladder)
     P = cfg.max_iterations + 6
     sig, tau = draw_perms(n, cfg.seed, P)
     psig = torch.as_tensor(sig, device=dev)    # one stream shared by all signals
     ptau = torch.as_tensor(tau, device=dev)
-    nslots = min(S, slots or DEFAULT_SLOTS)
+    nslots = min(S, slots or DEFAULT_SLOTS, slot_cap)
     cap = cfg.max_iterations * b
     out_pos = torch.zeros((S, k), dtype=torch.int64, device=dev)
     out_coef = torch.zeros((S, k), dtype=torch.complex128, device=dev)
@@ -289,13 +304,14 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
     wsb = L.sfft_iterative_ws_bytes(n, b, nslots, M, cap)
     ws = _WS.get(wsb, dev, tag=f"it{torch.cuda.current_stream(dev).cuda_stream}")
     import ctypes
-    lad = (ctypes.c_int64 * len(ladder))(*ladder)
+    lad = (ctypes.c_int64 * len(ladder))(*ladder) if ladder else None
     dt = 0 if X.dtype == torch.complex64 else 1
     gmax = torch.tensor([filt.peak], dtype=torch.float64, device=dev)
     check(L.sfft_run_iterative(dt, ptr(X), n, X.stride(0), S, nslots, ptr(filt.taps),
                                filt.support, b, ptr(filt.gtable), ptr(gmax),
                                ptr(twiddles(b, dev)), ptr(psig), ptr(ptau), P, 0, k,
-                               cfg.max_iterations, lad, len(ladder), cap,
+                               cfg.max_iterations, lad, len(ladder), 1 if split else 0, br,
+                               cap,
                                ptr(out_pos), ptr(out_coef), ptr(out_n), ptr(out_it), ptr(out_cv),
                                ptr(out_sm), ptr(sched), ptr(avail), ptr(ws), wsb,
                                stream_of(dev)), "sfft_run_iterative")
@@ -367,8 +383,9 @@ def run_iterative_stream(host_x, k: int, cfg: AlgorithmConfig, slots: int | None
 
 
 def run_iterative(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
-    """Permute, bucketize, locate single-tons by phase, subtract, repeat
-    (sfft/frameworks.py:439-570), then polish (:573-608)."""
+    """Permute, bucketize, locate single-tons (phase ladder or binary /
+    multiscale class splits), subtract, repeat (sfft/frameworks.py:439-570),
+    then polish (:573-608)."""
     return _single(run_iterative_batch, x, k, cfg)
 
 
