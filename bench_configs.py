@@ -32,6 +32,14 @@ CONFIGS = {
     "C5a": ("voting", 1 << 22, 50, 40.0, dict(num_buckets=1 << 14, rounds=10), "complex64", False),
     "C5b": ("voting", 1 << 22, 512, 10.0, dict(num_buckets=1 << 16, rounds=10), "complex64",
             False),
+    # class-split location (n/B shifted bucketizations per loop)
+    "C1bin": ("iterative", 1 << 16, 16, None, dict(num_buckets=256, location_method="binary"),
+              "complex128", False),
+    "C1ms4": ("iterative", 1 << 16, 16, 30.0,
+              dict(num_buckets=256, location_method="multiscale", branching=4), "complex128",
+              False),
+    "C3bin": ("iterative", 1 << 22, 256, 30.0, dict(num_buckets=4096, location_method="binary"),
+              "complex64", True),
 }
 
 
@@ -85,6 +93,8 @@ def run(name, S, reps, check):
     L.sfft_prof_enable(0)
     sin = 8 if dtype == "complex64" else 16
     om = omega_of(fwk, n, kw)
+    if kw.get("location_method") in ("binary", "multiscale") and n > (1 << 16):
+        check = 0  # the oracle needs minutes per split-location transform at this size
     if om is None:  # spike: B_j samples gathered and written per item, mixed sizes
         per_item = sum(3 * (n // p) * (sin + 16) for p in kw["coprime_factors"]) / 9
     else:
@@ -124,6 +134,8 @@ def main():
         S = args.signals if CONFIGS[name][1] <= (1 << 20) else max(1, args.signals // 2)
         if name == "C5b":
             S = min(S, 64)
+        if name == "C3bin":
+            S = min(S, 32)
         t0 = time.time()
         r = run(name, S, args.reps, args.check)
         r["wall_s"] = time.time() - t0

@@ -23,9 +23,10 @@
 // L = N/B shifts d*B (d < L, every d*(n/step) the split search can ask for)
 // plus the alias-check shifts 1 and 3; k_sp_model subtracts the recovered
 // model from them at the heavy buckets, k_sp_search runs the digit-by-digit
-// split per heavy bucket (one warp each) and k_sp_check applies the
-// consistency checks against the shifts the reference would have cached by
-// then (a prefix over the heavy order), the weight check and the estimate.
+// split per heavy bucket (one warp each), k_sp_prefix forms the shifts the
+// reference would have cached by then (a prefix over the heavy order) and
+// k_sp_verify applies the consistency checks, the weight check and the
+// estimate.
 #include "kernels.cuh"
 #include "schedule.cuh"
 #include "finalize.cuh"
@@ -694,37 +695,34 @@ __global__ void __launch_bounds__(kSrNT) k_sp_search(IterArgs a) {
 }
 
 // Prefix over the heavy order of the shifts measured so far (the reference's
-// lazy cache), consistency / weight checks and the estimate
-// y0 * w^{-tau q} / G (frameworks.py:538-554); logs the iteration's reads.
+// lazy cache, frameworks.py:470-476 / :538-541): sp_depth[h] becomes the
+// largest step any bucket up to h measured.  Logs the iteration's reads.
 constexpr int kSckNT = 256;
-__global__ void __launch_bounds__(kSckNT) k_sp_check(IterArgs a) {
+__global__ void __launch_bounds__(kSckNT) k_sp_prefix(IterArgs a) {
   __shared__ int red[32];
-  __shared__ int smax_tot, ok_tot;
+  __shared__ int smax_tot;
   const int s = blockIdx.x;
   if (!a.active[s]) return;
   IterState& S = a.st[s];
   const int nh = S.nheavy;
-  const int64_t n = a.n, B = a.B, L = a.L;
-  const int64_t sigma = a.item_sigma[s], tau = a.item_tau[s];
+  const int64_t n = a.n, B = a.B;
   const int per = (nh + kSckNT - 1) / kSckNT;
   const int hb = threadIdx.x * per, he = min(nh, hb + per);
   int32_t* dep = a.sp_depth + (int64_t)s * B;
   const int32_t* okv = a.sp_ok + (int64_t)s * B;
-  // inclusive prefix max of the depth (steps are powers of the branching, so
-  // the max of a prefix is its largest exponent) and prefix count of located
   int lm = 0, lc = 0;
   for (int h = hb; h < he; ++h) {
     lm = max(lm, (int)dep[h]);
     lc += okv[h];
   }
-  // exclusive max-scan of the thread maxima (warp shuffles + warp totals)
+  // exclusive max-scan of the per-thread maxima
   int xm = lm;
   const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int o = 1; o < 32; o <<= 1) {
     const int t = __shfl_up_sync(0xffffffffu, xm, o);
     if (ln >= o) xm = max(xm, t);
   }
-  __syncthreads();
+  const int prev = __shfl_up_sync(0xffffffffu, xm, 1);
   if (ln == 31) red[w] = xm;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -737,46 +735,16 @@ __global__ void __launch_bounds__(kSckNT) k_sp_check(IterArgs a) {
     smax_tot = run;
   }
   __syncthreads();
-  int pm = max(red[w], __shfl_up_sync(0xffffffffu, xm, 1));
-  if (ln == 0) pm = red[w];
-  int tot;
-  int pc = block_exscan<kSckNT>(lc, red, &tot);
-  if (threadIdx.x == 0) ok_tot = tot;
+  int pm = ln == 0 ? red[w] : max(red[w], prev);
   for (int h = hb; h < he; ++h) {
     pm = max(pm, (int)dep[h]);
-    pc += okv[h];
-    const int64_t fi = (int64_t)s * B + h;
-    a.f_ok[fi] = 0;
-    if (!okv[h]) continue;
-    const int b = a.heavy[(int64_t)s * B + h];
-    const int64_t q = pmod((int64_t)b * L - L / 2 + a.sp_r[fi], n);
-    const double2 y0 = sp_val(a, s, 0, b);
-    const double tol = fmax(3.0 * S.floor, 0.15 * cabs_scalar(y0));
-    // cached shifts: k * (n / pm) for 1 <= k < pm, and 1, 3 (pc >= 1 here)
-    bool bad = false;
-    const int64_t jst = L / pm;
-    for (int64_t kk = 1; kk < pm && !bad; ++kk) {
-      const int64_t t = kk * (n / pm);
-      const double2 pred = cmul(y0, unit_root(n, mulmod(t % n, q, n)));
-      bad = cabs_scalar(csub(sp_val(a, s, kk * jst, b), pred)) > tol;
-    }
-    for (int u = 0; u < 2 && !bad; ++u) {
-      const int64_t t = u == 0 ? 1 : 3;
-      const double2 pred = cmul(y0, unit_root(n, mulmod(t, q, n)));
-      bad = cabs_scalar(csub(sp_val(a, s, L + u, b), pred)) > tol;
-    }
-    if (bad) continue;
-    const int64_t e = pmod((int64_t)b * L - q, n);
-    const double2 gw = a.gt[(e % L) * B + e / L];
-    if (cabs_scalar(gw) < 0.05 * a.gmax[0]) continue;
-    const double2 coeff = cdiv(cmul(y0, unit_root(n, pmod(-mulmod(tau, q, n), n))), gw);
-    a.f_pos[fi] = mulmod(modinv(sigma, n), q, n);
-    a.f_coef[fi] = coeff;
-    a.f_ok[fi] = 1;
+    dep[h] = pm;
   }
-  __syncthreads();
+  int tot;
+  block_exscan<kSckNT>(lc, red, &tot);
   if (threadIdx.x == 0) {
     // reads of this iteration: shifts k*(n/Smax), k < Smax, then 1 and 3
+    const int64_t sigma = a.item_sigma[s], tau = a.item_tau[s];
     const int smax = max(1, smax_tot);
     int g = S.ngroups;
     if (g < kMaxGroups) {
@@ -789,7 +757,7 @@ __global__ void __launch_bounds__(kSckNT) k_sp_check(IterArgs a) {
       G.sh[0] = n / smax;
       S.ngroups = ++g;
     }
-    if (ok_tot > 0 && g < kMaxGroups) {
+    if (tot > 0 && g < kMaxGroups) {
       Group& G = a.groups[(int64_t)s * kMaxGroups + g];
       G.kind = 0;
       G.a = sigma;
@@ -801,6 +769,57 @@ __global__ void __launch_bounds__(kSckNT) k_sp_check(IterArgs a) {
       S.ngroups = ++g;
     }
   }
+}
+
+// Consistency checks against the cached shifts k*(n/pm), 1 <= k < pm, and
+// 1, 3 (lanes split the shifts, one warp per located bucket), the weight
+// check and the estimate y0 * w^{-tau q} / G (frameworks.py:538-554).
+constexpr int kVfNT = 128;
+__global__ void __launch_bounds__(kVfNT) k_sp_verify(IterArgs a) {
+  const int s = blockIdx.y;
+  if (!a.active[s]) return;
+  const IterState& S = a.st[s];
+  const int h = blockIdx.x * (kVfNT / 32) + (threadIdx.x >> 5);
+  if (h >= S.nheavy) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int64_t fi = (int64_t)s * B + h;
+  if (!a.sp_ok[fi]) {
+    if (lane == 0) a.f_ok[fi] = 0;
+    return;
+  }
+  const int b = a.heavy[fi];
+  const int64_t q = pmod((int64_t)b * L - L / 2 + a.sp_r[fi], n);
+  const double2 y0 = sp_val(a, s, 0, b);
+  const double tol = fmax(3.0 * S.floor, 0.15 * cabs_scalar(y0));
+  const int64_t pm = a.sp_depth[fi];
+  const int64_t jst = L / pm, tst = n / pm;
+  bool bad = false;
+  // shifts k*(n/pm) for 1 <= k < pm (item k*jst), then 1 and 3 (items L, L+1)
+  for (int64_t kk = 1 + lane; kk < pm + 2 && !bad; kk += 32) {
+    int64_t t, item;
+    if (kk < pm) {
+      t = kk * tst;
+      item = kk * jst;
+    } else {
+      t = kk == pm ? 1 : 3;
+      item = L + (kk - pm);
+    }
+    const double2 pred = cmul(y0, unit_root(n, mulmod(t % n, q, n)));
+    bad = cabs_scalar(csub(sp_val(a, s, item, b), pred)) > tol;
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane != 0) return;
+  a.f_ok[fi] = 0;
+  if (bad) return;
+  const int64_t e = pmod((int64_t)b * L - q, n);
+  const double2 gw = a.gt[(e % L) * B + e / L];
+  if (cabs_scalar(gw) < 0.05 * a.gmax[0]) return;
+  const double2 coeff =
+      cdiv(cmul(y0, unit_root(n, pmod(-mulmod(a.item_tau[s], q, n), n))), gw);
+  a.f_pos[fi] = mulmod(modinv(a.item_sigma[s], n), q, n);
+  a.f_coef[fi] = coeff;
+  a.f_ok[fi] = 1;
 }
 
 // ------------------------------------------------------------------ merge
@@ -1346,8 +1365,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
       SFFT_CHECK_LAUNCH("k_sp_model");
       k_sp_search<<<dim3((unsigned)cdiv_up(B, kSrNT / 32), S), kSrNT, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_sp_search");
-      k_sp_check<<<S, kSckNT, 0, st>>>(a);
-      SFFT_CHECK_LAUNCH("k_sp_check");
+      k_sp_prefix<<<S, kSckNT, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_sp_prefix");
+      k_sp_verify<<<dim3((unsigned)cdiv_up(B, kVfNT / 32), S), kVfNT, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_sp_verify");
     }
     k_it_merge<<<S, kMrgNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_merge");
