@@ -114,7 +114,7 @@ __device__ __forceinline__ double2 produce(const Prod& p, const ItemCtx& c, int 
     }
     return acc;
   } else {
-    return p.z[(int64_t)item * p.B + s];
+    return p.z[out_row(p, item) * p.B + s];
   }
 }
 

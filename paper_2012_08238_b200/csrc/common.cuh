@@ -208,6 +208,9 @@ struct Sample<double2> {
   }
 };
 
+__device__ __forceinline__ double2 to_d2_(float2 v) { return cmk((double)v.x, (double)v.y); }
+__device__ __forceinline__ double2 to_d2_(double2 v) { return v; }
+
 // ----------------------------------------------------------------- misc
 SFFT_HD int64_t cdiv_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

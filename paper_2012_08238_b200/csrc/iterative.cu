@@ -64,7 +64,9 @@ struct IterArgs {
   int Q;                         // signals in the queue
   const int32_t* avail;          // optional: signals [0, *avail) have arrived in HBM
   int64_t pstride;               // perms row stride per signal (0: shared stream)
-  int32_t* item_active;          // [S*M]
+  int32_t* item_active;          // [S*M] items of the per-item flat bucketization
+  int32_t* item_fold;            // [S*M] split loop items d*B of the row-correlation path
+  int use_fold;                  // split location folds its loop shifts d*B as a row correlation
   int32_t* pgate;                // [S] polish pass this round
   int64_t ladder[kMaxShifts];    // d_1..d_{M-1} (phase location)
   const int64_t* shifts;         // [M] shift of loop item j (device)
@@ -230,7 +232,10 @@ __global__ void k_cb_items(IterArgs a) {
   const int s = i / a.M, j = i - s * a.M;
   const IterState& S = a.st[s];
   const bool on = j < S.nsh;
-  a.item_active[i] = on;
+  // split location: the loop shifts d*B (d < L) are folded as a row correlation
+  const bool fold = on && a.use_fold && S.phase == PH_LOOP && j < a.L;
+  a.item_active[i] = on && !fold;
+  a.item_fold[i] = fold;
   a.item_sig[i] = S.sig > 0 ? S.sig : 0;
   if (!on) return;
   const int64_t d = (S.phase == PH_LOOP) ? a.shifts[j] : j;
@@ -694,6 +699,76 @@ __global__ void __launch_bounds__(kSrNT) k_sp_search(IterArgs a) {
   }
 }
 
+
+// ------------------------------------------------------------------ split fold
+// The split loop measures shifts d*B for every d < L with one sigma: sample i
+// of item d is U[i - d*B], U[u] = x[sigma (u - tau)], so in the fold matrix
+// (rows of B) item d reads the same columns d rows higher:
+//   folded_d[c] = sum_{r < R_c} taps[c + rB] * U[c + (r - d)B]   (rows in order)
+// One CTA owns 32 columns x kFdJ shifts: it gathers the (kFdJ + R - 1) rows of
+// its columns once (instead of kFdJ x R gathers), forms the sums from shared
+// memory in the reference's row order, and writes the folded slots into y;
+// the B-point FFTs then run in place (PROD_LOAD).  The values equal the
+// per-item fold bit for bit.
+constexpr int kFdNT = 256, kFdC = 32, kFdJ = 64, kFdRmax = 64;
+
+template <typename Tin>
+__global__ void __launch_bounds__(kFdNT) k_sp_fold(IterArgs a, const void* __restrict__ xv,
+                                                   int64_t xstride,
+                                                   const double* __restrict__ taps, int R) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int s = blockIdx.z;
+  if (!a.active[s]) return;
+  const int64_t n = a.n, B = a.B, L = a.L, omega = a.omega;
+  const int64_t c0 = (int64_t)blockIdx.x * kFdC;
+  const int64_t j0 = (int64_t)blockIdx.y * kFdJ;
+  if (j0 >= L) return;
+  const int64_t j1 = min(L, j0 + kFdJ);
+  const int64_t wlo = -(j1 - 1), whi = R - j0;  // rows [wlo, whi)
+  const int nrow = (int)(whi - wlo);
+  Tin* V = (Tin*)fsm;                                        // [nrow][kFdC]
+  double* G = (double*)(fsm + (size_t)(kFdRmax + kFdJ) * kFdC * sizeof(Tin));  // [R][kFdC]
+  const int64_t sigma = a.item_sigma[s], tau = a.item_tau[s];
+  const Tin* xs = (const Tin*)xv + (int64_t)a.st[s].sig * xstride;
+  const int c = threadIdx.x & (kFdC - 1), g = threadIdx.x / kFdC;
+  constexpr int NG = kFdNT / kFdC;
+  {
+    // column c, rows wlo + g, wlo + g + NG, ...: u advances by NG*B
+    int64_t u = c0 + c + (wlo + g) * B;
+    int64_t idx = mulmod(sigma, pmod(u - tau, n), n);
+    const int64_t step = mulmod(sigma, (NG * B) % n, n);
+    for (int w = g; w < nrow; w += NG) {
+      if (u < omega) V[w * kFdC + c] = __ldcg(xs + idx);
+      u += NG * B;
+      idx += step;
+      idx -= (idx >= n) ? n : 0;
+    }
+    for (int r = g; r < R; r += NG) {
+      const int64_t i = c0 + c + (int64_t)r * B;
+      G[r * kFdC + c] = i < omega ? __ldg(taps + i) : 0.0;
+    }
+  }
+  __syncthreads();
+  const int64_t col = c0 + c;
+  const int Rc = (int)((omega - col + B - 1) / B);  // rows of slot col
+  for (int64_t j = j0 + g; j < j1; j += NG) {
+    // u row of (r, j) is r - j; shared row index r - j - wlo
+    const Tin* v = V + (int)(-j - wlo) * kFdC + c;
+    double2 acc = cmk(0.0, 0.0);
+    for (int r = 0; r < Rc; ++r) {
+      const double gg = G[r * kFdC + c];
+      const double2 x = to_d2_(v[r * kFdC]);
+      acc = cadd_rn(acc, cmk(__dmul_rn(gg, x.x), __dmul_rn(gg, x.y)));
+    }
+    a.y[(j * a.S + s) * B + col] = acc;
+  }
+}
+
+template <typename Tin>
+static size_t sp_fold_smem() {
+  return (size_t)(kFdRmax + kFdJ) * kFdC * sizeof(Tin) + (size_t)kFdRmax * kFdC * sizeof(double);
+}
+
 // Prefix over the heavy order of the shifts measured so far (the reference's
 // lazy cache, frameworks.py:470-476 / :538-541): sp_depth[h] becomes the
 // largest step any bucket up to h measured.  Logs the iteration's reads.
@@ -1115,6 +1190,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * B,       // 33 hrank
       sizeof(int64_t) * (size_t)M,           // 34 loop shift of each item
       sizeof(int32_t) * (size_t)S * B * 3,   // 35 split search r / ok / depth
+      sizeof(int32_t) * (size_t)S * M,       // 36 item_fold
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -1288,6 +1364,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.sp_r = (int32_t*)(w + Lo.off[35]);
   a.sp_ok = a.sp_r + (size_t)S * B;
   a.sp_depth = a.sp_ok + (size_t)S * B;
+  a.item_fold = (int32_t*)(w + Lo.off[36]);
   void* bws = w + Lo.total;
   {
     // loop shifts: phase {0} + ladder; split {d*B : d < L} + {1, 3}
@@ -1325,6 +1402,22 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   p.out_M = M;
   p.out_S = S;
 
+  // split location: row-correlation fold when a CTA can hold its rows
+  const int fold_R = (loc == 1 && B % kFdC == 0 && cdiv_up(omega, B) <= kFdRmax &&
+                      !getenv("SFFT_NO_SPLIT_FOLD"))
+                         ? (int)cdiv_up(omega, B)
+                         : 0;
+  a.use_fold = fold_R > 0;
+  Prod pl = p;
+  pl.z = a.y;
+  pl.item_active = a.item_fold;
+  if (fold_R > 0) {
+    SFFT_CUDA(cudaFuncSetAttribute(k_sp_fold<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sp_fold_smem<float2>()));
+    SFFT_CUDA(cudaFuncSetAttribute(k_sp_fold<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sp_fold_smem<double2>()));
+  }
+
   const size_t dsm = (size_t)kFusedMaxB * (8 + 8 + 4);
   SFFT_CUDA(cudaFuncSetAttribute(k_it_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   SFFT_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
@@ -1348,6 +1441,17 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CHECK_LAUNCH("k_cb_items");
     int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
     if (rc) return rc;
+    if (fold_R > 0) {
+      // split loop shifts d*B: row-correlation fold, then the FFTs in place
+      dim3 gf((unsigned)(B / kFdC), (unsigned)cdiv_up(Lw, kFdJ), S);
+      if (dtype == 0)
+        k_sp_fold<float2><<<gf, kFdNT, sp_fold_smem<float2>(), st>>>(a, x, xstride, taps, fold_R);
+      else
+        k_sp_fold<double2><<<gf, kFdNT, sp_fold_smem<double2>(), st>>>(a, x, xstride, taps, fold_R);
+      SFFT_CHECK_LAUNCH("k_sp_fold");
+      rc = run_bucketize(dtype, PROD_LOAD, pl, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
+      if (rc) return rc;
+    }
     // ---- loop slots
     rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st,
