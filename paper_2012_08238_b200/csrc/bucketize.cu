@@ -118,30 +118,33 @@ __device__ __forceinline__ double2 produce(const Prod& p, const ItemCtx& c, int 
   }
 }
 
-// Two flat slots at once (8 gathers in flight per thread); each slot's rows
-// are still summed in row order without FMA contraction.
+// Two flat slots at once (8 gathers in flight per thread): slot s0 of item
+// ca and slot s1 >= s0 of item cb (the same or another item).  Each slot's
+// rows are still summed in row order without FMA contraction.
 template <typename Tin>
-__device__ __forceinline__ void produce_flat2(const Prod& p, const ItemCtx& c, int64_t s0,
-                                              int64_t s1, double2* o0, double2* o1) {
+__device__ __forceinline__ void produce_flat2(const Prod& p, const ItemCtx& ca, int64_t s0,
+                                              const ItemCtx& cb, int64_t s1, double2* o0,
+                                              double2* o1) {
   const int64_t n = p.n;
-  const Tin* xs = (const Tin*)c.xs;
-  int64_t ia = mulmod(c.a, pmod(s0 - c.b, n), n);
-  int64_t ib = mulmod(c.a, pmod(s1 - c.b, n), n);
+  const Tin* xa = (const Tin*)ca.xs;
+  const Tin* xb = (const Tin*)cb.xs;
+  int64_t ia = mulmod(ca.a, pmod(s0 - ca.b, n), n);
+  int64_t ib = mulmod(cb.a, pmod(s1 - cb.b, n), n);
   double2 aa = cmk(0.0, 0.0), ab = cmk(0.0, 0.0);
   int64_t i = s0, k = s1;
   const int64_t B = p.B;
   // s1 > s0, so slot s1 runs out of rows first or at the same time
   for (; k + 3 * B < p.omega; i += 4 * B, k += 4 * B) {
-    int64_t ia1 = ia + c.step; ia1 -= (ia1 >= n) ? n : 0;
-    int64_t ia2 = ia1 + c.step; ia2 -= (ia2 >= n) ? n : 0;
-    int64_t ia3 = ia2 + c.step; ia3 -= (ia3 >= n) ? n : 0;
-    int64_t ib1 = ib + c.step; ib1 -= (ib1 >= n) ? n : 0;
-    int64_t ib2 = ib1 + c.step; ib2 -= (ib2 >= n) ? n : 0;
-    int64_t ib3 = ib2 + c.step; ib3 -= (ib3 >= n) ? n : 0;
-    const double2 va0 = Sample<Tin>::load(xs, ia), va1 = Sample<Tin>::load(xs, ia1);
-    const double2 va2 = Sample<Tin>::load(xs, ia2), va3 = Sample<Tin>::load(xs, ia3);
-    const double2 vb0 = Sample<Tin>::load(xs, ib), vb1 = Sample<Tin>::load(xs, ib1);
-    const double2 vb2 = Sample<Tin>::load(xs, ib2), vb3 = Sample<Tin>::load(xs, ib3);
+    int64_t ia1 = ia + ca.step; ia1 -= (ia1 >= n) ? n : 0;
+    int64_t ia2 = ia1 + ca.step; ia2 -= (ia2 >= n) ? n : 0;
+    int64_t ia3 = ia2 + ca.step; ia3 -= (ia3 >= n) ? n : 0;
+    int64_t ib1 = ib + cb.step; ib1 -= (ib1 >= n) ? n : 0;
+    int64_t ib2 = ib1 + cb.step; ib2 -= (ib2 >= n) ? n : 0;
+    int64_t ib3 = ib2 + cb.step; ib3 -= (ib3 >= n) ? n : 0;
+    const double2 va0 = Sample<Tin>::load(xa, ia), va1 = Sample<Tin>::load(xa, ia1);
+    const double2 va2 = Sample<Tin>::load(xa, ia2), va3 = Sample<Tin>::load(xa, ia3);
+    const double2 vb0 = Sample<Tin>::load(xb, ib), vb1 = Sample<Tin>::load(xb, ib1);
+    const double2 vb2 = Sample<Tin>::load(xb, ib2), vb3 = Sample<Tin>::load(xb, ib3);
     const double ga0 = __ldg(p.taps + i), ga1 = __ldg(p.taps + i + B);
     const double ga2 = __ldg(p.taps + i + 2 * B), ga3 = __ldg(p.taps + i + 3 * B);
     const double gb0 = __ldg(p.taps + k), gb1 = __ldg(p.taps + k + B);
@@ -154,21 +157,21 @@ __device__ __forceinline__ void produce_flat2(const Prod& p, const ItemCtx& c, i
     ab = cadd_rn(ab, cmk(__dmul_rn(gb1, vb1.x), __dmul_rn(gb1, vb1.y)));
     ab = cadd_rn(ab, cmk(__dmul_rn(gb2, vb2.x), __dmul_rn(gb2, vb2.y)));
     ab = cadd_rn(ab, cmk(__dmul_rn(gb3, vb3.x), __dmul_rn(gb3, vb3.y)));
-    ia = ia3 + c.step; ia -= (ia >= n) ? n : 0;
-    ib = ib3 + c.step; ib -= (ib >= n) ? n : 0;
+    ia = ia3 + ca.step; ia -= (ia >= n) ? n : 0;
+    ib = ib3 + cb.step; ib -= (ib >= n) ? n : 0;
   }
   for (; i < p.omega; i += B) {
-    const double2 v = Sample<Tin>::load(xs, ia);
+    const double2 v = Sample<Tin>::load(xa, ia);
     const double g = __ldg(p.taps + i);
     aa = cadd_rn(aa, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
-    ia += c.step;
+    ia += ca.step;
     ia -= (ia >= n) ? n : 0;
   }
   for (; k < p.omega; k += B) {
-    const double2 v = Sample<Tin>::load(xs, ib);
+    const double2 v = Sample<Tin>::load(xb, ib);
     const double g = __ldg(p.taps + k);
     ab = cadd_rn(ab, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
-    ib += c.step;
+    ib += cb.step;
     ib -= (ib >= n) ? n : 0;
   }
   *o0 = aa;
@@ -194,13 +197,15 @@ __global__ void __launch_bounds__(kNT) k_fused(Prod p, FftPlan P, const double2*
   for (int k = threadIdx.x; k < B; k += kNT) o[k] = cdivr(sm[fft_pos(k, P)], bd);
 }
 
-// Cluster path (B = CL * M, CL in {2,4,8}): the CL CTAs of a thread-block
-// cluster own one item.  CTA p folds slots [pM, pM + M) into its shared
-// memory; the radix-CL first DIF stage reads the CL slot slices over DSMEM
-// (b_q[j] = w_B^{jq} sum_p a_p[j] w_CL^{pq}, q = cluster rank), and each CTA
-// finishes its length-M sub-transform locally: y[q + CL k] = FFT_M(b_q)[k]/B.
-// CL x more CTAs per bucketization than k_fused, so a 77k-sample gather is
-// spread over 8 SMs instead of one.
+// Cluster path (B = CL * M, power of two, CL in {2,4,8}, M in {256, 512,
+// 1024}): the CL CTAs of a thread-block cluster own NI consecutive items (see
+// cluster_items).  CTA q folds slots
+// [qM, qM + M) of every item into shared memory (rows in reference order,
+// fp64, no atomics); the radix-CL first DIF stage reads the CL slot slices
+// over DSMEM (b_q[j] = w_B^{jq} sum_p a_p[j] w_CL^{pq}, q = cluster rank);
+// each CTA then runs the NI length-M sub-transforms with radix-8 register
+// butterflies (twiddles in shared memory, digit reversal by shifts):
+// y[q + CL k] = FFT_M(b_q)[k] / B.  A 77k-sample gather is spread over CL SMs.
 constexpr int kClNT = 256;
 
 // the complex64 flat gather is latency bound: cap registers at 64 so that 4
@@ -210,60 +215,92 @@ constexpr int cluster_min_blocks() {
   return (MODE == PROD_FLAT && sizeof(Tin) == 8) ? 4 : 1;
 }
 
-template <typename Tin, int MODE, int CL>
-__global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>()) k_cluster(Prod p, FftPlan Pm,
-                                                   const double2* __restrict__ W,
-                                                   double2* __restrict__ out) {
+// items per cluster: one for the gathering producers (the 8 measurements of a
+// slot then run in 8 clusters side by side and share their L2 lines), 2048/M
+// (one butterfly per thread and FFT stage) for the gather-free ones
+template <int MODE, int M>
+constexpr int cluster_items() {
+  return (MODE == PROD_FLAT || MODE == PROD_SPIKE) ? 1 : 2048 / M;
+}
+
+template <typename Tin, int MODE, int CL, int M>
+__global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
+    k_cluster(Prod p, int64_t nitems, const double2* __restrict__ W, double2* __restrict__ out) {
+  constexpr int NI = cluster_items<MODE, M>();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ double2 sm[];
+  __shared__ int s_live[NI];
+  __shared__ ItemCtx s_ctx[NI];
   const int q = (int)cl.block_rank();
-  const int item = blockIdx.x / CL;
-  const ItemCtx c = item_ctx<MODE>(p, item, sizeof(Tin));
-  if (c.skip) return;  // uniform over the cluster (same item)
-  if (p.prof_items && threadIdx.x == 0 && q == 0) atomicAdd(p.prof_items, 1ull);
-  const int B = (int)p.B;
-  const int M = B / CL;
-  double2* a = sm;
-  double2* bq = sm + M;
-  if (MODE == PROD_FLAT && c.c == 0 && M % (2 * kClNT) == 0) {
+  const int64_t item0 = (int64_t)(blockIdx.x / CL) * NI;
+  const int B = CL * M;
+  double2* a = sm;               // [NI][M] folded slots of this CTA
+  double2* bq = sm + NI * M;     // [NI][M] sub-transform inputs
+  double2* tw = bq + NI * M;     // [M] w_M^e
+  if (threadIdx.x < NI) {
+    const int64_t it = item0 + threadIdx.x;
+    const bool in = it < nitems;
+    const ItemCtx c = item_ctx<MODE>(p, in ? (int)it : 0, sizeof(Tin));
+    s_ctx[threadIdx.x] = c;
+    s_live[threadIdx.x] = in && !c.skip;
+  }
+  for (int e = threadIdx.x; e < M; e += kClNT) tw[e] = __ldg(W + (int64_t)e * CL);
+  __syncthreads();
+  int nl = 0;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) nl += s_live[i];
+  if (nl == 0) return;  // uniform over the cluster (same items)
+  if (p.prof_items && threadIdx.x == 0 && q == 0) atomicAdd(p.prof_items, (unsigned long long)nl);
+  // ---- fold: every slot of the NI items in turn, item pairs side by side, so
+  // the shifted measurements of one signal re-read their samples from L2
+  if (NI == 1 && MODE == PROD_FLAT && M % (2 * kClNT) == 0 && s_ctx[0].c == 0) {
+    // two slots per call, 8 gathers in flight
+    const ItemCtx c = s_ctx[0];
     for (int j = threadIdx.x; j < M; j += 2 * kClNT)
-      produce_flat2<Tin>(p, c, (int64_t)q * M + j, (int64_t)q * M + j + kClNT, &a[j],
+      produce_flat2<Tin>(p, c, (int64_t)q * M + j, c, (int64_t)q * M + j + kClNT, &a[j],
                          &a[j + kClNT]);
   } else {
-    for (int j = threadIdx.x; j < M; j += kClNT)
-      a[j] = produce<Tin, MODE>(p, c, item, (int64_t)q * M + j);
+    for (int j = threadIdx.x; j < M; j += kClNT) {
+      const int64_t sl = (int64_t)q * M + j;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (s_live[i]) a[i * M + j] = produce<Tin, MODE>(p, s_ctx[i], (int)(item0 + i), sl);
+    }
   }
   cl.sync();
-  const double2* rem[CL];
-#pragma unroll
-  for (int r = 0; r < CL; ++r) rem[r] = cl.map_shared_rank(a, r);
+  // ---- radix-CL stage over DSMEM
   double2 wr[CL];
 #pragma unroll
   for (int r = 0; r < CL; ++r) wr[r] = __ldg(W + ((r * q) % CL) * M);
-  for (int j = threadIdx.x; j < M; j += kClNT) {
-    double2 acc = rem[0][j];
+  for (int t = threadIdx.x; t < NI * M; t += kClNT) {
+    const int j = t & (M - 1);
+    double2 acc = cl.map_shared_rank(a, 0)[t];
 #pragma unroll
-    for (int r = 1; r < CL; ++r) acc = cadd(acc, cmul(rem[r][j], wr[r]));
+    for (int r = 1; r < CL; ++r) acc = cadd(acc, cmul(cl.map_shared_rank(a, r)[t], wr[r]));
     const int e = j * q;
-    bq[j] = e ? cmul(acc, __ldg(W + e)) : acc;
+    bq[t] = e ? cmul(acc, __ldg(W + e)) : acc;
   }
   cl.sync();  // remote reads complete before any CTA of the cluster moves on
-  fft_dif(bq, 1, M, Pm, W, B, threadIdx.x, kClNT);
-  double2* o = out + out_row(p, item) * B + q;
+  // ---- NI sub-transforms of length M
+  fft_pow2<M, NI, kClNT>(bq, tw);
   const double bd = (double)B;
-  for (int k = threadIdx.x; k < M; k += kClNT) o[(int64_t)CL * k] = cdivr(bq[fft_pos(k, Pm)], bd);
+  for (int t = threadIdx.x; t < NI * M; t += kClNT) {
+    const int i = t / M, k = t - i * M;
+    if (!s_live[i]) continue;
+    out[out_row(p, item0 + i) * B + q + (int64_t)CL * k] = cdivr(bq[i * M + pow2_pos<M>(k)], bd);
+  }
 }
 
-template <typename Tin, int MODE, int CL>
-static int launch_cluster(const Prod& p, int64_t nitems, const FftPlan& Pm, const double2* W,
-                          double2* out, cudaStream_t st) {
-  const int M = (int)(p.B / CL);
-  const size_t sm = (size_t)2 * M * sizeof(double2);
-  auto kern = k_cluster<Tin, MODE, CL>;
+template <typename Tin, int MODE, int CL, int M>
+static int launch_cluster_m(const Prod& p, int64_t nitems, const double2* W, double2* out,
+                            cudaStream_t st) {
+  constexpr int NI = cluster_items<MODE, M>();
+  const size_t sm = (size_t)(2 * NI * M + M) * sizeof(double2);
+  auto kern = k_cluster<Tin, MODE, CL, M>;
   SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nitems * CL));
+  cfg.gridDim = dim3((unsigned)(cdiv_up(nitems, NI) * CL));
   cfg.blockDim = dim3(kClNT);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
@@ -274,9 +311,20 @@ static int launch_cluster(const Prod& p, int64_t nitems, const FftPlan& Pm, cons
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, p, Pm, W, out));
+  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, p, nitems, W, out));
   SFFT_CHECK_LAUNCH("k_cluster");
   return 0;
+}
+
+template <typename Tin, int MODE, int CL>
+static int launch_cluster(const Prod& p, int64_t nitems, const double2* W, double2* out,
+                          cudaStream_t st) {
+  const int64_t M = p.B / CL;
+  if (M == 256) return launch_cluster_m<Tin, MODE, CL, 256>(p, nitems, W, out, st);
+  if (M == 512) return launch_cluster_m<Tin, MODE, CL, 512>(p, nitems, W, out, st);
+  if (M == 1024) return launch_cluster_m<Tin, MODE, CL, 1024>(p, nitems, W, out, st);
+  set_error("bucketize: cluster slice must be 256, 512 or 1024 slots");
+  return -2;
 }
 
 // cluster size for B (0: use the one-CTA path)
@@ -475,11 +523,9 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
   FftPlan P;
   const int CL = cluster_size(B);
   if (CL > 1 && !cluster_disabled()) {
-    FftPlan Pm;
-    make_plan(B / CL, &Pm);
-    if (CL == 8) return launch_cluster<Tin, MODE, 8>(p, nitems, Pm, W, out, st);
-    if (CL == 4) return launch_cluster<Tin, MODE, 4>(p, nitems, Pm, W, out, st);
-    return launch_cluster<Tin, MODE, 2>(p, nitems, Pm, W, out, st);
+    if (CL == 8) return launch_cluster<Tin, MODE, 8>(p, nitems, W, out, st);
+    if (CL == 4) return launch_cluster<Tin, MODE, 4>(p, nitems, W, out, st);
+    return launch_cluster<Tin, MODE, 2>(p, nitems, W, out, st);
   }
   if (B <= kFusedMaxB && make_plan(B, &P)) {
     const size_t sm = (size_t)B * sizeof(double2);

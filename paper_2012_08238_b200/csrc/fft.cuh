@@ -129,4 +129,105 @@ __device__ __forceinline__ void fft_dif(double2* s, int G, int seg, const FftPla
   }
 }
 
+// ---------------------------------------------------------------- pow2 FFT
+// Radix-8 register butterflies for power-of-two lengths M = 2^LG (then one
+// radix-2/4 stage when LG % 3 != 0), NI segments of length M at s + i*M,
+// every butterfly of a stage on its own thread.  Twiddles tw[e] = w_M^e
+// (shared memory).  Output k of a segment lands at pow2_pos<M>(k).
+__device__ __forceinline__ void dft4_(double2& x0, double2& x1, double2& x2, double2& x3) {
+  const double2 t0 = cadd(x0, x2), t1 = csub(x0, x2);
+  const double2 t2 = cadd(x1, x3), d = csub(x1, x3);
+  const double2 t3 = cmk(d.y, -d.x);  // (x1 - x3) * (-i)
+  x0 = cadd(t0, t2);
+  x2 = csub(t0, t2);
+  x1 = cadd(t1, t3);
+  x3 = csub(t1, t3);
+}
+
+// X_m = sum_p a_p w8^{pm}, natural order
+__device__ __forceinline__ void dft8_(double2* a) {
+  constexpr double r = 0.70710678118654752440;
+  double2 b[4], c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    b[k] = cadd(a[k], a[k + 4]);
+    c[k] = csub(a[k], a[k + 4]);
+  }
+  c[1] = cmk(r * (c[1].x + c[1].y), r * (c[1].y - c[1].x));   // * w8
+  c[2] = cmk(c[2].y, -c[2].x);                                // * w8^2 = -i
+  c[3] = cmk(r * (c[3].y - c[3].x), -r * (c[3].x + c[3].y));  // * w8^3
+  dft4_(b[0], b[1], b[2], b[3]);
+  dft4_(c[0], c[1], c[2], c[3]);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    a[2 * m] = b[m];
+    a[2 * m + 1] = c[m];
+  }
+}
+
+template <int M>
+struct Pow2 {
+  static constexpr int LG = (M >= 2) ? 1 + Pow2<M / 2>::LG : 0;
+  static constexpr int N8 = LG / 3;
+  static constexpr int RL = 1 << (LG - 3 * N8);  // last radix 1, 2 or 4
+};
+template <>
+struct Pow2<1> {
+  static constexpr int LG = 0, N8 = 0, RL = 1;
+};
+
+template <int M>
+__device__ __forceinline__ int pow2_pos(int k) {
+  // digit reversal of the DIF stages (8, ..., 8, RL)
+  int pos = 0, span = M;
+#pragma unroll
+  for (int st = 0; st < Pow2<M>::N8; ++st) {
+    span >>= 3;
+    pos += (k & 7) * span;
+    k >>= 3;
+  }
+  if (Pow2<M>::RL > 1) pos += k;  // span == RL, digit k < RL, weight 1
+  return pos;
+}
+
+template <int M, int NI, int NT>
+__device__ __forceinline__ void fft_pow2(double2* __restrict__ s, const double2* __restrict__ tw) {
+  int Mb = M;
+#pragma unroll 1
+  for (int st = 0; st < Pow2<M>::N8; ++st) {
+    const int Mp = Mb >> 3;
+    const int tstr = M / Mb;
+#pragma unroll 1
+    for (int t = threadIdx.x; t < NI * (M / 8); t += NT) {
+      const int seg = t / (M / 8), tt = t - seg * (M / 8);
+      const int blk = tt / Mp, j = tt - blk * Mp;
+      double2* x = s + seg * M + blk * Mb + j;
+      double2 a[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) a[p] = x[p * Mp];
+      dft8_(a);
+      x[0] = a[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) x[q * Mp] = j ? cmul(a[q], tw[j * q * tstr]) : a[q];
+    }
+    __syncthreads();
+    Mb = Mp;
+  }
+  if (Pow2<M>::RL == 4) {
+    for (int t = threadIdx.x; t < NI * (M / 4); t += NT) {
+      double2* x = s + 4 * t;
+      dft4_(x[0], x[1], x[2], x[3]);
+    }
+    __syncthreads();
+  } else if (Pow2<M>::RL == 2) {
+    for (int t = threadIdx.x; t < NI * (M / 2); t += NT) {
+      double2* x = s + 2 * t;
+      const double2 u = x[0], v = x[1];
+      x[0] = cadd(u, v);
+      x[1] = csub(u, v);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace sfft
