@@ -269,19 +269,31 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
     }
   }
   cl.sync();
-  // ---- radix-CL stage over DSMEM
-  double2 wr[CL];
+  // ---- radix-CL stage over DSMEM: CTA q takes slots j in [q M/CL, (q+1) M/CL)
+  // of every CTA, forms the CL-point DFT over the CTAs and scatters output
+  // q' (times w_B^{j q'}) to CTA q' -- every folded value crosses the cluster
+  // once
+  constexpr int NJ = M / CL;
+  for (int t = threadIdx.x; t < NI * NJ; t += kClNT) {
+    const int i = t / NJ;
+    const int j = q * NJ + (t - i * NJ);
+    double2 v[8];
 #pragma unroll
-  for (int r = 0; r < CL; ++r) wr[r] = __ldg(W + ((r * q) % CL) * M);
-  for (int t = threadIdx.x; t < NI * M; t += kClNT) {
-    const int j = t & (M - 1);
-    double2 acc = cl.map_shared_rank(a, 0)[t];
+    for (int r = 0; r < CL; ++r) v[r] = cl.map_shared_rank(a, r)[i * M + j];
+    if (CL == 8) {
+      dft8_(v);
+    } else if (CL == 4) {
+      dft4_(v[0], v[1], v[2], v[3]);
+    } else {
+      const double2 u = v[0];
+      v[0] = cadd(u, v[1]);
+      v[1] = csub(u, v[1]);
+    }
 #pragma unroll
-    for (int r = 1; r < CL; ++r) acc = cadd(acc, cmul(cl.map_shared_rank(a, r)[t], wr[r]));
-    const int e = j * q;
-    bq[t] = e ? cmul(acc, __ldg(W + e)) : acc;
+    for (int r = 0; r < CL; ++r)
+      cl.map_shared_rank(bq, r)[i * M + j] = (j * r) ? cmul(v[r], __ldg(W + j * r)) : v[r];
   }
-  cl.sync();  // remote reads complete before any CTA of the cluster moves on
+  cl.sync();  // all slices scattered (and all remote reads of a done)
   // ---- NI sub-transforms of length M
   fft_pow2<M, NI, kClNT>(bq, tw);
   const double bd = (double)B;
