@@ -625,14 +625,18 @@ __device__ __forceinline__ int sub_splits(int64_t T, int maxTS) {
   return (int)(z < 1 ? 1 : (z > maxTS ? maxTS : z));
 }
 
+template <bool REAL>
 __global__ void __launch_bounds__(kSubNT) k_subtract(
     const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
     const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
     const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
-    const int32_t* tcount, int64_t tstride, const int32_t* gate, double2* __restrict__ part) {
+    const int32_t* tcount, int64_t tstride, const int32_t* gate, double2* __restrict__ part,
+    RealTab rt) {
   __shared__ int32_t s_row[kSubChunk];
   __shared__ int32_t s_q[kSubChunk];
-  __shared__ double2 s_a[kSubChunk];
+  __shared__ double2 s_a[kSubChunk];     // complex: c w^{tau m}; real: beta = c w^{tau m} w^{-m h} / B
+  __shared__ double2 s_al[kSubChunk];    // real: alpha = c w^{tau m} t0 / B
+  __shared__ double2 s_alsum;
   const int item = blockIdx.y;
   const int sig = item_sig ? item_sig[item] : item;
   if (gate && !gate[sig]) return;
@@ -660,18 +664,76 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
     const int64_t i = i0 + u;
     live[u] = i < nb;
     bk[u] = live[u] ? (int)(blist ? blist[(int64_t)item * nb + i] : i) : 0;
-    acc[u] = (live[u] && TS == 1) ? y[(int64_t)item * B + bk[u]] : cmk(0.0, 0.0);
+    acc[u] = (live[u] && TS == 1 && !REAL) ? y[(int64_t)item * B + bk[u]] : cmk(0.0, 0.0);
   }
   const int Bi = (int)B;
+  const double t0v = REAL ? rt.taps[0] : 0.0;
+  const double invB = 1.0 / (double)B;
+  if (REAL && threadIdx.x == 0) s_alsum = cmk(0.0, 0.0);
   for (int64_t t0 = 0; t0 < T; t0 += kSubChunk) {
     __syncthreads();
     for (int j = threadIdx.x; j < kSubChunk && t0 + j < T; j += kSubNT) {
       const int64_t m = mulmod(sg, pmod(tp[t0 + j], n), n);
       s_row[j] = (int)((L - m % L) % L);
       s_q[j] = (int)((m + L - 1) / L);
-      s_a[j] = cmul(tc[t0 + j], unit_root(n, mulmod(tt, m, n)));
+      const double2 cp = cmul(tc[t0 + j], unit_root(n, mulmod(tt, m, n)));
+      if (REAL) {
+        s_a[j] = cscale(cmul(cp, unit_root(n, pmod(-mulmod(m, rt.h % n, n), n))), invB);
+        s_al[j] = cscale(cp, t0v * invB);
+      } else {
+        s_a[j] = cp;
+      }
     }
     __syncthreads();
+    if (REAL && threadIdx.x < 32) {
+      // alpha is bucket-independent: one warp sums the chunk
+      const int tn = (int)((T - t0 < kSubChunk) ? (T - t0) : kSubChunk);
+      double2 z = cmk(0.0, 0.0);
+      for (int j = threadIdx.x; j < tn; j += 32) z = cadd(z, s_al[j]);
+      for (int o = 16; o; o >>= 1) {
+        z.x += __shfl_xor_sync(0xffffffffu, z.x, o);
+        z.y += __shfl_xor_sync(0xffffffffu, z.y, o);
+      }
+      if (threadIdx.x == 0) s_alsum = cadd(s_alsum, z);
+    }
+    if (REAL) {
+      if (live[0]) {
+        const int tn = (int)((T - t0 < kSubChunk) ? (T - t0) : kSubChunk);
+        int j = 0;
+        for (; j + 8 <= tn; j += 8) {
+          double w[8][kSubBPT];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const double* row = rt.at + (int64_t)s_row[j + v] * B;
+#pragma unroll
+            for (int u = 0; u < kSubBPT; ++u) {
+              int col = bk[u] - s_q[j + v];
+              col += (col < 0) ? Bi : 0;
+              w[v][u] = __ldg(row + col);
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+#pragma unroll
+            for (int u = 0; u < kSubBPT; ++u) {
+              acc[u].x = fma(s_a[j + v].x, w[v][u], acc[u].x);
+              acc[u].y = fma(s_a[j + v].y, w[v][u], acc[u].y);
+            }
+        }
+        for (; j < tn; ++j) {
+          const double* row = rt.at + (int64_t)s_row[j] * B;
+#pragma unroll
+          for (int u = 0; u < kSubBPT; ++u) {
+            int col = bk[u] - s_q[j];
+            col += (col < 0) ? Bi : 0;
+            const double w = __ldg(row + col);
+            acc[u].x = fma(s_a[j].x, w, acc[u].x);
+            acc[u].y = fma(s_a[j].y, w, acc[u].y);
+          }
+        }
+      }
+      continue;
+    }
     if (live[0]) {
       const int tn = (int)((T - t0 < kSubChunk) ? (T - t0) : kSubChunk);
       // 4 tones x 2 buckets of table reads in flight, then the ordered updates
@@ -704,6 +766,18 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
       }
     }
   }
+  if (REAL) {
+    // model = alpha_total + w^{b L h} S_b; running value y - model
+    __syncthreads();
+    const double2 al = s_alsum;
+#pragma unroll
+    for (int u = 0; u < kSubBPT; ++u) {
+      if (!live[u]) continue;
+      const double2 pb = unit_root(n, mulmod(mulmod(bk[u], L, n), rt.h % n, n));
+      const double2 model = cadd(al, cmul(pb, acc[u]));
+      acc[u] = TS == 1 ? csub(y[(int64_t)item * B + bk[u]], model) : cmk(-model.x, -model.y);
+    }
+  }
 #pragma unroll
   for (int u = 0; u < kSubBPT; ++u) {
     if (!live[u]) continue;
@@ -731,17 +805,50 @@ __global__ void k_sub_reduce(const double2* __restrict__ y, double2* __restrict_
   out[(int64_t)item * nb + i] = cadd(y[(int64_t)item * B + bk], acc);
 }
 
+// A_f = Re((B G_f - t0) w^{-f h}) in the transposed layout (f = rho + j L at
+// rho * B + j); the imaginary part is rounding noise for a symmetric window.
+__global__ void k_real_table(const double2* __restrict__ gt, const double* __restrict__ taps,
+                             int64_t n, int64_t B, int64_t h, double* __restrict__ at) {
+  const int64_t L = n / B;
+  const double t0 = taps[0];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rho = e / B, j = e - rho * B;
+    const int64_t f = rho + j * L;
+    const double2 g = gt[e];
+    const double2 w = unit_root(n, pmod(-mulmod(f, h % n, n), n));
+    at[e] = (g.x * (double)B - t0) * w.x - (g.y * (double)B) * w.y;
+  }
+}
+
+bool real_table_ok(int64_t omega) { return omega >= 2 && omega % 2 == 0 && !getenv("SFFT_NO_REAL_TABLE"); }
+
+int build_real_table(const double2* gt, const double* taps, int64_t n, int64_t B, int64_t omega,
+                     double* at, cudaStream_t st) {
+  k_real_table<<<(unsigned)std::min<int64_t>(4096, cdiv_up(n, 256)), 256, 0, st>>>(gt, taps, n, B,
+                                                                                 omega / 2, at);
+  SFFT_CHECK_LAUNCH("k_real_table");
+  return 0;
+}
+
 int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        const int32_t* blist, int64_t nitems, const double2* gt, int64_t n,
                        const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
                        const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
                        int64_t tstride, const int32_t* gate, cudaStream_t st, int TS,
-                       double2* part) {
+                       double2* part, const RealTab* rt) {
   if (nitems <= 0 || nb <= 0) return 0;
   if (TS < 1 || !part) TS = 1;
   dim3 g((unsigned)cdiv_up(nb, (int64_t)kSubNT * kSubBPT), (unsigned)nitems, (unsigned)TS);
-  k_subtract<<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma, tau_tot, tpos,
-                                   tcoef, tcount, tstride, gate, part);
+  if (rt && rt->at) {
+    k_subtract<true><<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma,
+                                           tau_tot, tpos, tcoef, tcount, tstride, gate, part,
+                                           *rt);
+  } else {
+    k_subtract<false><<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma,
+                                            tau_tot, tpos, tcoef, tcount, tstride, gate, part,
+                                            RealTab{});
+  }
   SFFT_CHECK_LAUNCH("k_subtract");
   if (TS > 1) {
     dim3 g2((unsigned)cdiv_up(nb, 256), (unsigned)nitems);

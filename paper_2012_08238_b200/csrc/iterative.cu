@@ -67,6 +67,7 @@ struct IterArgs {
   int32_t* item_active;          // [S*M] items of the per-item flat bucketization
   int32_t* item_fold;            // [S*M] split loop items d*B of the row-correlation path
   int use_fold;                  // split location folds its loop shifts d*B as a row correlation
+  RealTab rt;                    // real form of the response table (rt.at null: complex)
   int32_t* pgate;                // [S] polish pass this round
   int64_t ladder[kMaxShifts];    // d_1..d_{M-1} (phase location)
   const int64_t* shifts;         // [M] shift of loop item j (device)
@@ -1191,6 +1192,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int64_t) * (size_t)M,           // 34 loop shift of each item
       sizeof(int32_t) * (size_t)S * B * 3,   // 35 split search r / ok / depth
       sizeof(int32_t) * (size_t)S * M,       // 36 item_fold
+      sizeof(double) * (size_t)n,            // 37 real response table
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   for (int i = 0; i < cnt; ++i) {
@@ -1365,6 +1367,15 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.sp_ok = a.sp_r + (size_t)S * B;
   a.sp_depth = a.sp_ok + (size_t)S * B;
   a.item_fold = (int32_t*)(w + Lo.off[36]);
+  RealTab rt{};
+  if (real_table_ok(omega)) {
+    rt.at = (const double*)(w + Lo.off[37]);
+    rt.taps = taps;
+    rt.h = omega / 2;
+    int rc0 = build_real_table(gt, taps, n, B, omega, (double*)(w + Lo.off[37]), st);
+    if (rc0) return rc0;
+  }
+  a.rt = rt;
   void* bws = w + Lo.total;
   {
     // loop shifts: phase {0} + ladder; split {d*B : d < L} + {1, 3}
@@ -1455,7 +1466,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     // ---- loop slots
     rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st,
-                            splits(t_max, 128, kMaxSubSplit), a.part);
+                            splits(t_max, 128, kMaxSubSplit), a.part, &rt);
     if (rc) return rc;
     k_it_decide<<<S, kDecNT, dsm, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_decide");
@@ -1478,7 +1489,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CHECK_LAUNCH("k_it_merge");
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
-                            splits(h_max, 128, kMaxSubSplit), a.part);
+                            splits(h_max, 128, kMaxSubSplit), a.part, &rt);
     if (rc) return rc;
     k_it_resid<<<S, kDecNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_resid");

@@ -96,12 +96,25 @@ int run_subtract(const double2* y, double2* out, int64_t B, int64_t nb, const in
                  const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos,
                  const double2* tcoef, const int32_t* tcount, int64_t tstride, cudaStream_t st);
 
+// Real-table form of the flat response (even support Omega, taps symmetric
+// about h = Omega/2): G_f = (t0 + w^{f h} A_f) / B with A real, so a tone's
+// model at bucket b is (c ph)(t0/B) + w^{b L h} [(c ph w^{-m h} / B) A_{bL-m}]:
+// half the table bytes and half the multiplies of the complex form.
+struct RealTab {
+  const double* at;   // [L][B] A in the transposed layout of the complex table
+  const double* taps; // taps[0] = t0
+  int64_t h;          // Omega / 2
+};
+int build_real_table(const double2* gt, const double* taps, int64_t n, int64_t B, int64_t omega,
+                     double* at, cudaStream_t st);
+bool real_table_ok(int64_t omega);
+
 int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        const int32_t* blist, int64_t nitems, const double2* gt, int64_t n,
                        const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
                        const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
                        int64_t tstride, const int32_t* gate, cudaStream_t st, int TS = 1,
-                       double2* part = nullptr);
+                       double2* part = nullptr, const RealTab* rt = nullptr);
 
 // voting.cu
 size_t voting_ws_bytes(int64_t n, int64_t B, int S, int R, int C, int64_t Bpre);
