@@ -428,6 +428,85 @@ __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bo
   }
 }
 
+// Real-table form of ladder_model (RealTab): per tone and shift
+// beta_tj = c w^{(tau+d_j) m} w^{-m h} / B and alpha_tj = c w^{(tau+d_j) m} t0 / B;
+// ys[j] -= sum_t alpha_tj + w^{b L h} sum_t beta_tj A_{bL-m}.  The alpha sums
+// do not depend on the bucket: thread j of the block forms them (in tone order).
+template <int M>
+__device__ __forceinline__ void ladder_model_real(const IterArgs& a, int s, int b, bool live,
+                                                  int64_t tb, int64_t te, double2* ys,
+                                                  int64_t* t_row, int64_t* t_q,
+                                                  double2 (*t_be)[kMaxShifts],
+                                                  double2 (*t_al)[kMaxShifts], double2* s_al) {
+  const int64_t n = a.n, B = a.B, L = a.L;
+  const int64_t sigma = a.item_sigma[s];
+  const int64_t tau = a.item_tau[s];
+  const int64_t* rp = a.rec_pos + (int64_t)s * a.cap;
+  const double2* rc = a.rec_coef + (int64_t)s * a.cap;
+  const double t0v = a.rt.taps[0];
+  const double invB = 1.0 / (double)B;
+  const int64_t hh = a.rt.h % n;
+  double2 S[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) S[j] = cmk(0.0, 0.0);
+  if (threadIdx.x < M) s_al[threadIdx.x] = cmk(0.0, 0.0);
+  for (int64_t t0 = tb; t0 < te; t0 += kLocChunk) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < kLocChunk * M; q += kLocNT) {
+      const int tt = q / M, j = q - tt * M;
+      if (t0 + tt >= te || j == 0) continue;
+      const int64_t m = mulmod(sigma, pmod(rp[t0 + tt], n), n);
+      const int64_t tj = pmod(tau + a.ladder[j - 1], n);
+      const double2 cp = cmul(rc[t0 + tt], unit_root(n, mulmod(tj, m, n)));
+      t_be[tt][j] = cscale(cmul(cp, unit_root(n, pmod(-mulmod(m, hh, n), n))), invB);
+      t_al[tt][j] = cscale(cp, t0v * invB);
+      if (j == 1) {
+        t_row[tt] = (L - m % L) % L;
+        t_q[tt] = (m + L - 1) / L;
+      }
+    }
+    __syncthreads();
+    const int tn = (int)((te - t0 < kLocChunk) ? te - t0 : kLocChunk);
+    if (threadIdx.x > 0 && threadIdx.x < M)
+      for (int tt = 0; tt < tn; ++tt) s_al[threadIdx.x] = cadd(s_al[threadIdx.x], t_al[tt][threadIdx.x]);
+    if (live) {
+      int tt = 0;
+      for (; tt + 4 <= tn; tt += 4) {
+        double w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int64_t col = b - t_q[tt + u];
+          col += (col < 0) ? B : 0;
+          w[u] = __ldg(a.rt.at + t_row[tt + u] * B + col);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 1; j < M; ++j) {
+            S[j].x = fma(t_be[tt + u][j].x, w[u], S[j].x);
+            S[j].y = fma(t_be[tt + u][j].y, w[u], S[j].y);
+          }
+      }
+      for (; tt < tn; ++tt) {
+        int64_t col = b - t_q[tt];
+        col += (col < 0) ? B : 0;
+        const double w = __ldg(a.rt.at + t_row[tt] * B + col);
+#pragma unroll
+        for (int j = 1; j < M; ++j) {
+          S[j].x = fma(t_be[tt][j].x, w, S[j].x);
+          S[j].y = fma(t_be[tt][j].y, w, S[j].y);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (live && te > tb) {
+    const double2 pb = unit_root(n, mulmod(mulmod(b, L, n), hh, n));
+#pragma unroll
+    for (int j = 1; j < M; ++j) ys[j] = csub(ys[j], cadd(s_al[j], cmul(pb, S[j])));
+  }
+}
+
 constexpr int kLadPerSplit = 256;  // tones per split
 
 // splits of a slot's ladder model (0: small list, subtracted inline)
@@ -444,6 +523,8 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
   __shared__ double2 t_ph[kLocChunk][kMaxShifts];
+  __shared__ double2 t_al[kLocChunk][kMaxShifts];
+  __shared__ double2 s_al[kMaxShifts];
   const int s = blockIdx.y;
   if (!a.active[s]) return;
   const int nh = a.st[s].nheavy;
@@ -461,7 +542,10 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   double2 ys[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) ys[j] = cmk(0.0, 0.0);
-  ladder_model<M>(a, s, b, live, tb, te, ys, t_row, t_q, t_c, t_ph);
+  if (a.rt.at)
+    ladder_model_real<M>(a, s, b, live, tb, te, ys, t_row, t_q, t_ph, t_al, s_al);
+  else
+    ladder_model<M>(a, s, b, live, tb, te, ys, t_row, t_q, t_c, t_ph);
   if (!live) return;
   double2* o = a.part + (((int64_t)s * gridDim.z + blockIdx.z) * a.B + h) * (M - 1);
 #pragma unroll
@@ -477,6 +561,8 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
   __shared__ double2 t_ph[kLocChunk][kMaxShifts];
+  __shared__ double2 t_al[kLocChunk][kMaxShifts];
+  __shared__ double2 s_al[kMaxShifts];
   const int s = blockIdx.y;
   if (!a.active[s]) return;
   const IterState& S = a.st[s];
@@ -496,7 +582,10 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   for (int j = 0; j < M; ++j) ys[j] = a.y[((int64_t)j * a.S + s) * B + b];
   const int TS = lad_splits(a.rec_count[s], maxTS);
   if (TS == 0) {
-    ladder_model<M>(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_c, t_ph);
+    if (a.rt.at)
+      ladder_model_real<M>(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_ph, t_al, s_al);
+    else
+      ladder_model<M>(a, s, b, live, 0, a.rec_count[s], ys, t_row, t_q, t_c, t_ph);
   } else if (live) {
     for (int z = 0; z < TS; ++z) {
       const double2* p = a.part + (((int64_t)s * maxTS + z) * B + h) * (M - 1);
