@@ -271,7 +271,7 @@ def main():
     achieved = (pi.value * item_bytes) / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
     peak, peak_kind = peaks()
     # DRAM traffic of the same kernel from the committed ncu --set full capture
-    # (profiles/r1_k_cluster_ncu_raw.json: first C3 loop round, 1024 items)
+    # (profiles/r1_k_cluster_ncu_raw.json: first C3 loop round, "items" bucketizations)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r1_k_cluster_ncu_raw.json")) as f:
@@ -279,7 +279,7 @@ def main():
         unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
         rd = float(raw["dram__bytes_read.sum"][0]) * unit[raw["dram__bytes_read.sum"][1]]
         wr = float(raw["dram__bytes_write.sum"][0]) * unit[raw["dram__bytes_write.sum"][1]]
-        traffic = (rd + wr) / 1024.0  # per item, like bytes_per_item
+        traffic = (rd + wr) / float(raw.get("items", 1024))  # per item, like bytes_per_item
     except Exception:
         traffic = None
 
@@ -333,7 +333,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": traffic, "traffic_unit": "DRAM bytes per item (ncu)",
-                         "kernel": "k_cluster<float2,FLAT,8> (gather+window+fold, DSMEM radix-8 stage, FFT_512)",
+                         "kernel": "k_cluster<float2,FLAT,8,512> (gather+window+fold, DSMEM radix-8 exchange, radix-8 FFT_512)",
                          "bytes_per_item": item_bytes, "items": pi.value,
                          "launches": pl.value, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / ms if ms else None},
