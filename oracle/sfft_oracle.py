@@ -158,6 +158,76 @@ def spike_buckets(acc: Access, b: int, tau: int = 0) -> np.ndarray:
     return np.fft.fft(acc.read((step * np.arange(b, dtype=np.int64) - tau) % n)) / b
 
 
+# ---------------------------------------------------------------- Dirichlet bank
+
+@dataclass(frozen=True)
+class DirichletBank:
+    """make_dirichlet_bank (sfft/filters.py:168-187) [+ filter_freq_shift :190-200]."""
+    n: int
+    width: int            # L
+    b: int
+    half: bool
+    taps: np.ndarray      # complex128[L]
+    response: np.ndarray  # complex128[n], unnormalised transform of the padded taps
+    center: int = 0       # center_offset
+
+
+def dirichlet_bank(n: int, width: int, b: int, half: bool = True) -> DirichletBank:
+    if width * b != n:
+        raise OracleError("NonDivisorParameter", f"{width}*{b} != n={n}")
+    taps = np.full(width, math.sqrt(n) / width, dtype=np.complex128)
+    pad = np.zeros(n, dtype=np.complex128)
+    pad[:width] = taps
+    return DirichletBank(n, width, b, half, taps, np.fft.fft(pad))
+
+
+def dirichlet_shift(bank: DirichletBank, f0: int) -> DirichletBank:
+    """filter_freq_shift for a Dirichlet bank: taps *= w^{-f0 pos}, response
+    recomputed unnormalised, center_offset += f0 (sfft/filters.py:190-200)."""
+    pos = np.arange(bank.width, dtype=np.int64)
+    taps = bank.taps * unit_root(bank.n, -f0 * pos)
+    pad = np.zeros(bank.n, dtype=np.complex128)
+    pad[pos] = taps
+    return DirichletBank(bank.n, bank.width, bank.b, bank.half, taps, np.fft.fft(pad),
+                         (bank.center + f0) % bank.n)
+
+
+def dirichlet_buckets(acc: Access, bank: DirichletBank, offsets) -> np.ndarray:
+    """Box windows at each sample offset t: L consecutive samples x[t - i],
+    fold mod B, B * inverse transform, de-rotate by w^{-c t} at each bucket
+    center, average over offsets (sfft/bucketize.py:181-211)."""
+    n, b, L = acc.n, bank.b, bank.width
+    offsets = tuple(int(t) for t in offsets)
+    if not offsets:
+        raise OracleError("NonDivisorParameter", "at least one sample offset is required")
+    base = 0 if bank.half else L // 2
+    centers = (L * np.arange(b, dtype=np.int64) + base + bank.center) % n
+    pos = np.arange(L, dtype=np.int64)
+    half_mod = unit_root(n, -(L // 2) * pos) if not bank.half else np.ones(L, dtype=np.complex128)
+    total = np.zeros(b, dtype=np.complex128)
+    for t in offsets:
+        win = bank.taps * acc.read((t - pos) % n) * half_mod
+        pad = (-win.size) % b
+        z = np.concatenate([win, np.zeros(pad, dtype=win.dtype)]) if pad else win
+        v = b * np.fft.ifft(z.reshape(-1, b).sum(axis=0))
+        total += v * unit_root(n, centers * t)
+    return total / len(offsets)
+
+
+def freqshift_estimate(acc: Access, f: int, t: int, seed=0) -> complex:
+    """Mean of x[i] w^{f i} over t random (or all N) positions
+    (sfft/reconstruct.py:356-371)."""
+    if t < 1:
+        raise OracleError("InvalidParameter", f"t={t} must be >= 1")
+    n = acc.n
+    if t >= n:
+        idx = np.arange(n, dtype=np.int64)
+    else:
+        rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+        idx = rng.integers(0, n, size=t)
+    return complex(np.mean(acc.read(idx) * unit_root(n, f * idx)))
+
+
 # ---------------------------------------------------------------- decode
 
 def noise_floor(values, mult: float = 3.0) -> float:

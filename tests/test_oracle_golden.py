@@ -145,3 +145,40 @@ def test_split_search_unit():
         assert O.split_search(sub_for({off: 1 + 0.5j}), 0, 16, 2, 1e-12) == off
     with pytest.raises(O.Ambiguous):
         O.split_search(sub_for({}), 0, 8, 2, 1e-12)
+
+
+def test_dirichlet_golden():
+    """Dirichlet-bank bucketization and freq-shift estimates
+    (sfft/bucketize.py:181-211, sfft/reconstruct.py:356-371) pinned bit-exactly."""
+    import json
+    z = load_golden("stage_dirichlet")
+    off = 0
+    yo = 0
+    for i, (n, L, b, half, f0, no, cshift) in enumerate(z["meta"]):
+        x = stage_signal(20240904 + i, int(n))
+        np.testing.assert_array_equal(sig_checksum(x), z["checksum"][i])
+        bank = O.dirichlet_bank(int(n), int(L), int(b), bool(half))
+        if f0:
+            bank = O.dirichlet_shift(bank, int(f0))
+        assert bank.center == cshift
+        acc = O.Access(x)
+        y = O.dirichlet_buckets(acc, bank, z["offsets"][off:off + no])
+        np.testing.assert_array_equal(y, z["y"][yo:yo + b])
+        assert acc.count() == z["access"][i]
+        off += no
+        yo += b
+    for j, (n, f, t, seed) in enumerate(z["est_specs"]):
+        acc = O.Access(stage_signal(20240950 + j, int(n)))
+        assert O.freqshift_estimate(acc, int(f), int(t), int(seed)) == z["est"][j]
+        assert acc.count() == z["est_access"][j]
+    errs = json.loads(str(z["errors"]))
+    x = stage_signal(1, 2048)
+    with pytest.raises(O.OracleError) as e:
+        O.dirichlet_buckets(O.Access(x), O.dirichlet_bank(2048, 128, 16), ())
+    assert e.value.kind == errs["nooffset"]
+    with pytest.raises(O.OracleError) as e:
+        O.dirichlet_bank(2048, 100, 16)
+    assert e.value.kind == errs["bank"]
+    with pytest.raises(O.OracleError) as e:
+        O.freqshift_estimate(O.Access(x), 3, 0)
+    assert e.value.kind == errs["t0"]
