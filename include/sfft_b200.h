@@ -149,6 +149,29 @@ int sfft_subtract_flat(const void* y, void* out, int64_t B, int64_t nb, const in
 
 /* ---- runners (device-resident frameworks) ---------------------------------- */
 
+/* ---- Dirichlet bank and freq-shift estimate -------------- */
+
+/* Workspace bytes of sfft_dirichlet_bucketize for B buckets and noffsets offsets. */
+size_t sfft_dirichlet_ws_bytes(int64_t B, int64_t noffsets);
+
+/* bucketize_dirichlet (sfft/bucketize.py:181-211) for a bank of B boxes of
+ * width L (L*B == n, make_dirichlet_bank sfft/filters.py:168-187, possibly
+ * freq-shifted by filter_freq_shift :190-200): taps complex128[L];
+ * half_offset / center_offset as WindowFilter; offsets device int64[noffsets]
+ * (the sample offsets, any integers).  out complex128[B] = the averaged,
+ * de-rotated bucket values.  Reads L samples per offset. */
+int sfft_dirichlet_bucketize(int dtype, const void* x, int64_t n, const void* taps, int64_t L,
+                             int64_t B, int32_t half_offset, int64_t center_offset,
+                             int64_t noffsets, const int64_t* offsets, const void* W, void* out,
+                             void* ws, size_t ws_bytes, void* stream);
+
+/* estimate_freqshift (sfft/reconstruct.py:356-371): out = mean over the count
+ * positions idx (device int64, drawn by the caller exactly as the reference
+ * draws them) of x[i] * w^{f i}.  ws >= 4096 bytes. */
+int sfft_freqshift_estimate(int dtype, const void* x, int64_t n, const int64_t* idx,
+                            int64_t count, int64_t f, void* out, void* ws, size_t ws_bytes,
+                            void* stream);
+
 /* Workspace bytes of sfft_run_iterative for nslots slots (nshifts = 1 +
  * ladder length for phase location, n/B + 2 for split location; cap =
  * recovered-tone capacity per slot, max_iterations * B suffices). */

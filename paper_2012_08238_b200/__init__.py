@@ -13,12 +13,14 @@ from .errors import (AmbiguousSplit, ConfigMismatch, FilterKindMismatch, Invalid
                      SparseFFTError, ZeroTonBucket)
 from .signal import PermutationParams, SparseSpectrum, TimeSignal, phase_factor
 from .filters import (WindowFilter, default_flat_support, default_gauss_sigma,
-                      make_flat_filter)
-from .bucketize import (BucketSet, HashMapView, bucketize_flat, bucketize_flat_batch,
-                        bucketize_spike, bucketize_spike_batch, hash_view, hash_view_for)
+                      filter_freq_shift, make_dirichlet_bank, make_flat_filter)
+from .bucketize import (BucketSet, HashMapView, bucketize_dirichlet, bucketize_flat,
+                        bucketize_flat_batch, bucketize_spike, bucketize_spike_batch, hash_view,
+                        hash_view_for)
 
 __version__ = "0.1.0"
-from .reconstruct import VoteTable, robust_noise_floor, select_by_votes, vote_tally
+from .reconstruct import (VoteTable, estimate_freqshift, robust_noise_floor, select_by_votes,
+                          vote_tally)
 from .frameworks import (FRAMEWORKS, AlgorithmConfig, BatchResult, RecoveryResult,
                          run_algorithm, run_iterative, run_iterative_batch,
                          run_iterative_stream, run_peeling,

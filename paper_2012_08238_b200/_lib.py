@@ -111,6 +111,10 @@ SIGNATURES.update({
                                      i64, P_i64,
                                      vp, P_i32, P_i32, P_i32, P_i64, P_i64, P_i32, vp, sz, vp]),
     "sfft_schedule_layout": (C.c_int, [vp, vp]),
+    "sfft_dirichlet_ws_bytes": (sz, [i64, i64]),
+    "sfft_dirichlet_bucketize": (C.c_int, [C.c_int, vp, i64, vp, i64, i64, i32, i64, i64, P_i64,
+                                           vp, vp, vp, sz, vp]),
+    "sfft_freqshift_estimate": (C.c_int, [C.c_int, vp, i64, P_i64, i64, i64, vp, vp, sz, vp]),
 })
 SIGNATURES.update({
     "sfft_launch_count": (i64, []),

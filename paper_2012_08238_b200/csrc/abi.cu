@@ -147,6 +147,54 @@ SFFT_API int sfft_spike_bucketize(int dtype, const void* x, int64_t n, int64_t x
                        ws_bytes, (cudaStream_t)stream);
 }
 
+// Dirichlet bank bucketization (sfft/bucketize.py:181-211).
+SFFT_API size_t sfft_dirichlet_ws_bytes(int64_t B, int64_t noffsets) {
+  return (size_t)noffsets * (size_t)B * sizeof(double2) + bucketize_ws_bytes(B, noffsets) + 256;
+}
+
+SFFT_API int sfft_dirichlet_bucketize(int dtype, const void* x, int64_t n, const void* taps,
+                                      int64_t L, int64_t B, int32_t half_offset,
+                                      int64_t center_offset, int64_t noffsets,
+                                      const int64_t* offsets, const void* W, void* out, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_dirichlet_bucketize: dtype must be 0 or 1");
+  SFFT_REQUIRE(x && taps && offsets && W && out && ws, "sfft_dirichlet_bucketize: null pointer");
+  SFFT_REQUIRE(n > 0 && B > 0 && L > 0 && L * B == n && noffsets >= 1,
+               "sfft_dirichlet_bucketize: need L*B == n and at least one offset");
+  SFFT_REQUIRE(n < (int64_t(1) << 31), "sfft_dirichlet_bucketize: n must be < 2^31");
+  SFFT_REQUIRE(ws_bytes >= sfft_dirichlet_ws_bytes(B, noffsets),
+               "sfft_dirichlet_bucketize: workspace too small");
+  double2* y = (double2*)ws;
+  char* bws = (char*)ws + (((size_t)noffsets * B * sizeof(double2) + 255) & ~size_t(255));
+  Prod p{};
+  p.x = x;
+  p.xstride = 0;  // every item (offset) reads the one signal
+  p.n = n;
+  p.B = B;
+  p.omega = L;
+  p.ctaps = (const double2*)taps;
+  p.half_offset = half_offset ? 1 : 0;
+  p.item_a = offsets;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = run_bucketize(dtype, PROD_DIRICHLET, p, noffsets, (const double2*)W, y, bws,
+                         bucketize_ws_bytes(B, noffsets), st);
+  if (rc) return rc;
+  return run_dirichlet_combine(y, noffsets, offsets, n, L, B, half_offset ? 1 : 0,
+                               center_offset, (double2*)out, st);
+}
+
+// estimate_freqshift (sfft/reconstruct.py:356-371): mean of x[idx] w^{f idx}.
+SFFT_API int sfft_freqshift_estimate(int dtype, const void* x, int64_t n, const int64_t* idx,
+                                     int64_t count, int64_t f, void* out, void* ws,
+                                     size_t ws_bytes, void* stream) {
+  SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_freqshift_estimate: dtype must be 0 or 1");
+  SFFT_REQUIRE(x && idx && out && ws, "sfft_freqshift_estimate: null pointer");
+  SFFT_REQUIRE(n > 0 && count >= 1, "sfft_freqshift_estimate: need n > 0 and count >= 1");
+  SFFT_REQUIRE(ws_bytes >= 256 * sizeof(double2), "sfft_freqshift_estimate: workspace too small");
+  return run_freqshift(dtype, x, n, idx, count, f, (double2*)ws, (double2*)out,
+                       (cudaStream_t)stream);
+}
+
 // Mark one read schedule into a byte map (kind 0 flat: a=sigma b=tau_tot
 // c=omega; 1 spike: a=stride b=tau c=count; 2 all; 3 list: idx[c]).
 SFFT_API int sfft_access_mark(uint8_t* map, int64_t n, int kind, int64_t a, int64_t b,

@@ -100,6 +100,19 @@ __device__ __forceinline__ double2 produce(const Prod& p, const ItemCtx& c, int 
     const Tin* xs = (const Tin*)c.xs;
     const int64_t L = n / p.B;
     return Sample<Tin>::load(xs, pmod(L * s - c.a, n));
+  } else if (MODE == PROD_DIRICHLET) {
+    // conj of the folded box window: sum over rows r of
+    // (taps[i] * x[(t - i) mod n]) * hm_i, i = s + r B < L, hm_i = w^{-(L/2) i}
+    // unless half_offset (the forward FFT of the conjugate is the inverse one)
+    const Tin* xs = (const Tin*)c.xs;
+    const int64_t L = p.omega, t = pmod(c.a, n);
+    double2 acc = cmk(0.0, 0.0);
+    for (int64_t i = s; i < L; i += p.B) {
+      double2 w = cmul_rn(p.ctaps[i], Sample<Tin>::load(xs, pmod(t - i, n)));
+      if (!p.half_offset) w = cmul_rn(w, unit_root(n, pmod(-mulmod((L / 2) % n, i % n, n), n)));
+      acc = cadd_rn(acc, w);
+    }
+    return cmk(acc.x, -acc.y);
   } else if (MODE == PROD_GTAB) {
     double2 acc = cmk(0.0, 0.0);
     int64_t e = mulmod(c.a, s % n, n);
@@ -591,7 +604,88 @@ static int run_bucketize_inner(int dtype, int mode, const Prod& p, int64_t nitem
                       : run_bucketize_t<double2, PROD_SPIKE>(p, nitems, W, out, ws, ws_bytes, st);
   if (mode == PROD_GTAB)
     return run_bucketize_t<double2, PROD_GTAB>(p, nitems, W, out, ws, ws_bytes, st);
+  if (mode == PROD_DIRICHLET)
+    return dtype == 0
+               ? run_bucketize_t<float2, PROD_DIRICHLET>(p, nitems, W, out, ws, ws_bytes, st)
+               : run_bucketize_t<double2, PROD_DIRICHLET>(p, nitems, W, out, ws, ws_bytes, st);
   return run_bucketize_t<double2, PROD_LOAD>(p, nitems, W, out, ws, ws_bytes, st);
+}
+
+// out[k] = (sum_t B conj(y_t[k]) w^{c_k t}) / T over the offsets in order,
+// c_k = (k L + base + center) mod n (bucket_centers, sfft/filters.py:92-100)
+__global__ void k_dirichlet_combine(const double2* __restrict__ y, int64_t noff,
+                                    const int64_t* __restrict__ offsets, int64_t n, int64_t L,
+                                    int64_t B, int half, int64_t center, double2* out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= B) return;
+  const int64_t c = pmod(k * L + (half ? 0 : L / 2) + center, n);
+  const double bd = (double)B;
+  double2 tot = cmk(0.0, 0.0);
+  for (int64_t t = 0; t < noff; ++t) {
+    const double2 v = y[t * B + k];                           // FFT(conj z)[k] / B
+    const double2 vb = cmul(cmk(bd, 0.0), cmk(v.x, -v.y));   // b * ifft(z)[k]
+    tot = cadd(tot, cmul(vb, unit_root(n, mulmod(c, pmod(offsets[t], n), n))));
+  }
+  out[k] = cdiv(tot, cmk((double)noff, 0.0));
+}
+
+int run_dirichlet_combine(const double2* y, int64_t noff, const int64_t* offsets, int64_t n,
+                          int64_t L, int64_t B, int half_offset, int64_t center_offset,
+                          double2* out, cudaStream_t st) {
+  k_dirichlet_combine<<<(unsigned)cdiv_up(B, 256), 256, 0, st>>>(y, noff, offsets, n, L, B,
+                                                                  half_offset,
+                                                                  pmod(center_offset, n), out);
+  SFFT_CHECK_LAUNCH("k_dirichlet_combine");
+  return 0;
+}
+
+// mean_i x[idx_i] w^{f idx_i} (sfft/reconstruct.py:356-371): block partial
+// sums over contiguous index ranges, then an ordered sum of the partials
+constexpr int kFsBlocks = 256, kFsNT = 256;
+
+template <typename Tin>
+__global__ void __launch_bounds__(kFsNT) k_freqshift_part(const Tin* __restrict__ x, int64_t n,
+                                                          const int64_t* __restrict__ idx,
+                                                          int64_t count, int64_t f,
+                                                          double2* partial) {
+  __shared__ double2 red[kFsNT / 32];
+  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(count, i0 + per);
+  double2 acc = cmk(0.0, 0.0);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kFsNT) {
+    const int64_t e = pmod(idx[i], n);
+    acc = cadd(acc, cmul(Sample<Tin>::load(x, e), unit_root(n, mulmod(pmod(f, n), e, n))));
+  }
+  for (int o = 16; o; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = red[0];
+    for (int w = 1; w < kFsNT / 32; ++w) t = cadd(t, red[w]);
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_freqshift_final(const double2* partial, int nb, int64_t count, double2* out) {
+  double2 t = cmk(0.0, 0.0);
+  for (int b = 0; b < nb; ++b) t = cadd(t, partial[b]);
+  out[0] = cdiv(t, cmk((double)count, 0.0));
+}
+
+int run_freqshift(int dtype, const void* x, int64_t n, const int64_t* idx, int64_t count,
+                  int64_t f, double2* partial, double2* out, cudaStream_t st) {
+  const int nb = (int)std::min<int64_t>(kFsBlocks, cdiv_up(count, kFsNT));
+  if (dtype == 0)
+    k_freqshift_part<float2><<<nb, kFsNT, 0, st>>>((const float2*)x, n, idx, count, f, partial);
+  else
+    k_freqshift_part<double2><<<nb, kFsNT, 0, st>>>((const double2*)x, n, idx, count, f, partial);
+  SFFT_CHECK_LAUNCH("k_freqshift_part");
+  k_freqshift_final<<<1, 1, 0, st>>>(partial, nb, count, out);
+  SFFT_CHECK_LAUNCH("k_freqshift_final");
+  return 0;
 }
 
 BucketProf& bucket_prof() {

@@ -9,7 +9,7 @@
 
 namespace sfft {
 
-enum ProdMode { PROD_FLAT = 0, PROD_SPIKE = 1, PROD_GTAB = 2, PROD_LOAD = 3 };
+enum ProdMode { PROD_FLAT = 0, PROD_SPIKE = 1, PROD_GTAB = 2, PROD_LOAD = 3, PROD_DIRICHLET = 4 };
 
 struct Prod {
   const void* x;             // [nsig][xstride] float2 (c64) or double2 (c128)
@@ -26,6 +26,8 @@ struct Prod {
   const int32_t* item_active;  // per-item gate (null: all)
   const double2* z;          // PROD_LOAD source [nitems][B]
   unsigned long long* prof_items;  // profiling: count of non-skipped items (null: off)
+  const double2* ctaps;      // Dirichlet: complex box taps [omega] (omega = L)
+  int half_offset;           // Dirichlet: 1 = rounding boundaries (no half-bucket modulation)
   int out_M;                 // > 0: item i writes output row (i % out_M) * out_S + i / out_M
   int64_t out_S;             //      (items ordered signal-major, rows shift-major)
 };
@@ -54,6 +56,13 @@ size_t bucketize_ws_bytes(int64_t B, int64_t nitems);
 int run_bucketize(int dtype, int mode, const Prod& p, int64_t nitems, const double2* W,
                   double2* out, void* ws, size_t ws_bytes, cudaStream_t st);
 int run_twiddle(double2* W, int64_t B, cudaStream_t st);
+// Dirichlet bank (sfft/bucketize.py:181-211): per-offset transforms y [noff][B]
+// (forward FFT of the conjugated fold / B) combined into out [B]
+int run_dirichlet_combine(const double2* y, int64_t noff, const int64_t* offsets, int64_t n,
+                          int64_t L, int64_t B, int half_offset, int64_t center_offset,
+                          double2* out, cudaStream_t st);
+int run_freqshift(int dtype, const void* x, int64_t n, const int64_t* idx, int64_t count,
+                  int64_t f, double2* partial, double2* out, cudaStream_t st);
 int run_flat_taps(double* taps, int64_t omega, int64_t B, double gsig, cudaStream_t st);
 int run_absmax(const double2* v, int64_t count, double* out, cudaStream_t st);
 

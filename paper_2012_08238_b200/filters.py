@@ -15,11 +15,12 @@ import math
 import threading
 from dataclasses import dataclass
 
-from .errors import InvalidParameter
+from .errors import InvalidParameter, NonDivisorParameter
 from ._lib import check, lib, ptr, require_cuda, stream_of
 
 __all__ = ["WindowFilter", "FLAT", "SPIKE", "DIRICHLET", "default_gauss_sigma",
-           "default_flat_support", "make_flat_filter", "twiddles"]
+           "default_flat_support", "make_flat_filter", "make_dirichlet_bank",
+           "filter_freq_shift", "twiddles"]
 
 FLAT = "flat"
 SPIKE = "spike_train"
@@ -57,19 +58,21 @@ def default_flat_support(n: int, num_buckets: int) -> int:
 
 @dataclass(frozen=True, eq=False)
 class WindowFilter:
-    """Flat window with device-resident taps and response table."""
+    """A flat window (device taps + transposed response table) or a Dirichlet
+    bank (device complex box taps + natural-order response)."""
 
     kind: str
     n: int
     num_buckets: int
     bucket_width: int
     support: int
-    taps: object            # torch float64 [support] on the device
-    gtable: object          # torch complex128 [L][B]: gtable[r, j] = G[r + j*L]
+    taps: object            # flat: torch float64 [support]; Dirichlet: complex128 [L]
+    gtable: object          # flat: torch complex128 [L][B], gtable[r, j] = G[r + j*L]
     peak: float             # max |G|
     gauss_sigma: float = 0.0
     center_offset: int = 0
     half_bucket_offset: bool = True
+    response: object = None  # Dirichlet: complex128 [N] unnormalised box transform
 
     @property
     def device(self):
@@ -78,13 +81,31 @@ class WindowFilter:
     @property
     def freq_response(self):
         """G over [0, N) in natural order (device tensor)."""
+        if self.gtable is None:
+            return self.response
         return self.gtable.transpose(0, 1).reshape(self.n)
 
+    def bucket_centers(self):
+        """Position-space passband centers, one per bucket (sfft/filters.py:92-100)."""
+        import numpy as np
+        base = 0 if self.half_bucket_offset else self.bucket_width // 2
+        c = self.bucket_width * np.arange(self.num_buckets, dtype=np.int64) + base
+        if self.kind == DIRICHLET:
+            c = c + self.center_offset
+        elif self.kind == FLAT:
+            c = c - self.center_offset
+        return c % self.n
+
     def bucket_weight(self, bucket: int, position):
-        """G[(bucket*L - m) mod N] (sfft/filters.py:102-111, flat kind)."""
+        """Complex weight of spectrum ``position`` in ``bucket`` (sfft/filters.py:102-111):
+        flat G[(bucket*L - m) mod N]; Dirichlet response[(m - center) mod N]."""
         import numpy as np
         import torch
         m = np.asarray(position, dtype=np.int64)
+        if self.kind == DIRICHLET:
+            base = 0 if self.half_bucket_offset else self.bucket_width // 2
+            e = (m - (bucket * self.bucket_width + base)) % self.n
+            return self.response[torch.as_tensor(e, device=self.device)]
         e = (bucket * self.bucket_width - m) % self.n
         r = torch.as_tensor(e % self.bucket_width, device=self.device)
         j = torch.as_tensor(e // self.bucket_width, device=self.device)
@@ -133,3 +154,41 @@ def make_flat_filter(n: int, num_buckets: int, support: int | None = None,
     with _cache_lock:
         filt = _filt_cache.setdefault(key, filt)
     return filt
+
+
+def make_dirichlet_bank(n: int, bucket_width: int, num_buckets: int, half_offset: bool = True,
+                        device=None) -> WindowFilter:
+    """Bank of B modulated boxes of width L (sfft/filters.py:168-187): taps
+    sqrt(N)/L, unnormalised response; per-bucket modulation happens in the
+    bucketizer."""
+    L, b = bucket_width, num_buckets
+    if L * b != n:
+        raise NonDivisorParameter(f"bucket_width*num_buckets = {L}*{b} != n={n}")
+    import torch
+    dev = require_cuda(device)
+    taps = torch.full((L,), math.sqrt(n) / L, dtype=torch.complex128, device=dev)
+    pad = torch.zeros(n, dtype=torch.complex128, device=dev)
+    pad[:L] = taps
+    resp = torch.fft.fft(pad)  # setup only; the hot path never evaluates the response
+    return WindowFilter(kind=DIRICHLET, n=n, num_buckets=b, bucket_width=L, support=L,
+                        taps=taps, gtable=None, peak=float(resp.abs().max().item()),
+                        half_bucket_offset=half_offset, response=resp)
+
+
+def filter_freq_shift(f: WindowFilter, f0: int) -> WindowFilter:
+    """Move a Dirichlet bank's passbands by f0 bins: taps *= w^(-f0 * position),
+    center_offset += f0 (sfft/filters.py:190-200).  The device flat window keeps
+    real taps, so shifting it is not supported here."""
+    from dataclasses import replace
+    if f.kind != DIRICHLET:
+        raise NotImplementedError("filter_freq_shift: device path covers Dirichlet banks")
+    import numpy as np
+    import torch
+    from .signal import phase_factor
+    pos = np.arange(f.support, dtype=np.int64)
+    taps = f.taps * phase_factor(f.n, -int(f0) * pos, device=f.device)
+    pad = torch.zeros(f.n, dtype=torch.complex128, device=f.device)
+    pad[:f.support] = taps
+    resp = torch.fft.fft(pad)
+    return replace(f, taps=taps, response=resp, peak=float(resp.abs().max().item()),
+                   center_offset=(f.center_offset + int(f0)) % f.n)

@@ -14,11 +14,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._lib import check, lib, ptr, stream_of
-from .errors import FilterKindMismatch
+from .errors import FilterKindMismatch, InvalidParameter
 from .filters import FLAT
 
 __all__ = ["VoteTable", "robust_noise_floor", "vote_tally", "select_by_votes",
-           "noise_floors", "need_votes"]
+           "noise_floors", "need_votes", "estimate_freqshift"]
 
 
 def _dev_values(values, device=None):
@@ -139,3 +139,29 @@ def select_by_votes(table: VoteTable, keep: int, min_fraction: float) -> list:
                                  ptr(ws), wsb, stream_of(dev)), "sfft_vote_select")
     k = int(ncand.item())
     return [int(p) for p in cand[:k].cpu().tolist()]
+
+
+def estimate_freqshift(x, f: int, t: int, seed=0) -> complex:
+    """Coefficient at ``f`` by shift-to-DC random sampling (sfft/reconstruct.py:356-371):
+    mean of x[i] w^{f i} over t positions drawn exactly as the reference draws
+    them (numpy Generator on the host), or all N positions when t >= N."""
+    import torch
+    if t < 1:
+        raise InvalidParameter(f"t={t} must be >= 1")
+    n = x.n
+    if t >= n:
+        idx = np.arange(n, dtype=np.int64)
+    else:
+        rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+        idx = rng.integers(0, n, size=t)
+    xs = x.samples
+    dev = xs.device
+    it = torch.as_tensor(np.asarray(idx, dtype=np.int64), device=dev)
+    out = torch.empty(1, dtype=torch.complex128, device=dev)
+    ws = torch.empty(4096, dtype=torch.uint8, device=dev)
+    dt = 0 if xs.dtype == torch.complex64 else 1
+    check(lib().sfft_freqshift_estimate(dt, ptr(xs), n, ptr(it), int(it.numel()), int(f),
+                                        ptr(out), ptr(ws), 4096, stream_of(dev)),
+          "sfft_freqshift_estimate")
+    x.record(("list", it))
+    return complex(out.item())
