@@ -1223,7 +1223,7 @@ __global__ void k_po_apply(IterArgs a, const int32_t* corr) {
 // ------------------------------------------------------------------ host driver
 
 struct IterLayout {
-  size_t off[40];
+  size_t off[64];
   size_t total;
 };
 
@@ -1284,6 +1284,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(double) * (size_t)n,            // 37 real response table
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
+  static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
+                "IterLayout::off too small");
   for (int i = 0; i < cnt; ++i) {
     L.off[i] = o;
     o += al(sizes[i]);
