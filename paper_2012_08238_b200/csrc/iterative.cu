@@ -1275,7 +1275,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * cap,     // 28 corr (polish)
       sizeof(int32_t) * (size_t)S * M,       // 29 item_active
       sizeof(int32_t) * (size_t)S,           // 30 pgate
-      sizeof(uint32_t) * (size_t)S * ((n + 31) / 32),  // 31 read bitmap (samples_read)
+      0,                                     // 31 (unused)
       sizeof(int32_t) * (size_t)S * B,       // 32 heavy_b
       sizeof(int32_t) * (size_t)S * B,       // 33 hrank
       sizeof(int64_t) * (size_t)M,           // 34 loop shift of each item
@@ -1449,7 +1449,6 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   int32_t* corr = (int32_t*)(w + Lo.off[28]);
   a.item_active = (int32_t*)(w + Lo.off[29]);
   a.pgate = (int32_t*)(w + Lo.off[30]);
-  uint32_t* bitmap = (uint32_t*)(w + Lo.off[31]);
   a.heavy_b = (int32_t*)(w + Lo.off[32]);
   a.hrank = (int32_t*)(w + Lo.off[33]);
   int64_t* shifts = (int64_t*)(w + Lo.off[34]);
@@ -1488,7 +1487,6 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
   SFFT_CUDA(cudaMemsetAsync(a.stats, 0, sizeof(int32_t) * 8, st));
   SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
-  SFFT_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)S * ((n + 31) / 32), st));
 
   Prod p{};
   p.x = x;
@@ -1602,7 +1600,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
                                         out_coef, out_n, fin, rows);
     SFFT_CHECK_LAUNCH("k_finalize");
-    rc = run_union_bitmap(a.groups, ngroups, S, n, bitmap, out_samples, fin, rows, st);
+    rc = run_union_smem(a.groups, ngroups, S, n, out_samples, fin, rows, st);
     if (rc) return rc;
     if (out_sched) {
       k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched, fin, rows);

@@ -384,3 +384,94 @@ inline int run_union_bitmap(const Group* groups, const int32_t* ngroups, int S, 
 }
 
 }  // namespace sfft
+
+namespace sfft {
+
+// Shared-memory variant: CTA r of a finishing slot owns the index range
+// [r R, (r+1) R) as an R-bit map in shared memory, walks every read of the
+// slot's groups, sets the bits that fall in its range (shared atomics) and
+// popcounts its map; samples[row] accumulates the CTAs' counts.  No global
+// bitmap, no global atomics per read.
+constexpr int kMarkNT = 1024;
+constexpr int64_t kMarkBits = 1 << 20;  // 128 KB of shared memory per CTA
+
+static __global__ void __launch_bounds__(kMarkNT) k_mark_count_smem(
+    const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
+    const int32_t* gate, const int32_t* rows, unsigned long long* samples) {
+  extern __shared__ uint32_t mbits[];
+  __shared__ Group sg[kMaxGroups];
+  __shared__ GroupSh sp[kMaxGroups];
+  __shared__ unsigned long long red[32];
+  const int s = blockIdx.y;
+  if (gate && !gate[s]) return;
+  const int64_t r0 = (int64_t)blockIdx.x * kMarkBits;
+  if (r0 >= n) return;
+  const int64_t r1 = min(n, r0 + kMarkBits);
+  const int64_t words = (r1 - r0 + 31) / 32;
+  const int G = min(ngroups[s], kMaxGroups);
+  const Group* gs = groups + (int64_t)s * gstride;
+  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
+  for (int i = threadIdx.x; i < G; i += kMarkNT) sg[i] = gs[i];
+  for (int64_t w = threadIdx.x; w < words; w += kMarkNT) mbits[w] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += kMarkNT) merge_pieces(sg[i], n, &sp[i]);
+  __syncthreads();
+  for (int g = 0; g < G; ++g) {
+    if (sg[g].kind == 0) {
+      // flat pieces [lo, hi) of u: e = sigma u mod n, advanced incrementally
+      const int64_t sig = sg[g].a;
+      const int64_t step = mulmod(sig, kMarkNT % n, n);
+      for (int i = 0; i < sp[g].np; ++i) {
+        const int64_t lo = sp[g].lo[i], hi = sp[g].hi[i];
+        int64_t u = lo + threadIdx.x;
+        if (u >= hi) continue;
+        int64_t e = mulmod(sig, u, n);
+        for (; u < hi; u += kMarkNT) {
+          if (e >= r0 && e < r1) {
+            const int64_t o = e - r0;
+            atomicOr(&mbits[o >> 5], 1u << (o & 31));
+          }
+          e += step;
+          e -= (e >= n) ? n : 0;
+        }
+      }
+      continue;
+    }
+    const int64_t tot = sp[g].total;
+    for (int64_t j = threadIdx.x; j < tot; j += kMarkNT) {
+      const int64_t e = group_elem(sg[g], sp[g], n, j, mask);
+      if (e >= r0 && e < r1) {
+        const int64_t o = e - r0;
+        atomicOr(&mbits[o >> 5], 1u << (o & 31));
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long c = 0;
+  for (int64_t w = threadIdx.x; w < words; w += kMarkNT) c += __popc(mbits[w]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < kMarkNT / 32; ++i) t += red[i];
+    if (t) atomicAdd(samples + (rows ? rows[s] : s), t);
+  }
+}
+
+inline int run_union_smem(const Group* groups, const int32_t* ngroups, int S, int64_t n,
+                          int64_t* samples, const int32_t* gate, const int32_t* rows,
+                          cudaStream_t st) {
+  k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
+  SFFT_CHECK_LAUNCH("k_zero_rows");
+  const size_t sm = (size_t)(std::min<int64_t>(n, kMarkBits) + 31) / 32 * sizeof(uint32_t);
+  SFFT_CUDA(cudaFuncSetAttribute(k_mark_count_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+  dim3 g((unsigned)((n + kMarkBits - 1) / kMarkBits), S);
+  k_mark_count_smem<<<g, kMarkNT, sm, st>>>(groups, ngroups, kMaxGroups, n, gate, rows,
+                                            (unsigned long long*)samples);
+  SFFT_CHECK_LAUNCH("k_mark_count_smem");
+  return 0;
+}
+
+}  // namespace sfft
