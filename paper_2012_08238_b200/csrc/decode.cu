@@ -381,7 +381,32 @@ __global__ void __launch_bounds__(256) k_vote_collect(VoteRounds vr, FastVote fv
   for (int r = threadIdx.x; r < R; r += blockDim.x) ssig[r] = vr.sigma[(int64_t)s * R + r];
   __syncthreads();
   const int64_t* bps = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
-  if (MODE == 0) {
+  const bool fast32 = MODE == 0 && fv.nmask >= 0 && fv.logL >= 0 && !bps && vr.cs == 0 &&
+                      vr.n <= (int64_t(1) << 32) && vr.words <= 64 * 1024;
+  if (fast32) {
+    // power-of-two N: bucket of f in round r is ((sigma_r f mod 2^32 & (N-1)) + L/2 & (N-1)) >> log2 L
+    const uint32_t mask = (uint32_t)fv.nmask, half = (uint32_t)(vr.L >> 1);
+    const int lg = fv.logL;
+    const int words = (int)vr.words;
+    for (int64_t f0 = (int64_t)blockIdx.x * blockDim.x; f0 < vr.n;
+         f0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t f = f0 + threadIdx.x;
+      const uint32_t fu = (uint32_t)f;
+      int c = 0;
+      if (f < vr.n) {
+        // stop once the remaining rounds cannot lift the count to `need`
+        // (the count itself only matters for candidates)
+        for (int r = 0; r < R; ++r) {
+          const uint32_t m = ((uint32_t)ssig[r] * fu) & mask;
+          const uint32_t b = ((m + half) & mask) >> lg;
+          c += (sb[r * words + (b >> 5)] >> (b & 31)) & 1u;
+          if (c + (R - 1 - r) < need) break;
+        }
+      }
+      vappend(f < vr.n && c >= need, ((unsigned long long)(R - c) << 40) | (unsigned long long)f,
+              s, cnt, buf);
+    }
+  } else if (MODE == 0) {
     for (int64_t f0 = (int64_t)blockIdx.x * blockDim.x; f0 < vr.n;
          f0 += (int64_t)gridDim.x * blockDim.x) {
       const int64_t f = f0 + threadIdx.x;
