@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=2048, help="signals per step (queue length)")
-    ap.add_argument("--slots", type=int, default=512, help="device slots kept in flight")
+    ap.add_argument("--slots", type=int, default=2048, help="device slots kept in flight")
     ap.add_argument("--engines", type=int, default=1, help="concurrent engines (streams)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0,
