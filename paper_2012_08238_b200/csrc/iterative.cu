@@ -1230,7 +1230,7 @@ struct IterLayout {
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 constexpr int kMaxSubSplit = 16;   // tone splits of the full-B subtraction
-constexpr int kMaxLadSplit = 16;   // tone splits of the ladder model
+constexpr int kMaxLadSplit = 8;    // tone splits of the ladder model
 
 static int ht_size(int cap) {
   int h = 1;
