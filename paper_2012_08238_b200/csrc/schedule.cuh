@@ -393,7 +393,7 @@ namespace sfft {
 // popcounts its map; samples[row] accumulates the CTAs' counts.  No global
 // bitmap, no global atomics per read.
 constexpr int kMarkNT = 1024;
-constexpr int64_t kMarkBits = 1 << 20;  // 128 KB of shared memory per CTA
+constexpr int64_t kMarkBits = 176 * 1024 * 8;  // 176 KB of shared memory per CTA (N = 2^22: 3 CTAs)
 
 static __global__ void __launch_bounds__(kMarkNT) k_mark_count_smem(
     const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
