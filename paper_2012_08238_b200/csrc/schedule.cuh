@@ -1,15 +1,14 @@
-// Read schedules of the runners and the map-free samples_read count.
+// Read schedules of the runners and the samples_read count.
 //
 // The reference marks a bool map per gathered index (sfft/signal.py:82-86)
 // and counts it at the end (RecoveryResult.samples_read, sfft/frameworks.py:
 // 151-155).  Here each signal logs its measurement groups instead — a flat
 // group is one permutation sigma with a handful of extra shifts (the phase
-// ladder, or the polish shifts 0/1/2), a spike group one (stride, tau) — and
-// one CTA per signal counts |union of read indices| exactly:
+// ladder, or the polish shifts 0/1/2; kind 2: an arithmetic shift set), a
+// spike group one (stride, tau):
 //   flat group g reads {sigma_g * t : t in U_g},  U_g = union_d [-tau-d, Omega-tau-d) mod n
-//   an index e of group g is new iff no earlier group h holds it:
-//     flat h:  (sigma_h^{-1} e mod n) in U_h;  spike h: (e + tau_h) mod L_h == 0.
-// No bookkeeping store touches HBM during the gathers.
+// and k_mark_count_smem counts |union of read indices| exactly from bitmaps
+// in shared memory.  No bookkeeping store touches HBM during the gathers.
 #pragma once
 
 #include "block.cuh"
@@ -104,30 +103,6 @@ __device__ __forceinline__ int64_t mulmod_n(int64_t a, int64_t b, int64_t n, int
   return mask >= 0 ? ((a * b) & mask) : (a * b) % n;
 }
 
-__device__ __forceinline__ bool group_has(const Group& g, const GroupSh& gs, int64_t n,
-                                          int64_t e, int64_t mask) {
-  if (g.kind == 1) {
-    const int64_t v = pmod(e + g.tau, n);
-    return (v % g.a) == 0 && (v / g.a) < g.cnt;
-  }
-  const int64_t t = mulmod_n(gs.ainv, e, n, mask);
-  if (g.kind == 2) {
-    // (v + k*step) mod n in [0, w) for some k < c, v = t + tau; step | n
-    const int64_t w = g.cnt >= n ? n : g.cnt;
-    if (w >= n) return true;
-    const int64_t step = g.sh[0], c = g.nsh, S = n / step;
-    const int64_t v = pmod(t + g.tau, n);
-    const int64_t r = v % step, j0 = v / step;
-    if (r >= w) return false;
-    int64_t jm = (w - r + step - 1) / step;
-    jm = jm < S ? jm : S;
-    return j0 < jm || j0 + c - 1 >= S;
-  }
-  for (int i = 0; i < gs.np; ++i)
-    if (t >= gs.lo[i] && t < gs.hi[i]) return true;
-  return false;
-}
-
 // e of element j of group g (j < gs.total)
 __device__ __forceinline__ int64_t group_elem(const Group& g, const GroupSh& gs, int64_t n,
                                               int64_t j, int64_t mask) {
@@ -176,218 +151,14 @@ static __global__ void k_export_groups(const Group* __restrict__ groups, const i
   }
 }
 
-constexpr int kUnionNT = 512;
-
-// One CTA per signal: samples[s] = |union of the read sets of groups[s][0..ngroups[s])|.
-static __global__ void __launch_bounds__(kUnionNT) k_union_count(const Group* __restrict__ groups,
-                                                          const int32_t* ngroups, int gstride,
-                                                          int64_t n, int64_t* samples) {
-  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
-  __shared__ Group sg[kMaxGroups];
-  __shared__ GroupSh sp[kMaxGroups];
-  __shared__ unsigned long long red[32];
-  const int s = blockIdx.x;
-  const int G = min(ngroups[s], kMaxGroups);
-  const Group* gs = groups + (int64_t)s * gstride;
-  for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < G; i += kUnionNT) merge_pieces(sg[i], n, &sp[i]);
-  __syncthreads();
-  unsigned long long cnt = 0;
-  for (int g = 0; g < G; ++g) {
-    const int64_t tot = sp[g].total;
-    for (int64_t j = threadIdx.x; j < tot; j += kUnionNT) {
-      const int64_t e = group_elem(sg[g], sp[g], n, j, mask);
-      bool fresh = true;
-      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e, mask);
-      cnt += fresh;
-    }
-  }
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < kUnionNT / 32; ++i) t += red[i];
-    samples[s] = (int64_t)t;
-  }
-}
-
-}  // namespace sfft
-
-namespace sfft {
-
-// Multi-CTA variant: grid (chunks, S); the element space of all groups is cut
-// into gridDim.x ranges; counts are accumulated with integer atomics into
-// samples[s] (zeroed by the caller), so the result is exact and deterministic.
-static __global__ void __launch_bounds__(kUnionNT) k_union_count_mc(
-    const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
-    unsigned long long* samples, const int32_t* gate, const int32_t* rows) {
-  __shared__ Group sg[kMaxGroups];
-  __shared__ GroupSh sp[kMaxGroups];
-  __shared__ int64_t gstart[kMaxGroups + 1];
-  __shared__ unsigned long long red[32];
-  const int s = blockIdx.y;
-  if (gate && !gate[s]) return;
-  const int64_t row = rows ? rows[s] : s;
-  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
-  const int G = min(ngroups[s], kMaxGroups);
-  const Group* gs = groups + (int64_t)s * gstride;
-  for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < G; i += kUnionNT) merge_pieces(sg[i], n, &sp[i]);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int g = 0; g < G; ++g) {
-      gstart[g] = acc;
-      acc += sp[g].total;
-    }
-    gstart[G] = acc;
-  }
-  __syncthreads();
-  const int64_t all = gstart[G];
-  const int64_t per = (all + gridDim.x - 1) / gridDim.x;
-  const int64_t c0 = (int64_t)blockIdx.x * per;
-  const int64_t c1 = min(all, c0 + per);
-  unsigned long long cnt = 0;
-  for (int g = 0; g < G; ++g) {
-    const int64_t lo = max(c0, gstart[g]), hi = min(c1, gstart[g + 1]);
-    for (int64_t j = lo + threadIdx.x; j < hi; j += kUnionNT) {
-      const int64_t e = group_elem(sg[g], sp[g], n, j - gstart[g], mask);
-      bool fresh = true;
-      for (int h = 0; h < g && fresh; ++h) fresh = !group_has(sg[h], sp[h], n, e, mask);
-      cnt += fresh;
-    }
-  }
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < kUnionNT / 32; ++i) t += red[i];
-    if (t) atomicAdd(samples + row, t);
-  }
-}
-
-// samples[s] = |union of read sets| for every signal (exact, multi-CTA).
+// samples[row of s] = 0 for the gated signals (before the count accumulates).
 static __global__ void k_zero_rows(int64_t* v, int S, const int32_t* gate, const int32_t* rows) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S || (gate && !gate[s])) return;
   v[rows ? rows[s] : s] = 0;
 }
 
-inline int run_union_count(const Group* groups, const int32_t* ngroups, int S, int64_t n,
-                           int64_t* samples, cudaStream_t st, int chunks = 48,
-                           const int32_t* gate = nullptr, const int32_t* rows = nullptr) {
-  if (gate || rows) {
-    k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
-    SFFT_CHECK_LAUNCH("k_zero_rows");
-  } else {
-    SFFT_CUDA(cudaMemsetAsync(samples, 0, sizeof(int64_t) * S, st));
-  }
-  dim3 g(chunks, S);
-  k_union_count_mc<<<g, kUnionNT, 0, st>>>(groups, ngroups, kMaxGroups, n,
-                                           (unsigned long long*)samples, gate, rows);
-  SFFT_CHECK_LAUNCH("k_union_count_mc");
-  return 0;
-}
-
-}  // namespace sfft
-
-namespace sfft {
-
-// Bitmap variant for the continuous engine: every read index of a finishing
-// slot is OR-ed into the slot's N-bit map (L2 atomics), then the map is
-// popcounted and cleared for the slot's next signal.  O(total reads) instead
-// of O(reads x groups) membership tests.
-static __global__ void __launch_bounds__(kUnionNT) k_mark_bits(
-    const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
-    uint32_t* bits, int64_t words, const int32_t* gate) {
-  __shared__ Group sg[kMaxGroups];
-  __shared__ GroupSh sp[kMaxGroups];
-  __shared__ int64_t gstart[kMaxGroups + 1];
-  const int s = blockIdx.y;
-  if (gate && !gate[s]) return;
-  const int G = min(ngroups[s], kMaxGroups);
-  const Group* gs = groups + (int64_t)s * gstride;
-  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
-  for (int i = threadIdx.x; i < G; i += kUnionNT) sg[i] = gs[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < G; i += kUnionNT) merge_pieces(sg[i], n, &sp[i]);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int g = 0; g < G; ++g) {
-      gstart[g] = acc;
-      acc += sp[g].total;
-    }
-    gstart[G] = acc;
-  }
-  __syncthreads();
-  const int64_t all = gstart[G];
-  const int64_t per = (all + gridDim.x - 1) / gridDim.x;
-  const int64_t c0 = (int64_t)blockIdx.x * per;
-  const int64_t c1 = min(all, c0 + per);
-  uint32_t* b = bits + (int64_t)s * words;
-  for (int g = 0; g < G; ++g) {
-    const int64_t lo = max(c0, gstart[g]), hi = min(c1, gstart[g + 1]);
-    for (int64_t j = lo + threadIdx.x; j < hi; j += kUnionNT) {
-      const int64_t e = group_elem(sg[g], sp[g], n, j - gstart[g], mask);
-      atomicOr(&b[e >> 5], 1u << (e & 31));
-    }
-  }
-}
-
-static __global__ void k_popcount_clear(uint32_t* bits, int64_t words, const int32_t* gate,
-                                        const int32_t* rows, unsigned long long* samples) {
-  __shared__ unsigned long long red[32];
-  const int s = blockIdx.y;
-  if (gate && !gate[s]) return;
-  uint32_t* b = bits + (int64_t)s * words;
-  unsigned long long c = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = b[i];
-    if (v) {
-      c += __popc(v);
-      b[i] = 0u;
-    }
-  }
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += red[i];
-    if (t) atomicAdd(samples + (rows ? rows[s] : s), t);
-  }
-}
-
-// bits: [S][ceil(n/32)] zero on entry, zero again on return.
-inline int run_union_bitmap(const Group* groups, const int32_t* ngroups, int S, int64_t n,
-                            uint32_t* bits, int64_t* samples, const int32_t* gate,
-                            const int32_t* rows, cudaStream_t st) {
-  const int64_t words = (n + 31) / 32;
-  k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
-  SFFT_CHECK_LAUNCH("k_zero_rows");
-  k_mark_bits<<<dim3(64, S), kUnionNT, 0, st>>>(groups, ngroups, kMaxGroups, n, bits, words,
-                                                gate);
-  SFFT_CHECK_LAUNCH("k_mark_bits");
-  k_popcount_clear<<<dim3(32, S), 512, 0, st>>>(bits, words, gate, rows,
-                                                (unsigned long long*)samples);
-  SFFT_CHECK_LAUNCH("k_popcount_clear");
-  return 0;
-}
-
-}  // namespace sfft
-
-namespace sfft {
-
-// Shared-memory variant: CTA r of a finishing slot owns the index range
+// samples_read: CTA r of a finishing slot owns the index range
 // [r R, (r+1) R) as an R-bit map in shared memory, walks every read of the
 // slot's groups, sets the bits that fall in its range (shared atomics) and
 // popcounts its map; samples[row] accumulates the CTAs' counts.  No global
