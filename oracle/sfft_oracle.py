@@ -349,6 +349,8 @@ class Cfg:
     spike_prestage: bool = False
     prestage_width: int = 32
     min_vote_fraction: float = 0.5
+    a_max: int = 4
+    pursuit_shifts: int = 8
     seed: int = 0
 
 
@@ -748,3 +750,152 @@ def synth(n: int, k: int, snr_db, seed: int, positions=None, magnitudes=None):
             sd = math.sqrt(p / (10.0 ** (snr_db / 10.0)) / 2.0)
             x = x + (rng.normal(0.0, sd, n) + 1j * rng.normal(0.0, sd, n))
     return x, {int(f): complex(c) for f, c in zip(positions, coefs)}
+
+
+# ---------------------------------------------------------------- one-shot
+
+class _Singular(Exception):
+    """SingularMomentMatrix / RankDeficient (sfft/errors.py)."""
+
+
+def _hankel_counts(moms: np.ndarray, a_max: int) -> np.ndarray:
+    """count_collisions (sfft/reconstruct.py:245-267): pooled singular values of
+    the per-bucket a_max x a_max moment Hankel matrices.  moms: [2 a_max][B]."""
+    b = moms.shape[1]
+    if b == 0:
+        return np.zeros(0, dtype=np.int64)
+    h = np.empty((b, a_max, a_max), dtype=np.complex128)
+    for i in range(b):
+        m = moms[:, i]
+        for r in range(a_max):
+            h[i, r, :] = m[r:r + a_max]
+    svals = np.linalg.svd(h, compute_uv=False)
+    pooled = np.sort(svals.ravel())[::-1]
+    cutoff = pooled[min(2 * b, pooled.size) - 1]
+    floor = max(3.0 * np.median(pooled), 1e-12 * pooled[0]) if pooled[0] > 0 else np.inf
+    counts = np.zeros(b, dtype=np.int64)
+    for i in range(b):
+        sv = svals[i]
+        ok = (sv >= cutoff) & (sv >= 0.1 * sv[0]) & (sv > floor)
+        counts[i] = min(int(ok.sum()), a_max)
+    return counts
+
+
+def _prony_positions(m: np.ndarray, a: int, bucket: int, b: int, n: int) -> list:
+    """locate_prony (sfft/reconstruct.py:270-302): linear prediction by lstsq,
+    companion roots on the unit circle, nearest admissible positions."""
+    rows = m.size - a
+    mat = np.empty((rows, a), dtype=np.complex128)
+    for r in range(rows):
+        mat[r] = m[r:r + a]
+    rhs = -m[a:a + rows]
+    coeffs, _, rank, sv = np.linalg.lstsq(mat, rhs, rcond=None)
+    if rank < a or sv[0] <= 0 or sv[-1] < 1e-10 * sv[0]:
+        raise _Singular("moment system rank")
+    roots = np.roots(np.concatenate([[1.0], coeffs[::-1]]))
+    mags = np.abs(roots)
+    if np.any(mags < 1e-12):
+        raise _Singular("vanishing root magnitude")
+    roots = roots / mags
+    cand = (bucket + b * np.arange(n // b, dtype=np.int64)) % n
+    out = []
+    for z in roots:
+        raw = (-np.angle(z) * n / (2 * np.pi)) % n
+        out.append(_nearest(raw, cand, n))
+    return sorted(out)
+
+
+def _prony_coeffs(positions, shifts, values, n: int) -> np.ndarray:
+    """estimate_prony without `keep` (sfft/reconstruct.py:374-409)."""
+    positions = np.asarray(positions, dtype=np.int64)
+    a = positions.size
+    if a == 0:
+        return np.zeros(0, dtype=np.complex128)
+    if shifts.size < a:
+        raise _Singular("too few measurements")
+    vand = unit_root(n, np.outer(shifts, positions))
+    sol, _, rank, _ = np.linalg.lstsq(vand, values, rcond=None)
+    if rank < a:
+        raise _Singular("measurement matrix rank")
+    return sol
+
+
+def one_shot(acc: Access, k: int, cfg: Cfg) -> Outcome:
+    """run_oneshot (sfft/frameworks.py:216-311): spike-train moments at shifts
+    0..2a_max-1, ladder rungs and random pursuit shifts; Hankel collision
+    counts; single-tons by phase unwrapping, collisions by Prony with
+    escalation and a partner-subtraction refinement; least-squares
+    coefficients."""
+    n = acc.n
+    if k <= 0:
+        return _finish(acc, {}, 0, 0, True)
+    b = resolve_b("one_shot", cfg.num_buckets, n, k)
+    a_max = cfg.a_max
+    rng = np.random.default_rng(cfg.seed)
+    base = list(range(2 * a_max))
+    lad = ladder(n)
+    extra = [d for d in lad if d not in base]
+    pursuit = [int(t) for t in rng.integers(0, n, size=cfg.pursuit_shifts)]
+    shifts = np.array(base + extra + pursuit, dtype=np.int64)
+    meas = np.vstack([spike_buckets(acc, b, int(t)) for t in shifts])
+    rows = {d: meas[len(base) + j] for j, d in enumerate(extra)}
+    for d in lad:
+        if d in base:
+            rows[d] = meas[d]
+    moms = meas[:2 * a_max]
+    floor = noise_floor(np.abs(moms[0]))
+    counts = _hankel_counts(moms, a_max)
+    energy = np.abs(moms).mean(axis=0)
+
+    def solve(i, positions):
+        c = _prony_coeffs(positions, shifts, meas[:, i], n)
+        model = unit_root(n, np.outer(shifts, positions)) @ c
+        return c, float(np.abs(meas[:, i] - model).max())
+
+    def refine(i, positions, coeffs):
+        out = []
+        for j, f in enumerate(positions):
+            others = [(g, c) for l, (g, c) in enumerate(zip(positions, coeffs)) if l != j]
+            y0 = moms[0, i] - sum(c for _, c in others)
+            ys = {d: rows[d][i] - sum(c * unit_root(n, d * g) for g, c in others) for d in lad}
+            q = unwrap(y0, ys, n)
+            out.append(int(i + round((q - i) / b) * b) % n if q is not None else f)
+        return sorted(set(out))
+
+    entries: dict = {}
+    for i in range(b):
+        if counts[i] == 0 or energy[i] < floor:
+            continue
+        tol = max(float(floor), 0.05 * float(energy[i]))
+        best = None
+        if counts[i] == 1:
+            q = unwrap(moms[0, i], {d: rows[d][i] for d in lad}, n)
+            if q is not None:
+                pos = [int(i + round((q - i) / b) * b) % n]
+                try:
+                    c, r = solve(i, pos)
+                    best = (r, pos, c)
+                except _Singular:
+                    best = None
+        if best is None or best[0] >= tol:
+            for a in range(max(int(counts[i]), 2), a_max + 1):
+                try:
+                    pos = sorted(set(_prony_positions(moms[:, i], a, i, b, n)))
+                    pos = refine(i, pos, _prony_coeffs(pos, shifts, meas[:, i], n))
+                    c, r = solve(i, pos)
+                except _Singular:
+                    continue
+                if best is None or r < best[0]:
+                    best = (r, pos, c)
+                if r < tol:
+                    break
+        if best is None:
+            try:
+                pos = sorted(set(_prony_positions(moms[:, i], 1, i, b, n)))
+                c, r = solve(i, pos)
+                best = (r, pos, c)
+            except _Singular:
+                continue
+        for f, c in zip(best[1], best[2]):
+            entries[f] = entries.get(f, 0.0) + complex(c)
+    return _finish(acc, entries, k, 1, True)

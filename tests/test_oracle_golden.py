@@ -182,3 +182,23 @@ def test_dirichlet_golden():
     with pytest.raises(O.OracleError) as e:
         O.freqshift_estimate(O.Access(x), 3, 0)
     assert e.value.kind == errs["t0"]
+
+
+ONESHOT = runner_cases("oneshot")
+
+
+@pytest.mark.parametrize("case", ONESHOT, ids=[c[0]["name"] for c in ONESHOT])
+def test_oneshot_golden(case):
+    """One-shot (spike moments, Hankel counts, Prony, least squares;
+    sfft/frameworks.py:216-311) pinned bit-exactly."""
+    rec, arr = case
+    x = regen_signal(rec, arr)
+    np.testing.assert_allclose(sig_checksum(x), arr["checksum"], rtol=1e-12, atol=1e-9)
+    kw = dict(rec["cfg"])
+    kw.pop("framework")
+    out = O.one_shot(O.Access(x), rec["k"], O.Cfg(framework="one_shot", **kw))
+    assert list(out.entries.keys()) == arr["pos"].tolist()
+    np.testing.assert_array_equal(np.array(list(out.entries.values()), dtype=complex),
+                                  arr["coef"])
+    assert out.samples_read == rec["samples_read"]
+    assert out.iterations == rec["iterations"] and out.converged == rec["converged"]
