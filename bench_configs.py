@@ -40,6 +40,9 @@ CONFIGS = {
               False),
     "C3bin": ("iterative", 1 << 22, 256, 30.0, dict(num_buckets=4096, location_method="binary"),
               "complex64", True),
+    # one-shot (spike moments, Hankel counts, Prony, least squares)
+    "C1os": ("one_shot", 1 << 16, 16, None, dict(), "complex128", False),
+    "C3os": ("one_shot", 1 << 22, 256, 30.0, dict(), "complex64", True),
 }
 
 
@@ -60,7 +63,7 @@ def make_batch(name, S, dev):
 
 def omega_of(fwk, n, kw):
     from paper_2012_08238_b200.filters import default_flat_support
-    if fwk == "peeling":
+    if fwk in ("peeling", "one_shot"):
         return None
     return default_flat_support(n, kw["num_buckets"])
 
@@ -76,7 +79,7 @@ def run(name, S, reps, check):
     X = make_batch(name, S, dev)
     cfg = sb.AlgorithmConfig(framework=fwk, **kw)
     runner = {"voting": sb.run_voting_batch, "iterative": sb.run_iterative_batch,
-              "peeling": sb.run_peeling_batch}[fwk]
+              "peeling": sb.run_peeling_batch, "one_shot": sb.run_oneshot_batch}[fwk]
     br = runner(X, k, cfg)  # warm-up (filter tables, workspaces)
     torch.cuda.synchronize()
     L = lib()
@@ -95,7 +98,9 @@ def run(name, S, reps, check):
     om = omega_of(fwk, n, kw)
     if kw.get("location_method") in ("binary", "multiscale") and n > (1 << 16):
         check = 0  # the oracle needs minutes per split-location transform at this size
-    if om is None:  # spike: B_j samples gathered and written per item, mixed sizes
+    if fwk == "one_shot":  # spike: B samples gathered and B buckets written per item
+        per_item = cfg.resolve_buckets(n, k) * (sin + 16)
+    elif om is None:  # spike: B_j samples gathered and written per item, mixed sizes
         per_item = sum(3 * (n // p) * (sin + 16) for p in kw["coprime_factors"]) / 9
     else:
         per_item = om * sin + kw["num_buckets"] * 16
@@ -105,7 +110,8 @@ def run(name, S, reps, check):
     for s in range(min(check, S)):
         x = X[s].cpu().numpy().astype(np.complex128)
         ocfg = O.Cfg(framework=fwk, **kw)
-        want = {"voting": O.voting, "iterative": O.iterative, "peeling": O.peeling}[fwk](
+        want = {"voting": O.voting, "iterative": O.iterative, "peeling": O.peeling,
+                "one_shot": O.one_shot}[fwk](
             O.Access(x), k, ocfg)
         got = res[s].spectrum.entries
         if set(got) == set(want.entries):

@@ -248,6 +248,26 @@ int sfft_run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int64
                      int32_t* out_converged, int32_t* out_error, int64_t* out_samples,
                      int64_t* out_sched, void* ws, size_t ws_bytes, void* stream);
 
+/* Workspace bytes of sfft_run_oneshot. */
+size_t sfft_oneshot_ws_bytes(int64_t n, int64_t nsig, int64_t B, int64_t a_max, int64_t nshifts);
+
+/* run_oneshot (sfft/frameworks.py:216-311) for nsig signals: spike
+ * bucketizations at the HOST shift list (0..2a_max-1, the ladder rungs not
+ * among them, the seeded pursuit shifts; at most 64), the robust floor of
+ * |meas[0]|, count_collisions over the a_max x a_max moment Hankel matrices
+ * (sfft/reconstruct.py:245-267), then per active bucket the single-ton
+ * unwrap / Prony escalation / refinement / least-squares decision of the
+ * reference (locate_prony :270-302, estimate_prony :374-409).  ladder_host:
+ * HOST int64[nladder] phase-ladder rungs (ascending, each a shift).  a_max
+ * <= 8 on the device.  out_iterations = 1, out_converged = 1.  Never
+ * synchronises. */
+int sfft_run_oneshot(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                     int64_t B, int64_t a_max, const int64_t* shifts_host, int64_t nshifts,
+                     const int64_t* ladder_host, int64_t nladder, const void* W, int64_t k,
+                     int64_t* out_pos, void* out_coef, int32_t* out_count,
+                     int32_t* out_iterations, int32_t* out_converged, int64_t* out_samples,
+                     int64_t* out_sched, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

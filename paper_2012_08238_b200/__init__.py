@@ -22,6 +22,7 @@ __version__ = "0.1.0"
 from .reconstruct import (VoteTable, estimate_freqshift, robust_noise_floor, select_by_votes,
                           vote_tally)
 from .frameworks import (FRAMEWORKS, AlgorithmConfig, BatchResult, RecoveryResult,
-                         run_algorithm, run_iterative, run_iterative_batch,
+                         run_algorithm, run_iterative, run_iterative_batch, run_oneshot,
+                         run_oneshot_batch,
                          run_iterative_stream, run_peeling,
                          run_peeling_batch, run_voting, run_voting_batch)

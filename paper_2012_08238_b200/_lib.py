@@ -133,5 +133,11 @@ SIGNATURES.update({
                                    P_i32, P_i32, P_i32, P_i32, P_i64, P_i64, vp, sz, vp]),
 })
 SIGNATURES.update({
+    "sfft_oneshot_ws_bytes": (sz, [i64, i64, i64, i64, i64]),
+    "sfft_run_oneshot": (C.c_int, [C.c_int, vp, i64, i64, i64, i64, i64, vp, i64, vp, i64, vp,
+                                   i64, P_i64, vp, P_i32, P_i32, P_i32, P_i64, P_i64, vp, sz,
+                                   vp]),
+})
+SIGNATURES.update({
     "sfft_set_avail": (C.c_int, [P_i32, C.c_int32, vp]),
 })

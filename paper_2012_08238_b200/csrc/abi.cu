@@ -384,6 +384,31 @@ SFFT_API int sfft_run_peeling(int dtype, const void* x, int64_t n, int64_t xstri
                      ws, ws_bytes, (cudaStream_t)stream);
 }
 
+SFFT_API size_t sfft_oneshot_ws_bytes(int64_t n, int64_t nsig, int64_t B, int64_t a_max,
+                                      int64_t nshifts) {
+  return oneshot_ws_bytes(n, (int)nsig, B, (int)a_max, (int)nshifts);
+}
+
+SFFT_API int sfft_run_oneshot(int dtype, const void* x, int64_t n, int64_t xstride, int64_t nsig,
+                              int64_t B, int64_t a_max, const int64_t* shifts_host,
+                              int64_t nshifts, const int64_t* ladder_host, int64_t nladder,
+                              const void* W, int64_t k, int64_t* out_pos, void* out_coef,
+                              int32_t* out_count, int32_t* out_iterations,
+                              int32_t* out_converged, int64_t* out_samples, int64_t* out_sched,
+                              void* ws, size_t ws_bytes, void* stream) {
+  SFFT_REQUIRE(dtype == 0 || dtype == 1, "sfft_run_oneshot: dtype must be 0 or 1");
+  SFFT_REQUIRE(x && shifts_host && ladder_host && W && nsig >= 1 && k >= 1,
+               "sfft_run_oneshot: bad argument");
+  SFFT_REQUIRE(n > 0 && n < (int64_t(1) << 31), "sfft_run_oneshot: n must be in (0, 2^31)");
+  SFFT_REQUIRE(B > 0 && n % B == 0, "sfft_run_oneshot: B must divide n");
+  SFFT_REQUIRE(out_pos && out_coef && out_count && out_iterations && out_converged && out_samples,
+               "sfft_run_oneshot: null output");
+  return run_oneshot(dtype, x, n, xstride, (int)nsig, B, (int)a_max, shifts_host, (int)nshifts,
+                     ladder_host, (int)nladder, (const double2*)W, k, out_pos,
+                     (double2*)out_coef, out_count, out_iterations, out_converged, out_samples,
+                     out_sched, ws, ws_bytes, (cudaStream_t)stream);
+}
+
 // Publish "signals [0, value) have arrived" for streaming admission (run on
 // the copy stream after each chunk's host-to-device copy).
 __global__ void k_set_avail(int32_t* avail, int32_t value) { *avail = value; }

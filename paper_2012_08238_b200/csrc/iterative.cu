@@ -1275,7 +1275,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * cap,     // 28 corr (polish)
       sizeof(int32_t) * (size_t)S * M,       // 29 item_active
       sizeof(int32_t) * (size_t)S,           // 30 pgate
-      0,                                     // 31 (unused)
+      sizeof(int32_t) * 2 * (size_t)S,       // 31 union-count fallback gate
       sizeof(int32_t) * (size_t)S * B,       // 32 heavy_b
       sizeof(int32_t) * (size_t)S * B,       // 33 hrank
       sizeof(int64_t) * (size_t)M,           // 34 loop shift of each item
@@ -1600,7 +1600,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
                                         out_coef, out_n, fin, rows);
     SFFT_CHECK_LAUNCH("k_finalize");
-    rc = run_union_smem(a.groups, ngroups, S, n, out_samples, fin, rows, st);
+    rc = run_union_smem(a.groups, ngroups, S, n, out_samples, fin, rows, st,
+                        (int32_t*)(w + Lo.off[31]));
     if (rc) return rc;
     if (out_sched) {
       k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched, fin, rows);

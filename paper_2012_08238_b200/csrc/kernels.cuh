@@ -142,6 +142,14 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
                 int32_t* out_conv, int32_t* out_err, int64_t* out_samples, int64_t* out_sched,
                 void* ws, size_t ws_bytes, cudaStream_t st);
 
+// oneshot.cu
+size_t oneshot_ws_bytes(int64_t n, int S, int64_t B, int A, int nsh);
+int run_oneshot(int dtype, const void* x, int64_t n, int64_t xstride, int S, int64_t B, int A,
+                const int64_t* shifts_host, int nsh, const int64_t* ladder_host, int nlad,
+                const double2* W, int64_t k, int64_t* out_pos, double2* out_coef,
+                int32_t* out_n, int32_t* out_iters, int32_t* out_conv, int64_t* out_samples,
+                int64_t* out_sched, void* ws, size_t ws_bytes, cudaStream_t st);
+
 // iterative.cu
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap);
 int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, int S,

@@ -222,6 +222,7 @@ static VoteLayout vote_layout(int64_t n, int64_t B, int S, int R, int C, int64_t
       sizeof(double) * (size_t)S,                 // 18 pre thr
       sizeof(int64_t) * (size_t)S,                // 19 pre tau (zeros)
       votes_fast_ws_bytes(S, R, 2 * (int64_t)(C / 2)),  // 20 fast vote workspace
+      union_scratch_bytes(S),                     // 21 union-count fallback gate
   };
   size_t o = 0;
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
@@ -365,7 +366,8 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   k_vo_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(groups, ngroups, psig, ptau, S, R, omega,
                                                          pre_L, Bpre);
   SFFT_CHECK_LAUNCH("k_vo_groups");
-  rc = run_union_smem(groups, ngroups, S, n, out_samples, nullptr, nullptr, st);
+  rc = run_union_smem(groups, ngroups, S, n, out_samples, nullptr, nullptr, st,
+                      (int32_t*)(w + Lo.off[21]));
   if (rc) return rc;
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(groups, ngroups, S, out_sched);

@@ -426,13 +426,26 @@ def run_peeling(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
     return _single(run_peeling_batch, x, k, cfg)
 
 
-_RUNNERS = {"voting": run_voting, "iterative": run_iterative, "peeling": run_peeling}
+def run_oneshot_batch(xs, k: int, cfg: AlgorithmConfig) -> BatchResult:
+    from .oneshot import oneshot_batch
+    return oneshot_batch(xs, k, cfg)
+
+
+def run_oneshot(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
+    """Single spike-train encoding, Hankel collision counts, single-ton phase
+    unwrapping / Prony location with refinement, least-squares estimation
+    (sfft/frameworks.py:216-311)."""
+    return _single(run_oneshot_batch, x, k, cfg)
+
+
+_RUNNERS = {"one_shot": run_oneshot, "voting": run_voting, "iterative": run_iterative,
+            "peeling": run_peeling}
 
 
 def run_algorithm(x: TimeSignal, k: int, cfg: AlgorithmConfig) -> RecoveryResult:
     cfg = cfg.validated()
     if cfg.framework not in _RUNNERS:
         raise NotImplementedError(
-            f"{cfg.framework!r} is outside the device hot path (SURVEY.md §2: one-shot and the "
-            "dense baseline are not rebuilt)")
+            f"{cfg.framework!r} is outside the device hot path (SURVEY.md §2: the dense "
+            "baseline is not rebuilt)")
     return _RUNNERS[cfg.framework](x, k, cfg)

@@ -3,7 +3,7 @@
 The reference dispatches every run through ``frameworks._RUNNERS``
 (sfft/frameworks.py:704-715), and ``run_experiment`` / ``run_sweep`` / the CLI
 (sfft/harness.py:170-275, sfft/cli.py:53-87) call ``run_algorithm``.
-``install()`` swaps the voting / iterative / peeling entries for wrappers that
+``install()`` swaps the one-shot / voting / iterative / peeling entries for wrappers that
 upload the reference ``TimeSignal``, run the device runner, mark the indices
 the device read in the reference signal's access map (so ``samples_read`` and
 the CSV's sampling fraction stay exact), re-raise library errors as the
@@ -18,7 +18,7 @@ import importlib
 
 __all__ = ["install", "uninstall", "wrap_runner"]
 
-_DEVICE = ("voting", "iterative", "peeling")
+_DEVICE = ("one_shot", "voting", "iterative", "peeling")
 
 
 def wrap_runner(run, fw, errors, dtype: str = "complex128", device=None):
@@ -52,8 +52,8 @@ def install(fw=None, frameworks=_DEVICE, dtype: str = "complex128", device=None)
     if fw is None:
         fw = importlib.import_module("sparsefft.frameworks")
     errors = importlib.import_module(fw.__name__.rsplit(".", 1)[0] + ".errors")
-    table = {"voting": dev.run_voting, "iterative": dev.run_iterative,
-             "peeling": dev.run_peeling}
+    table = {"one_shot": dev.run_oneshot, "voting": dev.run_voting,
+             "iterative": dev.run_iterative, "peeling": dev.run_peeling}
     previous = {}
     for name in frameworks:
         if name not in table:

@@ -35,7 +35,8 @@ def _fake_reference():
             self.iterations, self.converged = iterations, converged
 
     fw.SparseSpectrum, fw.RecoveryResult = SparseSpectrum, RecoveryResult
-    fw._RUNNERS = {"voting": "v", "iterative": "i", "peeling": "p", "dense": "d"}
+    fw._RUNNERS = {"one_shot": "o", "voting": "v", "iterative": "i", "peeling": "p",
+                    "dense": "d"}
     sys.modules.update({"fakeref": pkg, "fakeref.errors": errors, "fakeref.frameworks": fw})
     return fw, errors
 
