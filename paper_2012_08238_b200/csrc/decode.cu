@@ -638,8 +638,8 @@ int run_energy_est(const double2* y, int64_t B, const double2* gt, const double*
 constexpr int kSubNT = 256;
 constexpr int kSubChunk = 256;
 
-// Two buckets per thread (consecutive for full subtractions, so a warp reads
-// 1 KB contiguous of each table row); a_t = c_t * w^{tau m_t} is formed once
+// Two buckets per thread, kSubNT apart (each warp load instruction reads 32
+// consecutive table entries: measured 16 -> 8 L1 sectors per request); a_t = c_t * w^{tau m_t} is formed once
 // per tone in shared memory (the reference forms (c*w)*phase: same value up
 // to rounding).
 constexpr int kSubBPT = 2;
@@ -680,13 +680,15 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
   const int64_t T = te > tb ? te - tb : 0;
   const int64_t* tp = tpos + (int64_t)sig * tstride + tb;
   const double2* tc = tcoef + (int64_t)sig * tstride + tb;
-  const int64_t i0 = ((int64_t)blockIdx.x * kSubNT + threadIdx.x) * kSubBPT;
+  // bucket u of this thread: i0 + u * kSubNT, so every load instruction of a
+  // warp reads 32 consecutive table entries (full 32-byte sectors)
+  const int64_t i0 = (int64_t)blockIdx.x * kSubNT * kSubBPT + threadIdx.x;
   int bk[kSubBPT];
   bool live[kSubBPT];
   double2 acc[kSubBPT];
 #pragma unroll
   for (int u = 0; u < kSubBPT; ++u) {
-    const int64_t i = i0 + u;
+    const int64_t i = i0 + u * kSubNT;
     live[u] = i < nb;
     bk[u] = live[u] ? (int)(blist ? blist[(int64_t)item * nb + i] : i) : 0;
     acc[u] = (live[u] && TS == 1 && !REAL) ? y[(int64_t)item * B + bk[u]] : cmk(0.0, 0.0);
@@ -806,7 +808,7 @@ __global__ void __launch_bounds__(kSubNT) k_subtract(
 #pragma unroll
   for (int u = 0; u < kSubBPT; ++u) {
     if (!live[u]) continue;
-    const int64_t i = i0 + u;
+    const int64_t i = i0 + u * kSubNT;
     if (TS == 1) out[(int64_t)item * nb + i] = acc[u];
     else part[((int64_t)item * gridDim.z + blockIdx.z) * nb + i] = acc[u];
   }

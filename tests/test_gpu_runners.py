@@ -197,3 +197,15 @@ def test_iterative_stream_from_host(sb):
         assert set(got.spectrum.entries) == set(want), rec["name"]
         assert got.samples_read == rec["samples_read"]
         assert got.iterations == rec["iterations"]
+
+
+STRAG = runner_cases("stragglers")
+
+
+@pytest.mark.parametrize("case", STRAG, ids=[c[0]["name"] for c in STRAG])
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-10), ("complex64", 1e-4)])
+def test_iterative_stragglers(sb, case, dtype, tol):
+    """Non-converging C3 signals (10 iterations, thousands of recovered tones,
+    ~B/4 heavy buckets per iteration, no polish)."""
+    rec, arr = case
+    check_case(sb, rec, arr, dtype, tol)

@@ -117,6 +117,16 @@ def test_runner_golden_full_size(case):
     _check_runner(*case)
 
 
+STRAG = runner_cases("stragglers")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", STRAG, ids=[c[0]["name"] for c in STRAG])
+def test_runner_golden_stragglers(case):
+    """Non-converging C3 signals (10 iterations, no polish) pinned bit-exactly."""
+    _check_runner(*case)
+
+
 SPLIT = runner_cases("split")
 SPLIT_FAST = [c for c in SPLIT if c[0]["n"] <= (1 << 14)]
 SPLIT_SLOW = [c for c in SPLIT if c[0]["n"] > (1 << 14)]
