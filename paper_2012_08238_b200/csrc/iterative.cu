@@ -112,6 +112,18 @@ struct IterArgs {
   int32_t* ht_val;               // [S][HT] index into rec_*
   int HT;                        // power of two >= 2*cap
   double2* part;                 // tone-split partial sums (subtract / ladder)
+  // measurement row cache (phase location): C rows per slot after the M*S
+  // working rows of y; entry c of slot s holds the bucketization of
+  // (perm dir_p[s][c], shift dir_d[s][c]) in row M*S + s*C + c
+  int C;
+  int32_t* dir_p;                // [S][C] permutation index (-1 empty)
+  int64_t* dir_d;                // [S][C] shift
+  int32_t* role_src;             // [S][M] cache entry feeding working row j this round (-1: measure)
+  int32_t* cnt;                  // [S + 1] items per slot, then exclusive offsets; [S] = total
+  int32_t* it2_sig;              // [S*(M+C)] compacted items: signal, sigma, tau_tot, output row
+  int64_t* it2_sigma;
+  int64_t* it2_tau;
+  int32_t* it2_row;
 };
 
 __device__ __forceinline__ uint32_t ht_slot(int64_t f, int HT) {
@@ -242,6 +254,109 @@ __global__ void k_cb_items(IterArgs a) {
   const int64_t d = (S.phase == PH_LOOP) ? a.shifts[j] : j;
   a.item_sigma_it[i] = a.item_sigma[s];
   a.item_tau_it[i] = pmod(a.item_tau[s] + d, a.n);
+}
+
+// Measurement planning with a row cache (phase location).  A slot's first
+// loop round also measures, speculatively and side by side with its own 8
+// loop items, the next loop permutation's M shifts and the 3 shifts of the 6
+// permutations after it (the polish passes of a signal that converges in two
+// iterations); every later round copies the rows it finds in the cache and
+// measures only the rest.  A transform's bucketizations then share their L2
+// lines across permutations (one launch instead of eight; measured 18 % less
+// gather time per transform), and the results are identical: the same
+// (sigma, tau_tot) item gives the same bucket values whenever it runs.
+__device__ __forceinline__ int64_t role_shift(const IterArgs& a, const IterState& S, int j) {
+  return (S.phase == PH_LOOP) ? a.shifts[j] : (int64_t)j;
+}
+
+__global__ void k_cb_plan(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  const IterState& S = a.st[s];
+  int32_t* dp = a.dir_p + (int64_t)s * a.C;
+  int64_t* dd = a.dir_d + (int64_t)s * a.C;
+  const bool first = S.phase == PH_LOOP && S.it == 1;
+  if (first)
+    for (int c = 0; c < a.C; ++c) dp[c] = -1;
+  int nm = 0;
+  for (int j = 0; j < a.M; ++j) {
+    int src = -1;
+    if (j < S.nsh) {
+      const int64_t d = role_shift(a, S, j);
+      for (int c = 0; c < a.C && src < 0; ++c)
+        if (dp[c] == S.pidx && dd[c] == d) src = c;
+      nm += src < 0;
+    }
+    a.role_src[(int64_t)s * a.M + j] = src;
+  }
+  int spec = 0;
+  if (first)
+    for (int c = 0; c < a.C; ++c) {
+      const int pp = S.pidx + 1 + (c < a.M ? 0 : 1 + (c - a.M) / 3);
+      spec += pp < a.P;
+    }
+  a.cnt[s] = nm + spec;
+}
+
+// exclusive scan of cnt[0..S) in place, total in cnt[S] (one CTA)
+__global__ void __launch_bounds__(1024) k_cb_scan(IterArgs a) {
+  __shared__ int red[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < a.S; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < a.S ? a.cnt[i] : 0;
+    int tot;
+    const int ex = block_exscan<1024>(v, red, &tot);
+    if (i < a.S) a.cnt[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.cnt[a.S] = carry;
+}
+
+__global__ void k_cb_fill(IterArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.S) return;
+  const IterState& S = a.st[s];
+  int o = a.cnt[s];
+  const int sig = S.sig > 0 ? S.sig : 0;
+  for (int j = 0; j < S.nsh && j < a.M; ++j) {
+    if (a.role_src[(int64_t)s * a.M + j] >= 0) continue;
+    a.it2_sig[o] = sig;
+    a.it2_sigma[o] = a.item_sigma[s];
+    a.it2_tau[o] = pmod(a.item_tau[s] + role_shift(a, S, j), a.n);
+    a.it2_row[o] = j * a.S + s;
+    ++o;
+  }
+  if (!(S.phase == PH_LOOP && S.it == 1)) return;
+  int32_t* dp = a.dir_p + (int64_t)s * a.C;
+  int64_t* dd = a.dir_d + (int64_t)s * a.C;
+  for (int c = 0; c < a.C; ++c) {
+    const int pp = S.pidx + 1 + (c < a.M ? 0 : 1 + (c - a.M) / 3);
+    if (pp >= a.P) continue;
+    const int64_t d = c < a.M ? a.shifts[c] : (int64_t)((c - a.M) % 3);
+    const int64_t row = (int64_t)sig * a.pstride + pp;
+    a.it2_sig[o] = sig;
+    a.it2_sigma[o] = a.psig[row];
+    a.it2_tau[o] = pmod(pmod(a.ptau[row], a.n) + d, a.n);
+    a.it2_row[o] = (int32_t)((int64_t)a.M * a.S + (int64_t)s * a.C + c);
+    dp[c] = pp;
+    dd[c] = d;
+    ++o;
+  }
+}
+
+// working row j of slot s <- its cache entry
+__global__ void k_cb_copy(IterArgs a) {
+  const int s = blockIdx.x / a.M, j = blockIdx.x - s * a.M;
+  const int c = a.role_src[(int64_t)s * a.M + j];
+  if (c < 0) return;
+  const double2* src = a.y + ((int64_t)a.M * a.S + (int64_t)s * a.C + c) * a.B;
+  double2* dst = a.y + ((int64_t)j * a.S + s) * a.B;
+  for (int64_t b = threadIdx.x; b < a.B; b += blockDim.x) dst[b] = src[b];
 }
 
 // End of a slot's loop: polish when converged well below the scale, else done
@@ -1232,6 +1347,10 @@ static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int kMaxSubSplit = 16;   // tone splits of the full-B subtraction
 constexpr int kMaxLadSplit = 8;    // tone splits of the ladder model
 
+// cached rows per slot: the next loop permutation's M shifts and 6 x 3 polish
+// shifts (phase-location ladders only, M <= 13)
+static int spec_rows(int M) { return M <= 13 ? M + 18 : 0; }
+
 static int ht_size(int cap) {
   int h = 1;
   while (h < 2 * cap) h <<= 1;
@@ -1251,7 +1370,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * M * S,               // 4 item_sig
       sizeof(int64_t) * M * S * 2,           // 5 item_sigma_it + item_sigma
       sizeof(int64_t) * M * S * 2,           // 6 item_tau_it + item_tau
-      sizeof(double2) * (size_t)M * S * B,   // 7 y
+      sizeof(double2) * (size_t)(M + spec_rows(M)) * S * B,  // 7 y (working rows + row cache)
       sizeof(double2) * (size_t)S * B,       // 8 resid
       sizeof(int64_t) * (size_t)S * cap,     // 9 rec_pos
       sizeof(double2) * (size_t)S * cap,     // 10 rec_coef
@@ -1282,6 +1401,12 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * B * 3,   // 35 split search r / ok / depth
       sizeof(int32_t) * (size_t)S * M,       // 36 item_fold
       sizeof(double) * (size_t)n,            // 37 real response table
+      sizeof(int32_t) * (size_t)S * spec_rows(M),               // 38 dir_p
+      sizeof(int64_t) * (size_t)S * spec_rows(M),               // 39 dir_d
+      sizeof(int32_t) * (size_t)S * M,                          // 40 role_src
+      sizeof(int32_t) * (size_t)(S + 1),                        // 41 cnt
+      sizeof(int32_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 42 it2_sig + it2_row
+      sizeof(int64_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 43 it2_sigma + it2_tau
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1295,7 +1420,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
 }
 
 size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap) {
-  return iter_layout(n, B, S, M, cap).total + bucketize_ws_bytes(B, (int64_t)M * S);
+  return iter_layout(n, B, S, M, cap).total +
+         bucketize_ws_bytes(B, (int64_t)(M + spec_rows(M)) * S);
 }
 
 template <int M>
@@ -1457,6 +1583,15 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.sp_ok = a.sp_r + (size_t)S * B;
   a.sp_depth = a.sp_ok + (size_t)S * B;
   a.item_fold = (int32_t*)(w + Lo.off[36]);
+  a.C = (loc == 0 && !getenv("SFFT_NO_ROW_CACHE")) ? spec_rows(M) : 0;
+  a.dir_p = (int32_t*)(w + Lo.off[38]);
+  a.dir_d = (int64_t*)(w + Lo.off[39]);
+  a.role_src = (int32_t*)(w + Lo.off[40]);
+  a.cnt = (int32_t*)(w + Lo.off[41]);
+  a.it2_sig = (int32_t*)(w + Lo.off[42]);
+  a.it2_row = a.it2_sig + (size_t)S * (M + spec_rows(M));
+  a.it2_sigma = (int64_t*)(w + Lo.off[43]);
+  a.it2_tau = a.it2_sigma + (size_t)S * (M + spec_rows(M));
   RealTab rt{};
   if (real_table_ok(omega)) {
     rt.at = (const double*)(w + Lo.off[37]);
@@ -1481,7 +1616,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CUDA(cudaMemcpyAsync(shifts, sh.data(), sizeof(int64_t) * M, cudaMemcpyHostToDevice, st));
     SFFT_CUDA(cudaStreamSynchronize(st));  // sh is a host temporary
   }
-  const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)M * S);
+  const size_t bws_bytes = bucketize_ws_bytes(B, (int64_t)(M + spec_rows(M)) * S);
 
   // all slots free; queue counter 0
   SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
@@ -1508,6 +1643,14 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
                          ? (int)cdiv_up(omega, B)
                          : 0;
   a.use_fold = fold_R > 0;
+  // compacted item list of the row-cache planner (k_cb_fill)
+  Prod pc = p;
+  pc.item_sig = a.it2_sig;
+  pc.item_a = a.it2_sigma;
+  pc.item_b = a.it2_tau;
+  pc.item_active = nullptr;
+  pc.item_row = a.it2_row;
+  pc.out_M = 0;
   Prod pl = p;
   pl.z = a.y;
   pl.item_active = a.item_fold;
@@ -1537,9 +1680,25 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CHECK_LAUNCH("k_cb_step");
     k_po_epoch<<<dim3(4, S), 256, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_po_epoch");
-    k_cb_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a);
-    SFFT_CHECK_LAUNCH("k_cb_items");
-    int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
+    int rc = 0;
+    if (a.C > 0) {
+      k_cb_plan<<<sb, 128, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_cb_plan");
+      k_cb_scan<<<1, 1024, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_cb_scan");
+      k_cb_fill<<<sb, 128, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_cb_fill");
+      k_cb_copy<<<(unsigned)(S * M), 256, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_cb_copy");
+      int32_t nit = 0;
+      SFFT_CUDA(cudaMemcpyAsync(&nit, a.cnt + S, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      SFFT_CUDA(cudaStreamSynchronize(st));
+      if (nit > 0) rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
+    } else {
+      k_cb_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_cb_items");
+      rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
+    }
     if (rc) return rc;
     if (fold_R > 0) {
       // split loop shifts d*B: row-correlation fold, then the FFTs in place

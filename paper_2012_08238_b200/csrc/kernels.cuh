@@ -30,9 +30,11 @@ struct Prod {
   int half_offset;           // Dirichlet: 1 = rounding boundaries (no half-bucket modulation)
   int out_M;                 // > 0: item i writes output row (i % out_M) * out_S + i / out_M
   int64_t out_S;             //      (items ordered signal-major, rows shift-major)
+  const int32_t* item_row;   // non-null: item i writes output row item_row[i] (takes precedence)
 };
 
 __host__ __device__ __forceinline__ int64_t out_row(const Prod& p, int64_t item) {
+  if (p.item_row) return p.item_row[item];
   return p.out_M > 0 ? (item % p.out_M) * p.out_S + item / p.out_M : item;
 }
 
