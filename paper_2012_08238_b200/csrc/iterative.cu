@@ -314,7 +314,10 @@ __global__ void __launch_bounds__(1024) k_cb_scan(IterArgs a) {
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) a.cnt[a.S] = carry;
+  if (threadIdx.x == 0) {
+    a.cnt[a.S] = carry;
+    a.stats[5] = carry;  // read by the host with the round status
+  }
 }
 
 __global__ void k_cb_fill(IterArgs a) {
@@ -1583,7 +1586,11 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.sp_ok = a.sp_r + (size_t)S * B;
   a.sp_depth = a.sp_ok + (size_t)S * B;
   a.item_fold = (int32_t*)(w + Lo.off[36]);
-  a.C = (loc == 0 && !getenv("SFFT_NO_ROW_CACHE")) ? spec_rows(M) : 0;
+  // the row cache pays where the gathers dominate (C3: Omega = 76,848) and
+  // enough slots fill the GPU; small windows and small batches are latency-
+  // bound and keep the per-round items
+  a.C = (loc == 0 && omega >= 32768 && S >= 512 && !getenv("SFFT_NO_ROW_CACHE")) ? spec_rows(M)
+                                                                                 : 0;
   a.dir_p = (int32_t*)(w + Lo.off[38]);
   a.dir_d = (int64_t*)(w + Lo.off[39]);
   a.role_src = (int32_t*)(w + Lo.off[40]);
@@ -1671,7 +1678,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   // streaming admission may spend rounds waiting for data: no round cap then
   const int max_rounds = avail ? (1 << 30) : (Q / S + 2) * (max_it + 8) + 16;
   int round = 0;
-  for (; round < max_rounds; ++round) {
+  // Round prologue (admission, the step of every slot's state machine, item
+  // planning).  It runs at the end of the previous round, so that the host
+  // reads the next round's item count with the round's one status read.
+  auto prologue = [&]() -> int {
     k_cb_admit<<<sb, 128, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_cb_admit");
     k_cb_clear<<<dim3(16, S), 256, 0, st>>>(a);
@@ -1680,7 +1690,6 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CHECK_LAUNCH("k_cb_step");
     k_po_epoch<<<dim3(4, S), 256, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_po_epoch");
-    int rc = 0;
     if (a.C > 0) {
       k_cb_plan<<<sb, 128, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_cb_plan");
@@ -1688,15 +1697,28 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
       SFFT_CHECK_LAUNCH("k_cb_scan");
       k_cb_fill<<<sb, 128, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_cb_fill");
-      k_cb_copy<<<(unsigned)(S * M), 256, 0, st>>>(a);
-      SFFT_CHECK_LAUNCH("k_cb_copy");
-      int32_t nit = 0;
-      SFFT_CUDA(cudaMemcpyAsync(&nit, a.cnt + S, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      SFFT_CUDA(cudaStreamSynchronize(st));
-      if (nit > 0) rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
     } else {
       k_cb_items<<<(unsigned)cdiv_up((int64_t)M * S, 256), 256, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_cb_items");
+    }
+    return 0;
+  };
+  int nit = 0;  // planned items of the coming round (row-cache path)
+  {
+    int rc0 = prologue();
+    if (rc0) return rc0;
+    if (a.C > 0) {
+      SFFT_CUDA(cudaMemcpyAsync(&nit, a.stats + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      SFFT_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  for (; round < max_rounds; ++round) {
+    int rc = 0;
+    if (a.C > 0) {
+      k_cb_copy<<<(unsigned)(S * M), 256, 0, st>>>(a);
+      SFFT_CHECK_LAUNCH("k_cb_copy");
+      if (nit > 0) rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
+    } else {
       rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
     }
     if (rc) return rc;
@@ -1768,11 +1790,14 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     }
     k_cb_release<<<sb, 128, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_cb_release");
+    rc = prologue();
+    if (rc) return rc;
     int32_t hs[8];
     SFFT_CUDA(cudaMemcpyAsync(hs, a.stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
     SFFT_CUDA(cudaStreamSynchronize(st));
     t_max = hs[1];
     h_max = hs[2];
+    nit = hs[5];
     if (hs[3] >= Q) break;
   }
   SFFT_REQUIRE(round < max_rounds, "iterative: round limit reached (internal error)");
