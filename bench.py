@@ -271,7 +271,7 @@ def main():
     achieved = (pi.value * item_bytes) / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
     peak, peak_kind = peaks()
     # DRAM traffic of the same kernel from the committed ncu --set full capture
-    # (profiles/r1_k_cluster_ncu_raw.json: first C3 loop round, "items" bucketizations)
+    # (profiles/r1_k_cluster_ncu_raw.json: the co-scheduled first round, "items" bucketizations)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r1_k_cluster_ncu_raw.json")) as f:
