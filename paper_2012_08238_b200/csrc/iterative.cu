@@ -1589,8 +1589,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   // the row cache pays where the gathers dominate (C3: Omega = 76,848) and
   // enough slots fill the GPU; small windows and small batches are latency-
   // bound and keep the per-round items
-  a.C = (loc == 0 && omega >= 32768 && S >= 512 && !getenv("SFFT_NO_ROW_CACHE")) ? spec_rows(M)
-                                                                                 : 0;
+  // (SFFT_ROW_CACHE=1 forces it on, SFFT_NO_ROW_CACHE=1 off: parity tests run both)
+  const bool rc_on = getenv("SFFT_ROW_CACHE") ? atoi(getenv("SFFT_ROW_CACHE")) != 0
+                                              : (omega >= 32768 && S >= 512);
+  a.C = (loc == 0 && rc_on && !getenv("SFFT_NO_ROW_CACHE")) ? spec_rows(M) : 0;
   a.dir_p = (int32_t*)(w + Lo.off[38]);
   a.dir_d = (int64_t*)(w + Lo.off[39]);
   a.role_src = (int32_t*)(w + Lo.off[40]);

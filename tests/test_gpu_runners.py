@@ -209,3 +209,38 @@ def test_iterative_stragglers(sb, case, dtype, tol):
     ~B/4 heavy buckets per iteration, no polish)."""
     rec, arr = case
     check_case(sb, rec, arr, dtype, tol)
+
+
+@pytest.mark.parametrize("slots", [1, 2, 3])
+def test_row_cache_continuous_batching(sb, slots, monkeypatch):
+    """The measurement row cache (speculative next-loop / polish rows, hits
+    copied, misses measured) forced on for C1 with slots refilled as signals
+    finish: every signal gets the reference's result."""
+    import torch
+    monkeypatch.setenv("SFFT_ROW_CACHE", "1")
+    cases = [c for c in CASES if c[0]["name"].startswith("C1")]
+    X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).cuda()
+    res = sb.run_iterative_batch(X, 16, _cfg(sb, cases[0][0]), slots=slots).to_results()
+    for (rec, arr), got in zip(cases, res):
+        want = dict(zip(arr["pos"].tolist(), arr["coef"].tolist()))
+        assert set(got.spectrum.entries) == set(want), rec["name"]
+        err = max(abs(got.spectrum.entries[f] - c) / abs(c) for f, c in want.items())
+        assert err <= 1e-10
+        assert (got.samples_read, got.iterations, got.converged) == \
+            (rec["samples_read"], rec["iterations"], rec["converged"]), rec["name"]
+
+
+def test_row_cache_c3_default_gate(sb):
+    """C3 (converging and non-converging signals) through 512 slots, where the
+    row cache is on by default, against the reference golden vectors."""
+    import torch
+    cases = [c for c in CASES if c[0]["name"].startswith("C3")] + list(STRAG)
+    X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).cuda()
+    res = sb.run_iterative_batch(X, 256, _cfg(sb, cases[0][0]), slots=512).to_results()
+    for (rec, arr), got in zip(cases, res):
+        want = dict(zip(arr["pos"].tolist(), arr["coef"].tolist()))
+        assert set(got.spectrum.entries) == set(want), rec["name"]
+        err = max(abs(got.spectrum.entries[f] - c) / abs(c) for f, c in want.items())
+        assert err <= 1e-10, (rec["name"], err)
+        assert (got.samples_read, got.iterations, got.converged) == \
+            (rec["samples_read"], rec["iterations"], rec["converged"]), rec["name"]
