@@ -1783,7 +1783,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
                                         out_coef, out_n, fin, rows);
     SFFT_CHECK_LAUNCH("k_finalize");
-    rc = run_union_smem(a.groups, ngroups, S, n, out_samples, fin, rows, st,
+    rc = run_union_count(a.groups, ngroups, S, n, out_samples, fin, rows, st,
                         (int32_t*)(w + Lo.off[31]));
     if (rc) return rc;
     if (out_sched) {

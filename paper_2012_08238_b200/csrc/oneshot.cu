@@ -610,7 +610,7 @@ int run_oneshot(int dtype, const void* x, int64_t n, int64_t xstride, int S, int
   k_os_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(S, nsh, n, B, dshifts, groups, ngroups,
                                                          out_iters, out_conv);
   SFFT_CHECK_LAUNCH("k_os_groups");
-  rc = run_union_smem(groups, ngroups, S, n, out_samples, nullptr, nullptr, st);
+  rc = run_union_count(groups, ngroups, S, n, out_samples, nullptr, nullptr, st);
   if (rc) return rc;
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(groups, ngroups, S, out_sched);

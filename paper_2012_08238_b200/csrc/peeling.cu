@@ -460,7 +460,7 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   SFFT_CHECK_LAUNCH("k_finalize");
   k_pe_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(a, groups, ngroups);
   SFFT_CHECK_LAUNCH("k_pe_groups");
-  int rc = run_union_smem(groups, ngroups, S, n, out_samples, nullptr, nullptr, st);
+  int rc = run_union_count(groups, ngroups, S, n, out_samples, nullptr, nullptr, st);
   if (rc) return rc;
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(groups, ngroups, S, out_sched);

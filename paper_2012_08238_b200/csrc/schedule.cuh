@@ -7,8 +7,8 @@
 // ladder, or the polish shifts 0/1/2; kind 2: an arithmetic shift set), a
 // spike group one (stride, tau):
 //   flat group g reads {sigma_g * t : t in U_g},  U_g = union_d [-tau-d, Omega-tau-d) mod n
-// and k_mark_count_smem counts |union of read indices| exactly from bitmaps
-// in shared memory.  No bookkeeping store touches HBM during the gathers.
+// and k_union_excl(_p2) counts |union of read indices| exactly by exclusion
+// (no bitmap).  No bookkeeping store touches HBM during the gathers.
 #pragma once
 
 #include "block.cuh"
@@ -156,78 +156,6 @@ static __global__ void k_zero_rows(int64_t* v, int S, const int32_t* gate, const
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S || (gate && !gate[s])) return;
   v[rows ? rows[s] : s] = 0;
-}
-
-// samples_read: CTA r of a finishing slot owns the index range
-// [r R, (r+1) R) as an R-bit map in shared memory, walks every read of the
-// slot's groups, sets the bits that fall in its range (shared atomics) and
-// popcounts its map; samples[row] accumulates the CTAs' counts.  No global
-// bitmap, no global atomics per read.
-constexpr int kMarkNT = 1024;
-constexpr int64_t kMarkBits = 176 * 1024 * 8;  // 176 KB of shared memory per CTA (N = 2^22: 3 CTAs)
-
-static __global__ void __launch_bounds__(kMarkNT) k_mark_count_smem(
-    const Group* __restrict__ groups, const int32_t* ngroups, int gstride, int64_t n,
-    const int32_t* gate, const int32_t* rows, unsigned long long* samples) {
-  extern __shared__ uint32_t mbits[];
-  __shared__ Group sg[kMaxGroups];
-  __shared__ GroupSh sp[kMaxGroups];
-  __shared__ unsigned long long red[32];
-  const int s = blockIdx.y;
-  if (gate && !gate[s]) return;
-  const int64_t r0 = (int64_t)blockIdx.x * kMarkBits;
-  if (r0 >= n) return;
-  const int64_t r1 = min(n, r0 + kMarkBits);
-  const int64_t words = (r1 - r0 + 31) / 32;
-  const int G = min(ngroups[s], kMaxGroups);
-  const Group* gs = groups + (int64_t)s * gstride;
-  const int64_t mask = (n & (n - 1)) == 0 ? n - 1 : -1;
-  for (int i = threadIdx.x; i < G; i += kMarkNT) sg[i] = gs[i];
-  for (int64_t w = threadIdx.x; w < words; w += kMarkNT) mbits[w] = 0u;
-  __syncthreads();
-  for (int i = threadIdx.x; i < G; i += kMarkNT) merge_pieces(sg[i], n, &sp[i]);
-  __syncthreads();
-  for (int g = 0; g < G; ++g) {
-    if (sg[g].kind == 0) {
-      // flat pieces [lo, hi) of u: e = sigma u mod n, advanced incrementally
-      const int64_t sig = sg[g].a;
-      const int64_t step = mulmod(sig, kMarkNT % n, n);
-      for (int i = 0; i < sp[g].np; ++i) {
-        const int64_t lo = sp[g].lo[i], hi = sp[g].hi[i];
-        int64_t u = lo + threadIdx.x;
-        if (u >= hi) continue;
-        int64_t e = mulmod(sig, u, n);
-        for (; u < hi; u += kMarkNT) {
-          if (e >= r0 && e < r1) {
-            const int64_t o = e - r0;
-            atomicOr(&mbits[o >> 5], 1u << (o & 31));
-          }
-          e += step;
-          e -= (e >= n) ? n : 0;
-        }
-      }
-      continue;
-    }
-    const int64_t tot = sp[g].total;
-    for (int64_t j = threadIdx.x; j < tot; j += kMarkNT) {
-      const int64_t e = group_elem(sg[g], sp[g], n, j, mask);
-      if (e >= r0 && e < r1) {
-        const int64_t o = e - r0;
-        atomicOr(&mbits[o >> 5], 1u << (o & 31));
-      }
-    }
-  }
-  __syncthreads();
-  unsigned long long c = 0;
-  for (int64_t w = threadIdx.x; w < words; w += kMarkNT) c += __popc(mbits[w]);
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < kMarkNT / 32; ++i) t += red[i];
-    if (t) atomicAdd(samples + (rows ? rows[s] : s), t);
-  }
 }
 
 // Is index e read by group g?  (The inverse of group_elem.)
@@ -415,40 +343,29 @@ static __global__ void k_union_gate(int S, const int32_t* gate, const int32_t* f
   if (s < S) out[s] = (!gate || gate[s]) && fallback[s];
 }
 
-// Scratch for run_union_smem's fallback gate: 2 ints per slot.
+// Scratch for run_union_count's fallback gate: 2 ints per slot.
 inline size_t union_scratch_bytes(int S) { return sizeof(int32_t) * 2 * (size_t)S; }
 
-inline int run_union_smem(const Group* groups, const int32_t* ngroups, int S, int64_t n,
+inline int run_union_count(const Group* groups, const int32_t* ngroups, int S, int64_t n,
                           int64_t* samples, const int32_t* gate, const int32_t* rows,
                           cudaStream_t st, int32_t* scratch = nullptr) {
   k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
   SFFT_CHECK_LAUNCH("k_zero_rows");
-  if (!getenv("SFFT_UNION_BITMAP")) {
-    const unsigned ctas = (unsigned)std::min<int64_t>(8, std::max<int64_t>(1, n >> 20));
-    const bool p2 = (n & (n - 1)) == 0 && n <= (int64_t(1) << 31) && scratch;
-    const int32_t* g2 = gate;
-    if (p2) {
-      SFFT_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int32_t) * S, st));
-      k_union_excl_p2<<<dim3(ctas, S), kUxNT, 0, st>>>(groups, ngroups, kMaxGroups, n, gate,
-                                                       rows, (unsigned long long*)samples,
-                                                       scratch);
-      SFFT_CHECK_LAUNCH("k_union_excl_p2");
-      k_union_gate<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(S, gate, scratch, scratch + S);
-      SFFT_CHECK_LAUNCH("k_union_gate");
-      g2 = scratch + S;
-    }
-    k_union_excl<<<dim3(ctas, S), kUxNT, 0, st>>>(groups, ngroups, kMaxGroups, n, g2, rows,
-                                                  (unsigned long long*)samples);
-    SFFT_CHECK_LAUNCH("k_union_excl");
-    return 0;
+  const unsigned ctas = (unsigned)std::min<int64_t>(8, std::max<int64_t>(1, n >> 20));
+  const bool p2 = (n & (n - 1)) == 0 && n <= (int64_t(1) << 31) && scratch;
+  const int32_t* g2 = gate;
+  if (p2) {
+    SFFT_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int32_t) * S, st));
+    k_union_excl_p2<<<dim3(ctas, S), kUxNT, 0, st>>>(groups, ngroups, kMaxGroups, n, gate, rows,
+                                                     (unsigned long long*)samples, scratch);
+    SFFT_CHECK_LAUNCH("k_union_excl_p2");
+    k_union_gate<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(S, gate, scratch, scratch + S);
+    SFFT_CHECK_LAUNCH("k_union_gate");
+    g2 = scratch + S;
   }
-  const size_t sm = (size_t)(std::min<int64_t>(n, kMarkBits) + 31) / 32 * sizeof(uint32_t);
-  SFFT_CUDA(cudaFuncSetAttribute(k_mark_count_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm));
-  dim3 g((unsigned)((n + kMarkBits - 1) / kMarkBits), S);
-  k_mark_count_smem<<<g, kMarkNT, sm, st>>>(groups, ngroups, kMaxGroups, n, gate, rows,
-                                            (unsigned long long*)samples);
-  SFFT_CHECK_LAUNCH("k_mark_count_smem");
+  k_union_excl<<<dim3(ctas, S), kUxNT, 0, st>>>(groups, ngroups, kMaxGroups, n, g2, rows,
+                                                (unsigned long long*)samples);
+  SFFT_CHECK_LAUNCH("k_union_excl");
   return 0;
 }
 

@@ -366,7 +366,7 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   k_vo_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(groups, ngroups, psig, ptau, S, R, omega,
                                                          pre_L, Bpre);
   SFFT_CHECK_LAUNCH("k_vo_groups");
-  rc = run_union_smem(groups, ngroups, S, n, out_samples, nullptr, nullptr, st,
+  rc = run_union_count(groups, ngroups, S, n, out_samples, nullptr, nullptr, st,
                       (int32_t*)(w + Lo.off[21]));
   if (rc) return rc;
   if (out_sched) {
