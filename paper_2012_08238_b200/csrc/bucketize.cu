@@ -397,7 +397,8 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
                                               int B2, int RG, const double2* __restrict__ W,
                                               const int32_t* item_sig, const int32_t* active,
                                               double2* __restrict__ out, int out_M,
-                                              int64_t out_S, const int32_t* item_active) {
+                                              int64_t out_S, const int32_t* item_active,
+                                              const int32_t* item_row) {
   extern __shared__ double2 sm[];
   const int item = blockIdx.y;
   if (item_active && !item_active[item]) return;
@@ -416,7 +417,8 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
   }
   __syncthreads();
   fft_dif(sm, RG, seg, P2, W, B, threadIdx.x, kNT);
-  const int64_t row = out_M > 0 ? (item % out_M) * out_S + item / out_M : item;
+  const int64_t row = item_row ? item_row[item]
+                                 : (out_M > 0 ? (item % out_M) * out_S + item / out_M : item);
   double2* o = out + row * B;
   const double bd = (double)B;
   for (int t = threadIdx.x; t < RG * B2; t += kNT) {
@@ -424,6 +426,32 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
     const int k1 = r0 + g;
     if (k1 >= B1) continue;
     o[k1 + (int64_t)B1 * k2] = cdivr(sm[g * seg + fft_pos(k2, P2)], bd);
+  }
+}
+
+// Four-step flat path, fold pass: the folded slots of every item, two per
+// thread (8 gathers in flight, rows in reference order), written to the item's
+// output row, which the column pass then reads coalesced (PROD_LOAD) before the
+// row pass overwrites it.  Small blocks and few registers keep many gathers in
+// flight per SM, which the column pass (86 registers, one block per SM) cannot.
+constexpr int kFrNT = 256;
+template <typename Tin>
+__global__ void __launch_bounds__(kFrNT) k_fold_rows(Prod p, double2* __restrict__ out) {
+  const int item = blockIdx.y;
+  const ItemCtx c = item_ctx<PROD_FLAT>(p, item, sizeof(Tin));
+  if (c.skip) return;
+  if (p.prof_items && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(p.prof_items, 1ull);
+  const int64_t s0 = (int64_t)blockIdx.x * 2 * kFrNT + threadIdx.x;
+  const int64_t s1 = s0 + kFrNT;
+  double2* o = out + out_row(p, item) * p.B;
+  if (s1 < p.B && c.c == 0) {
+    double2 a0, a1;
+    produce_flat2<Tin>(p, c, s0, c, s1, &a0, &a1);
+    o[s0] = a0;
+    o[s1] = a1;
+  } else {
+    if (s0 < p.B) o[s0] = produce<Tin, PROD_FLAT>(p, c, item, s0);
+    if (s1 < p.B) o[s1] = produce<Tin, PROD_FLAT>(p, c, item, s1);
   }
 }
 
@@ -442,7 +470,8 @@ __global__ void __launch_bounds__(256) k_dft_direct(const double2* __restrict__ 
                                                     const int32_t* item_sig,
                                                     const int32_t* active,
                                                     double2* __restrict__ out, int out_M,
-                                                    int64_t out_S, const int32_t* item_active) {
+                                                    int64_t out_S, const int32_t* item_active,
+                                                    const int32_t* item_row) {
   const int item = blockIdx.y;
   if (item_active && !item_active[item]) return;
   if (active) {
@@ -462,7 +491,8 @@ __global__ void __launch_bounds__(256) k_dft_direct(const double2* __restrict__ 
     e += k;
     if (e >= B) e -= B;
   }
-  const int64_t row = out_M > 0 ? (item % out_M) * out_S + item / out_M : item;
+  const int64_t row = item_row ? item_row[item]
+                                 : (out_M > 0 ? (item % out_M) * out_S + item / out_M : item);
   out[row * B + k] = cdivr(acc, (double)B);
 }
 
@@ -536,7 +566,7 @@ static bool cluster_disabled() {
 
 size_t bucketize_ws_bytes(int64_t B, int64_t nitems) {
   FftPlan P;
-  if (B <= kFusedMaxB && make_plan(B, &P)) return 0;
+  if (B <= 4096 && make_plan(B, &P)) return 0;  // flat B > 4096 takes the four-step path
   return (size_t)nitems * (size_t)B * sizeof(double2);
 }
 
@@ -546,13 +576,18 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
   if (nitems <= 0) return 0;
   const int64_t B = p.B;
   FftPlan P;
-  const int CL = cluster_size(B);
+  // flat windows with B > 4096: the fold pass + four-step FFT beats the
+  // 1024-slot cluster slices (env SFFT_FLAT_FOURSTEP_MIN overrides the bound)
+  static const int64_t fs_min =
+      getenv("SFFT_FLAT_FOURSTEP_MIN") ? atoll(getenv("SFFT_FLAT_FOURSTEP_MIN")) : 4097;
+  const bool four = MODE == PROD_FLAT && B >= fs_min;
+  const int CL = four ? 0 : cluster_size(B);
   if (CL > 1 && !cluster_disabled()) {
     if (CL == 8) return launch_cluster<Tin, MODE, 8>(p, nitems, W, out, st);
     if (CL == 4) return launch_cluster<Tin, MODE, 4>(p, nitems, W, out, st);
     return launch_cluster<Tin, MODE, 2>(p, nitems, W, out, st);
   }
-  if (B <= kFusedMaxB && make_plan(B, &P)) {
+  if (!four && B <= kFusedMaxB && make_plan(B, &P)) {
     const size_t sm = (size_t)B * sizeof(double2);
     if (ensure_smem(k_fused<Tin, MODE>, sm)) return -3;
     SFFT_CUDA(cudaFuncSetAttribute(k_fused<Tin, MODE>,
@@ -576,11 +611,23 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
     if (ensure_smem(k_cols<Tin, MODE>, smc)) return -3;
     if (ensure_smem(k_rows, smr)) return -3;
     dim3 gc((unsigned)cdiv_up(B2, CG), (unsigned)nitems);
-    k_cols<Tin, MODE><<<gc, kNT, smc, st>>>(p, P1, (int)B1, (int)B2, CG, W, z);
+    if (MODE == PROD_FLAT && !getenv("SFFT_NO_FOLD_ROWS")) {
+      // fold into the output rows, then the column pass from there
+      dim3 gf((unsigned)cdiv_up(B, 2 * kFrNT), (unsigned)nitems);
+      k_fold_rows<Tin><<<gf, kFrNT, 0, st>>>(p, out);
+      SFFT_CHECK_LAUNCH("k_fold_rows");
+      Prod pz = p;
+      pz.z = out;
+      pz.prof_items = nullptr;
+      if (ensure_smem(k_cols<Tin, PROD_LOAD>, smc)) return -3;
+      k_cols<Tin, PROD_LOAD><<<gc, kNT, smc, st>>>(pz, P1, (int)B1, (int)B2, CG, W, z);
+    } else {
+      k_cols<Tin, MODE><<<gc, kNT, smc, st>>>(p, P1, (int)B1, (int)B2, CG, W, z);
+    }
     SFFT_CHECK_LAUNCH("k_cols");
     dim3 gr((unsigned)cdiv_up(B1, RG), (unsigned)nitems);
     k_rows<<<gr, kNT, smr, st>>>(z, P2, (int)B1, (int)B2, RG, W, p.item_sig, p.active, out,
-                                 p.out_M, p.out_S, p.item_active);
+                                 p.out_M, p.out_S, p.item_active, p.item_row);
     SFFT_CHECK_LAUNCH("k_rows");
     return 0;
   }
@@ -588,7 +635,7 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
   k_slots<Tin, MODE><<<g, 256, 0, st>>>(p, z);
   SFFT_CHECK_LAUNCH("k_slots");
   k_dft_direct<<<g, 256, 0, st>>>(z, B, W, p.item_sig, p.active, out, p.out_M, p.out_S,
-                                  p.item_active);
+                                  p.item_active, p.item_row);
   SFFT_CHECK_LAUNCH("k_dft_direct");
   return 0;
 }

@@ -244,3 +244,24 @@ def test_row_cache_c3_default_gate(sb):
         assert err <= 1e-10, (rec["name"], err)
         assert (got.samples_read, got.iterations, got.converged) == \
             (rec["samples_read"], rec["iterations"], rec["converged"]), rec["name"]
+
+
+@pytest.mark.parametrize("row_cache", ["0", "1"])
+def test_iterative_four_step_b8192(sb, row_cache, monkeypatch):
+    """B = 8192 takes the fold pass + four-step FFT (outputs through the
+    per-item rows of the row cache when it is on), against the oracle."""
+    import torch
+    from oracle import sfft_oracle as O
+    monkeypatch.setenv("SFFT_ROW_CACHE", row_cache)
+    n, k = 1 << 18, 64
+    xs = [O.synth(n, k, 30.0, 700 + j)[0] for j in range(3)]
+    cfg = sb.AlgorithmConfig(framework="iterative", num_buckets=8192)
+    got = sb.run_iterative_batch(torch.as_tensor(np.stack(xs)).cuda(), k, cfg,
+                                 slots=2).to_results()
+    for x, res in zip(xs, got):
+        want = O.iterative(O.Access(x), k, O.Cfg(framework="iterative", num_buckets=8192))
+        assert set(res.spectrum.entries) == set(want.entries)
+        err = max(abs(res.spectrum.entries[f] - c) / abs(c) for f, c in want.entries.items())
+        assert err <= 1e-10
+        assert (res.samples_read, res.iterations, res.converged) == \
+            (want.samples_read, want.iterations, want.converged)
