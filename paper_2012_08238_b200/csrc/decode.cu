@@ -76,27 +76,14 @@ int run_floor(const double2* values, int64_t nsets, int64_t B, double mult,
 
 // Heavy bitmap of one round: the first `hc` eligible buckets in (-|v|, idx)
 // order.  bits[B/32 words].  One CTA per item.
-__global__ void __launch_bounds__(kFloorNT) k_heavy_bitmap(const double2* __restrict__ values,
-                                                           int64_t B, const double* thr,
-                                                           int64_t hc, const int32_t* item_sig,
-                                                           const int32_t* active,
-                                                           uint32_t* __restrict__ bits,
-                                                           int32_t* nheavy) {
-  constexpr int NT = kFloorNT;
-  __shared__ unsigned hist[256];
-  __shared__ long long sh[4];
-  __shared__ int redi[32];
-  const int item = blockIdx.x;
-  if (active) {
-    const int sig = item_sig ? item_sig[item] : item;
-    if (!active[sig]) return;
-  }
-  const double2* v = values + (int64_t)item * B;
+// Heavy bitmap of one set from its keys (|v| bits): the first hc eligible
+// buckets (|v| >= thr) in (-|v|, idx) order; *nheavy_out = their count.
+template <int NT, typename KeyF>
+__device__ void heavy_bits_k(KeyF key, int64_t B, double thr, int64_t hc, uint32_t* bw,
+                             int32_t* nheavy_out, unsigned* hist, long long* sh, int* redi) {
   const int64_t words = (B + 31) / 32;
-  uint32_t* bw = bits + (int64_t)item * words;
-  const double t = fmax(thr[item], 0.0);
+  const double t = fmax(thr, 0.0);
   const unsigned long long lo = dbits(t);
-  MagKey key{v};
   // eligible count
   int e = 0;
   for (int64_t i = threadIdx.x; i < B; i += NT) e += key(i) >= lo;
@@ -106,7 +93,7 @@ __global__ void __launch_bounds__(kFloorNT) k_heavy_bitmap(const double2* __rest
   if (E <= hc) {
     for (int64_t i = threadIdx.x; i < B; i += NT)
       if (key(i) >= lo) atomicOr(&bw[i >> 5], 1u << (i & 31));
-    if (threadIdx.x == 0 && nheavy) nheavy[item] = E;
+    if (threadIdx.x == 0 && nheavy_out) *nheavy_out = E;
     return;
   }
   // threshold: the (E-hc)-th smallest eligible key; above it all heavy, at it
@@ -132,7 +119,72 @@ __global__ void __launch_bounds__(kFloorNT) k_heavy_bitmap(const double2* __rest
     }
     if (h) atomicOr(&bw[i >> 5], 1u << (i & 31));
   }
-  if (threadIdx.x == 0 && nheavy) nheavy[item] = (int)hc;
+  if (threadIdx.x == 0 && nheavy_out) *nheavy_out = (int)hc;
+}
+
+__global__ void __launch_bounds__(kFloorNT) k_heavy_bitmap(const double2* __restrict__ values,
+                                                           int64_t B, const double* thr,
+                                                           int64_t hc, const int32_t* item_sig,
+                                                           const int32_t* active,
+                                                           uint32_t* __restrict__ bits,
+                                                           int32_t* nheavy) {
+  constexpr int NT = kFloorNT;
+  __shared__ unsigned hist[256];
+  __shared__ long long sh[4];
+  __shared__ int redi[32];
+  const int item = blockIdx.x;
+  if (active) {
+    const int sig = item_sig ? item_sig[item] : item;
+    if (!active[sig]) return;
+  }
+  const int64_t words = (B + 31) / 32;
+  heavy_bits_k<NT>(MagKey{values + (int64_t)item * B}, B, thr[item], hc,
+                   bits + (int64_t)item * words, nheavy ? nheavy + item : nullptr, hist, sh, redi);
+}
+
+// Floor (A8) and heavy bitmap (A9) of one set in one CTA from |v| bits cached
+// in shared memory (each |v| computed once instead of once per radix pass).
+__global__ void __launch_bounds__(kFloorBigNT) k_floor_heavy(const double2* __restrict__ values,
+                                                             int64_t B, double mult, int64_t hc,
+                                                             double* floor_out,
+                                                             uint32_t* __restrict__ bits,
+                                                             int32_t* nheavy) {
+  constexpr int NT = kFloorBigNT;
+  extern __shared__ unsigned long long fcache[];
+  __shared__ unsigned hist[256];
+  __shared__ long long sh[4];
+  __shared__ double redd[32];
+  __shared__ unsigned long long redu[32];
+  __shared__ int redi[32];
+  const int item = blockIdx.x;
+  const double2* v = values + (int64_t)item * B;
+  for (int64_t i = threadIdx.x; i < B; i += NT) fcache[i] = dbits(cabs_(v[i]));
+  __syncthreads();
+  double med, peak;
+  median_and_peak_k<NT>(SmemKey{fcache}, B, &med, &peak, hist, sh, redd, redu);
+  const double fl = fmax(fmax(fmin(mult * med, 0.25 * peak), 1e-9 * peak), 1e-300);
+  if (threadIdx.x == 0) floor_out[item] = fl;
+  const int64_t words = (B + 31) / 32;
+  heavy_bits_k<NT>(SmemKey{fcache}, B, fl, hc, bits + (int64_t)item * words,
+                   nheavy ? nheavy + item : nullptr, hist, sh, redi);
+}
+
+int run_floor_heavy(const double2* values, int64_t nsets, int64_t B, double mult, int64_t hc,
+                    double* floor_out, uint32_t* bits, int32_t* nheavy, cudaStream_t st) {
+  if (nsets <= 0) return 0;
+  // small sets: the two 256-thread kernels are faster than one 1024-thread CTA
+  if (B > kFloorCache || B < 4096) {
+    int rc = run_floor(values, nsets, B, mult, nullptr, nullptr, floor_out, nullptr, st);
+    return rc ? rc : run_heavy_bitmap(values, nsets, B, floor_out, hc, nullptr, nullptr, bits,
+                                      nheavy, st);
+  }
+  const size_t sm = (size_t)B * 8;
+  SFFT_CUDA(cudaFuncSetAttribute(k_floor_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sm ? sm : 1)));
+  k_floor_heavy<<<(unsigned)nsets, kFloorBigNT, sm, st>>>(values, B, mult, hc, floor_out, bits,
+                                                         nheavy);
+  SFFT_CHECK_LAUNCH("k_floor_heavy");
+  return 0;
 }
 
 int run_heavy_bitmap(const double2* values, int64_t nsets, int64_t B, const double* thr,

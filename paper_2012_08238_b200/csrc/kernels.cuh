@@ -76,6 +76,9 @@ int run_count_nonzero(const uint8_t* map, int64_t n, int64_t* out, cudaStream_t 
 int run_floor(const double2* values, int64_t nsets, int64_t B, double mult,
               const int32_t* item_sig, const int32_t* active, double* floor_out, double* peak_out,
               cudaStream_t st);
+// floor + heavy bitmap of each set in one kernel (|v| bits cached in shared memory)
+int run_floor_heavy(const double2* values, int64_t nsets, int64_t B, double mult, int64_t hc,
+                    double* floor_out, uint32_t* bits, int32_t* nheavy, cudaStream_t st);
 int run_heavy_bitmap(const double2* values, int64_t nsets, int64_t B, const double* thr,
                      int64_t hc, const int32_t* item_sig, const int32_t* active, uint32_t* bits,
                      int32_t* nheavy, cudaStream_t st);

@@ -299,9 +299,7 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   p.item_b = ptau;
   int rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)S * R, W, a.y, bws, bws_bytes, st);
   if (rc) return rc;
-  rc = run_floor(a.y, (int64_t)S * R, B, 3.0, nullptr, nullptr, thr, nullptr, st);
-  if (rc) return rc;
-  rc = run_heavy_bitmap(a.y, (int64_t)S * R, B, thr, 2 * k, nullptr, nullptr, bits, nullptr, st);
+  rc = run_floor_heavy(a.y, (int64_t)S * R, B, 3.0, 2 * k, thr, bits, nullptr, st);
   if (rc) return rc;
   VoteRounds vr;
   vr.bits = bits;
@@ -339,9 +337,7 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
     q.item_a = ptz;
     rc = run_bucketize(dtype, PROD_SPIKE, q, S, Wpre, py, bws, bws_bytes, st);
     if (rc) return rc;
-    rc = run_floor(py, S, Bpre, 3.0, nullptr, nullptr, pthr, nullptr, st);
-    if (rc) return rc;
-    rc = run_heavy_bitmap(py, S, Bpre, pthr, 2 * k, nullptr, nullptr, pbits, nullptr, st);
+    rc = run_floor_heavy(py, S, Bpre, 3.0, 2 * k, pthr, pbits, nullptr, st);
     if (rc) return rc;
     k_vo_prefilter<<<S, 256, 0, st>>>(a, pbits, Bpre);
     SFFT_CHECK_LAUNCH("k_vo_prefilter");
