@@ -611,7 +611,7 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
     if (ensure_smem(k_cols<Tin, MODE>, smc)) return -3;
     if (ensure_smem(k_rows, smr)) return -3;
     dim3 gc((unsigned)cdiv_up(B2, CG), (unsigned)nitems);
-    if (MODE == PROD_FLAT && !getenv("SFFT_NO_FOLD_ROWS")) {
+    if (MODE == PROD_FLAT) {
       // fold into the output rows, then the column pass from there
       dim3 gf((unsigned)cdiv_up(B, 2 * kFrNT), (unsigned)nitems);
       k_fold_rows<Tin><<<gf, kFrNT, 0, st>>>(p, out);
