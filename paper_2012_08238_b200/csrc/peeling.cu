@@ -66,7 +66,10 @@ struct Verdict {
 // distance (_nearest_candidate, reconstruct.py:136-140) is among the four
 // around (raw - b)/B; the reference distance formula and its tie rule (smaller
 // candidate) are applied to those.
-__device__ Verdict classify_one(const PeelArgs& a, int s, int j, int64_t b, int32_t* err) {
+// m_in (optional): the bucket's moments already in registers (the peel loop
+// just updated them), saving a dependent re-read.
+__device__ Verdict classify_one(const PeelArgs& a, int s, int j, int64_t b, int32_t* err,
+                                const double2* m_in = nullptr) {
   Verdict v{0, 0, cmk(0.0, 0.0)};
   const int ns = (int)a.sh[j];
   const int64_t n = a.n, B = a.Bs[j], L = a.p[j];
@@ -74,7 +77,7 @@ __device__ Verdict classify_one(const PeelArgs& a, int s, int j, int64_t b, int3
   double2 m[3];
   double sabs = 0.0;
   for (int t = 0; t < ns; ++t) {
-    m[t] = moment(a, j, s, t, b);
+    m[t] = m_in ? m_in[t] : moment(a, j, s, t, b);
     sabs += cabs_(m[t]);
   }
   if (sabs / ns < fl) return v;  // zero
@@ -183,15 +186,22 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget) {
   int nrec = 0;
   int64_t peels = 0;
   while (peels < budget) {
-    // pop the first still-single entry, verified tier first (all lanes agree)
+    // pop the first still-single entry, verified tier first (all lanes agree);
+    // the warp checks 32 queue entries per step instead of one
     int64_t g = -1;
     for (int tier = 0; tier < 2 && g < 0; ++tier) {
       while (head[tier] < tail[tier]) {
-        const int64_t e = q[tier][head[tier]++];
-        if (kind[e] == 1) {
-          g = e;
+        const int64_t at = head[tier] + lane;
+        const int64_t e = at < tail[tier] ? q[tier][at] : -1;
+        const bool single = e >= 0 && kind[e] == 1;
+        const unsigned hit = __ballot_sync(0xffffffffu, single);
+        if (hit) {
+          const int first = __ffs(hit) - 1;
+          g = __shfl_sync(0xffffffffu, e, first);
+          head[tier] += first + 1;
           break;
         }
+        head[tier] = (head[tier] + 32 < tail[tier]) ? head[tier] + 32 : tail[tier];
       }
     }
     if (g < 0) break;
@@ -227,11 +237,13 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget) {
     if (lane < a.nst) {
       const int j = lane;
       const int64_t b = f % a.Bs[j];
+      double2 mv[3];
       for (int t = 0; t < a.sh[j]; ++t) {
         double2* mp = a.meas + a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b;
-        *mp = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
+        mv[t] = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
+        *mp = mv[t];
       }
-      v = classify_one(a, s, j, b, a.err + s);
+      v = classify_one(a, s, j, b, a.err + s, mv);
       gi = a.boff[j] + b;
       kind[gi] = v.kind;
       cfs[gi] = v.f;
