@@ -238,7 +238,8 @@ constexpr int cluster_items() {
 
 template <typename Tin, int MODE, int CL, int M>
 __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
-    k_cluster(Prod p, int64_t nitems, const double2* __restrict__ W, double2* __restrict__ out) {
+    k_cluster(Prod p, int64_t nitems, const double2* __restrict__ W, double2* __restrict__ out,
+              int strided_off) {
   constexpr int NI = cluster_items<MODE, M>();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -265,46 +266,82 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
   for (int i = 0; i < NI; ++i) nl += s_live[i];
   if (nl == 0) return;  // uniform over the cluster (same items)
   if (p.prof_items && threadIdx.x == 0 && q == 0) atomicAdd(p.prof_items, (unsigned long long)nl);
-  // ---- fold: every slot of the NI items in turn, item pairs side by side, so
-  // the shifted measurements of one signal re-read their samples from L2
-  if (NI == 1 && MODE == PROD_FLAT && M % (2 * kClNT) == 0 && s_ctx[0].c == 0) {
-    // two slots per call, 8 gathers in flight
-    const ItemCtx c = s_ctx[0];
-    for (int j = threadIdx.x; j < M; j += 2 * kClNT)
-      produce_flat2<Tin>(p, c, (int64_t)q * M + j, c, (int64_t)q * M + j + kClNT, &a[j],
-                         &a[j + kClNT]);
-  } else {
-    for (int j = threadIdx.x; j < M; j += kClNT) {
-      const int64_t sl = (int64_t)q * M + j;
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-        if (s_live[i]) a[i * M + j] = produce<Tin, MODE>(p, s_ctx[i], (int)(item0 + i), sl);
-    }
-  }
-  cl.sync();
-  // ---- radix-CL stage over DSMEM: CTA q takes slots j in [q M/CL, (q+1) M/CL)
-  // of every CTA, forms the CL-point DFT over the CTAs and scatters output
-  // q' (times w_B^{j q'}) to CTA q' -- every folded value crosses the cluster
-  // once
   constexpr int NJ = M / CL;
-  for (int t = threadIdx.x; t < NI * NJ; t += kClNT) {
-    const int i = t / NJ;
-    const int j = q * NJ + (t - i * NJ);
-    double2 v[8];
-#pragma unroll
-    for (int r = 0; r < CL; ++r) v[r] = cl.map_shared_rank(a, r)[i * M + j];
-    if (CL == 8) {
-      dft8_(v);
-    } else if (CL == 4) {
-      dft4_(v[0], v[1], v[2], v[3]);
-    } else {
-      const double2 u = v[0];
-      v[0] = cadd(u, v[1]);
-      v[1] = csub(u, v[1]);
+  // ---- strided-ownership fold (flat gathers, one item): CTA q folds the
+  // slots n1 M + n2 for every n1 < CL and its own n2 slice [q NJ, (q+1) NJ),
+  // so the radix-CL stage over n1 is local; its CL outputs (times w_B^{n2 k1})
+  // go straight to CTA k1.  One cluster barrier instead of two, and every
+  // folded value crosses the cluster once.  Bit-identical to the pull form.
+  if (NI == 1 && MODE == PROD_FLAT && s_ctx[0].c == 0 && (M / 2) % kClNT == 0 &&
+      !strided_off) {
+    const ItemCtx c = s_ctx[0];
+    // local index j = n1 NJ + jj  ->  slot n1 M + q NJ + jj; pairs (j, j + M/2)
+    for (int j = threadIdx.x; j < M / 2; j += kClNT) {
+      const int j2 = j + M / 2;
+      const int64_t s0 = (int64_t)(j / NJ) * M + q * NJ + (j % NJ);
+      const int64_t s1 = (int64_t)(j2 / NJ) * M + q * NJ + (j2 % NJ);
+      produce_flat2<Tin>(p, c, s0, c, s1, &a[j], &a[j2]);
     }
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < NJ; jj += kClNT) {
+      const int n2 = q * NJ + jj;
+      double2 v[8];
 #pragma unroll
-    for (int r = 0; r < CL; ++r)
-      cl.map_shared_rank(bq, r)[i * M + j] = (j * r) ? cmul(v[r], __ldg(W + j * r)) : v[r];
+      for (int r = 0; r < CL; ++r) v[r] = a[r * NJ + jj];
+      if (CL == 8) {
+        dft8_(v);
+      } else if (CL == 4) {
+        dft4_(v[0], v[1], v[2], v[3]);
+      } else {
+        const double2 u = v[0];
+        v[0] = cadd(u, v[1]);
+        v[1] = csub(u, v[1]);
+      }
+#pragma unroll
+      for (int r = 0; r < CL; ++r)
+        cl.map_shared_rank(bq, r)[n2] = (n2 * r) ? cmul(v[r], __ldg(W + n2 * r)) : v[r];
+    }
+  } else {
+    // ---- fold: every slot of the NI items in turn, item pairs side by side, so
+    // the shifted measurements of one signal re-read their samples from L2
+    if (NI == 1 && MODE == PROD_FLAT && M % (2 * kClNT) == 0 && s_ctx[0].c == 0) {
+      // two slots per call, 8 gathers in flight
+      const ItemCtx c = s_ctx[0];
+      for (int j = threadIdx.x; j < M; j += 2 * kClNT)
+        produce_flat2<Tin>(p, c, (int64_t)q * M + j, c, (int64_t)q * M + j + kClNT, &a[j],
+                           &a[j + kClNT]);
+    } else {
+      for (int j = threadIdx.x; j < M; j += kClNT) {
+        const int64_t sl = (int64_t)q * M + j;
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+          if (s_live[i]) a[i * M + j] = produce<Tin, MODE>(p, s_ctx[i], (int)(item0 + i), sl);
+      }
+    }
+    cl.sync();
+    // ---- radix-CL stage over DSMEM: CTA q takes slots j in [q M/CL, (q+1) M/CL)
+    // of every CTA, forms the CL-point DFT over the CTAs and scatters output
+    // q' (times w_B^{j q'}) to CTA q' -- every folded value crosses the cluster
+    // once
+    for (int t = threadIdx.x; t < NI * NJ; t += kClNT) {
+      const int i = t / NJ;
+      const int j = q * NJ + (t - i * NJ);
+      double2 v[8];
+#pragma unroll
+      for (int r = 0; r < CL; ++r) v[r] = cl.map_shared_rank(a, r)[i * M + j];
+      if (CL == 8) {
+        dft8_(v);
+      } else if (CL == 4) {
+        dft4_(v[0], v[1], v[2], v[3]);
+      } else {
+        const double2 u = v[0];
+        v[0] = cadd(u, v[1]);
+        v[1] = csub(u, v[1]);
+      }
+#pragma unroll
+      for (int r = 0; r < CL; ++r)
+        cl.map_shared_rank(bq, r)[i * M + j] = (j * r) ? cmul(v[r], __ldg(W + j * r)) : v[r];
+    }
   }
   cl.sync();  // all slices scattered (and all remote reads of a done)
   // ---- NI sub-transforms of length M
@@ -336,7 +373,8 @@ static int launch_cluster_m(const Prod& p, int64_t nitems, const double2* W, dou
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, p, nitems, W, out));
+  static const int strided_off = getenv("SFFT_NO_STRIDED_FOLD") ? 1 : 0;
+  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, p, nitems, W, out, strided_off));
   SFFT_CHECK_LAUNCH("k_cluster");
   return 0;
 }
