@@ -1169,6 +1169,29 @@ __global__ void __launch_bounds__(kMrgNT) k_it_merge(IterArgs a) {
 }
 
 // ------------------------------------------------------------------ residual test
+// Residual convergence test, early out (frameworks.py:562-565): the test is
+// max_b |y0 - model(found)| < 1.3 floor, so one bucket at or above the bound
+// decides "not converged".  The residual at the first kResPre heavy buckets is
+// formed exactly as the full pass forms it (the candidate-restricted
+// subtraction is bitwise equal at those buckets); a witness clears the slot's
+// gate and skips its full-B pass (non-converging signals find a witness at
+// once).  Padded entries use bucket 0, whose residual is as valid a witness.
+constexpr int kResPre = 32;
+
+__global__ void k_resid_list(IterArgs a, int32_t* plist) {
+  const int s = blockIdx.x, i = threadIdx.x;
+  if (!a.gate[s] || i >= kResPre) return;
+  plist[(int64_t)s * kResPre + i] = i < a.st[s].nheavy ? a.heavy[(int64_t)s * a.B + i] : 0;
+}
+
+__global__ void k_resid_pre(IterArgs a, const double2* rpre) {
+  const int s = blockIdx.x, i = threadIdx.x;
+  if (!a.gate[s]) return;
+  const bool witness = i < kResPre &&
+                       cabs_(rpre[(int64_t)s * kResPre + i]) >= 1.3 * a.st[s].floor;
+  if (__any_sync(0xffffffffu, witness) && i == 0) a.gate[s] = 0;
+}
+
 __global__ void __launch_bounds__(kDecNT) k_it_resid(IterArgs a) {
   __shared__ double redd[32];
   const int s = blockIdx.x;
@@ -1410,6 +1433,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)(S + 1),                        // 41 cnt
       sizeof(int32_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 42 it2_sig + it2_row
       sizeof(int64_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 43 it2_sigma + it2_tau
+      sizeof(double2) * (size_t)S * kResPre,                    // 44 residual pre-check values
+      sizeof(int32_t) * (size_t)S * kResPre,                    // 45 residual pre-check buckets
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1601,6 +1626,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.it2_row = a.it2_sig + (size_t)S * (M + spec_rows(M));
   a.it2_sigma = (int64_t*)(w + Lo.off[43]);
   a.it2_tau = a.it2_sigma + (size_t)S * (M + spec_rows(M));
+  double2* rpre = (double2*)(w + Lo.off[44]);
+  int32_t* rlist = (int32_t*)(w + Lo.off[45]);
   RealTab rt{};
   if (real_table_ok(omega)) {
     rt.at = (const double*)(w + Lo.off[37]);
@@ -1759,6 +1786,16 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     }
     k_it_merge<<<S, kMrgNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_merge");
+    if (loc == 0) {
+      k_resid_list<<<S, 32, 0, st>>>(a, rlist);
+      SFFT_CHECK_LAUNCH("k_resid_list");
+      rc = run_subtract_gated(a.y, rpre, B, kResPre, rlist, S, gt, n, nullptr, a.item_sigma,
+                              a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
+                              splits(h_max, 128, kMaxSubSplit), a.part, &rt);
+      if (rc) return rc;
+      k_resid_pre<<<S, 32, 0, st>>>(a, rpre);
+      SFFT_CHECK_LAUNCH("k_resid_pre");
+    }
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
                             splits(h_max, 128, kMaxSubSplit), a.part, &rt);
