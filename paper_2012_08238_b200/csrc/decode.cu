@@ -587,7 +587,8 @@ int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, 
   } else {
     SFFT_CUDA(cudaFuncSetAttribute(k_vote_collect<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sm ? sm : 1)));
-    const unsigned gx = (unsigned)std::min<int64_t>(cdiv_up(vr.n, 256), 1024);
+    // >= 16 positions per thread: the per-block bitmap copy is amortised
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv_up(vr.n, 256 * 16), 1024));
     k_vote_collect<0><<<dim3(gx, S), 256, sm, st>>>(vr, fv, need, hc, hl, nh, sinv, cnt, buf);
     SFFT_CHECK_LAUNCH("k_vote_collect<scan>");
   }
