@@ -333,7 +333,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": traffic, "traffic_unit": "DRAM bytes per item (ncu)",
-                         "kernel": "k_cluster<float2,FLAT,8,512> (gather+window+fold, DSMEM radix-8 exchange, radix-8 FFT_512)",
+                         "kernel": "k_cluster<float2,FLAT,8,512> (gather+window+fold with strided slot ownership, local radix-8 + one DSMEM push, radix-8 FFT_512)",
                          "bytes_per_item": item_bytes, "items": pi.value,
                          "launches": pl.value, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / ms if ms else None},
