@@ -31,6 +31,10 @@
 #include "schedule.cuh"
 #include "finalize.cuh"
 
+#ifndef SFFT_SPEC_POLISH
+#define SFFT_SPEC_POLISH 5
+#endif
+
 namespace sfft {
 
 enum SlotPhase { PH_FREE = 0, PH_LOOP = 1, PH_POLISH = 2, PH_FINISH = 3, PH_IDLE = 4 };
@@ -1373,9 +1377,10 @@ static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int kMaxSubSplit = 16;   // tone splits of the full-B subtraction
 constexpr int kMaxLadSplit = 8;    // tone splits of the ladder model
 
-// cached rows per slot: the next loop permutation's M shifts and 6 x 3 polish
-// shifts (phase-location ladders only, M <= 13)
-static int spec_rows(int M) { return M <= 13 ? M + 18 : 0; }
+// cached rows per slot: the next loop permutation's M shifts and kSpecPolish x 3
+// polish shifts (phase-location ladders only, M <= 13)
+constexpr int kSpecPolish = SFFT_SPEC_POLISH;
+static int spec_rows(int M) { return M <= 13 ? M + 3 * kSpecPolish : 0; }
 
 static int ht_size(int cap) {
   int h = 1;
