@@ -51,6 +51,9 @@ def parse():
     return ap.parse_args()
 
 
+GATHER_CEILING = 202e9  # gathers/s, marginal rate of k_cluster (support sweep)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -337,6 +340,16 @@ def main():
                          "bytes_per_item": item_bytes, "items": pi.value,
                          "launches": pl.value, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / ms if ms else None},
+            # the bound the gather-fold actually runs against: one L1TEX wavefront
+            # (a 128-byte line) per random 8-byte sample; ceiling = the marginal
+            # gather rate of the window-support sweep (profiles/r1_gather_bound_microbench.txt)
+            "gather_bound": {"achieved_gathers_per_s": (pi.value * omega) / (kern_ms * 1e-3)
+                             if kern_ms > 0 else None,
+                             "ceiling_gathers_per_s": GATHER_CEILING,
+                             "frac": (pi.value * omega) / (kern_ms * 1e-3) / GATHER_CEILING
+                             if kern_ms > 0 else None,
+                             "ceiling_source": "profiles/r1_gather_bound_microbench.txt (4.96 ps "
+                                               "per gather, k_cluster support sweep)"},
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": launches,
