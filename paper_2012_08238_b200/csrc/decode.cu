@@ -704,7 +704,7 @@ __device__ __forceinline__ int sub_splits(int64_t T, int maxTS) {
 }
 
 template <bool REAL>
-__global__ void __launch_bounds__(kSubNT) k_subtract(
+__global__ void __launch_bounds__(kSubNT, 4) k_subtract(
     const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
     const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
     const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
