@@ -572,20 +572,30 @@ __device__ __forceinline__ void ladder_model_real(const IterArgs& a, int s, int 
 #pragma unroll
   for (int j = 0; j < M; ++j) S[j] = cmk(0.0, 0.0);
   if (threadIdx.x < M) s_al[threadIdx.x] = cmk(0.0, 0.0);
+  // per-tone quantities once per tone (m, w^{-m h}, table row), then the
+  // per-(tone, shift) factors from them: the same values as forming each
+  // (tone, shift) entry from scratch, with one sincos per tone fewer per shift
+  __shared__ int64_t u_m[kLocChunk];
+  __shared__ double2 u_wmh[kLocChunk], u_c[kLocChunk];
   for (int64_t t0 = tb; t0 < te; t0 += kLocChunk) {
+    __syncthreads();
+    for (int tt = threadIdx.x; tt < kLocChunk; tt += kLocNT) {
+      if (t0 + tt >= te) continue;
+      const int64_t m = mulmod(sigma, pmod(rp[t0 + tt], n), n);
+      u_m[tt] = m;
+      u_wmh[tt] = unit_root(n, pmod(-mulmod(m, hh, n), n));
+      u_c[tt] = rc[t0 + tt];
+      t_row[tt] = (L - m % L) % L;
+      t_q[tt] = (m + L - 1) / L;
+    }
     __syncthreads();
     for (int q = threadIdx.x; q < kLocChunk * M; q += kLocNT) {
       const int tt = q / M, j = q - tt * M;
       if (t0 + tt >= te || j == 0) continue;
-      const int64_t m = mulmod(sigma, pmod(rp[t0 + tt], n), n);
       const int64_t tj = pmod(tau + a.ladder[j - 1], n);
-      const double2 cp = cmul(rc[t0 + tt], unit_root(n, mulmod(tj, m, n)));
-      t_be[tt][j] = cscale(cmul(cp, unit_root(n, pmod(-mulmod(m, hh, n), n))), invB);
+      const double2 cp = cmul(u_c[tt], unit_root(n, mulmod(tj, u_m[tt], n)));
+      t_be[tt][j] = cscale(cmul(cp, u_wmh[tt]), invB);
       t_al[tt][j] = cscale(cp, t0v * invB);
-      if (j == 1) {
-        t_row[tt] = (L - m % L) % L;
-        t_q[tt] = (m + L - 1) / L;
-      }
     }
     __syncthreads();
     const int tn = (int)((te - t0 < kLocChunk) ? te - t0 : kLocChunk);
