@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kDecNT) k_it_decide(IterArgs a) {
 
 // ------------------------------------------------------------------ locate
 constexpr int kLocNT = 128;
-constexpr int kLocChunk = 32;
+constexpr int kLocChunk = 64;
 
 // Sum of the recovered model over tones [tb, te) at heavy bucket b for the
 // ladder shifts j = 1..M-1, subtracted from ys[] (running, in tone order).
