@@ -1259,7 +1259,7 @@ __global__ void k_po_after(IterArgs a) {
   }
 }
 
-constexpr int kPoNT = 64;
+constexpr int kPoNT = 128;
 constexpr int kPoChunk = 128;
 
 // Occupancy of the buckets of every recovered tone under this pass's
