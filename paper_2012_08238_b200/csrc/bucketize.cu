@@ -173,14 +173,43 @@ __device__ __forceinline__ void produce_flat2(const Prod& p, const ItemCtx& ca, 
     ia = ia3 + ca.step; ia -= (ia >= n) ? n : 0;
     ib = ib3 + cb.step; ib -= (ib >= n) ? n : 0;
   }
-  for (; i < p.omega; i += B) {
+  // tails (slot a: at most 4 rows left, slot b: at most 3): every load in
+  // flight at once, then the adds in row order
+  Tin ta[4], tb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (i + u * B < p.omega) ta[u] = __ldcg(xa + ia);
+    if (k + u * B < p.omega) tb[u] = __ldcg(xb + ib);
+    ia += ca.step;
+    ia -= (ia >= n) ? n : 0;
+    ib += cb.step;
+    ib -= (ib >= n) ? n : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (i + u * B < p.omega) {
+      const double2 v = to_d2_(ta[u]);
+      const double g = __ldg(p.taps + i + u * B);
+      aa = cadd_rn(aa, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (k + u * B < p.omega) {
+      const double2 v = to_d2_(tb[u]);
+      const double g = __ldg(p.taps + k + u * B);
+      ab = cadd_rn(ab, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
+    }
+  }
+  // rows beyond those (only when s1 - s0 >= B; no caller does that)
+  for (i += 4 * B; i < p.omega; i += B) {
     const double2 v = Sample<Tin>::load(xa, ia);
     const double g = __ldg(p.taps + i);
     aa = cadd_rn(aa, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
     ia += ca.step;
     ia -= (ia >= n) ? n : 0;
   }
-  for (; k < p.omega; k += B) {
+  for (k += 4 * B; k < p.omega; k += B) {
     const double2 v = Sample<Tin>::load(xb, ib);
     const double g = __ldg(p.taps + k);
     ab = cadd_rn(ab, cmk(__dmul_rn(g, v.x), __dmul_rn(g, v.y)));
