@@ -101,3 +101,14 @@ def test_oneshot_k0_and_errors(sb):
                                                                  num_buckets=48))
     with pytest.raises(sb.ConfigMismatch):
         sb.run_oneshot(sb.TimeSignal(x), 4, sb.AlgorithmConfig(framework="voting"))
+
+
+def test_oneshot_device_limits(sb):
+    """a_max above the device limit (8) or too many shifts raise
+    InvalidParameter before any sample is read."""
+    x = sb.TimeSignal(np.zeros(4096, dtype=np.complex128))
+    with pytest.raises(sb.InvalidParameter):
+        sb.run_oneshot(x, 4, sb.AlgorithmConfig(framework="one_shot", a_max=9))
+    with pytest.raises(sb.InvalidParameter):
+        sb.run_oneshot(x, 4, sb.AlgorithmConfig(framework="one_shot", pursuit_shifts=80))
+    assert x.access_count == 0
