@@ -51,7 +51,9 @@ def parse():
     return ap.parse_args()
 
 
-GATHER_CEILING = 202e9  # gathers/s, marginal rate of k_cluster (support sweep)
+KERNEL_DESC = ("bucketization launches of the step: k_run_fold (one gather per sample of a "
+               "(signal, sigma) run, every shift folded from the thread's shared-memory column) "
+               "+ the in-place cluster FFT pass k_cluster<PROD_LOAD,8,512>")
 
 
 def peaks():
@@ -65,21 +67,32 @@ def peaks():
 
 # ------------------------------------------------------------------ CPU side
 
-def _cpu_worker(seed):
+def _cpu_worker(args):
+    seed, memo = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import functools
+
     import numpy as np
     from oracle import sfft_oracle as O
+    if memo and not hasattr(O.flat_window, "cache_info"):
+        # the reference builds the filter inside every runner call
+        # (sfft/frameworks.py:457); "memo" times the path with it cached
+        O.flat_window = functools.lru_cache(maxsize=4)(O.flat_window)
+        O.flat_window(N, B)
     mags = 10 ** np.random.default_rng(seed + 1000).uniform(0, 1, K)
     x, _ = O.synth(N, K, SNR_DB, seed, magnitudes=mags)
     cfg = O.Cfg(framework="iterative", num_buckets=B, max_iterations=10)
     t0 = time.perf_counter()
     out = O.iterative(O.Access(x), K, cfg)
-    return time.perf_counter() - t0, len(out.entries)
+    dt = time.perf_counter() - t0
+    return dt, (dict(out.entries), out.samples_read, out.iterations, out.converged)
 
 
-def cpu_baseline(nsig: int):
+def cpu_baseline(nsig: int, memo: bool = False, want_results: bool = False):
     """Oracle port of the reference CPU path, one single-threaded process per
-    host core; throughput = transforms / (summed CPU seconds / workers)."""
+    host core; throughput = transforms / (summed per-transform CPU seconds /
+    workers) -- conservative against wall time, which also counts signal
+    generation and process start-up (reported in ``sample``)."""
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
     nsig = nsig or min(cores, 32)
@@ -91,7 +104,7 @@ def cpu_baseline(nsig: int):
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, list(range(nsig)))
+        res = pool.map(_cpu_worker, [(i, memo) for i in range(nsig)], chunksize=1)
     wall = time.perf_counter() - t0
     for k, v in env_old.items():
         if v is None:
@@ -100,11 +113,45 @@ def cpu_baseline(nsig: int):
             os.environ[k] = v
     secs = [r[0] for r in res]
     value = nsig / (sum(secs) / workers)
-    return {"value": value, "unit": "transforms/s", "cores": workers,
-            "kind": "port",
-            "sample": f"{nsig} seeded C3 signals (gen_signal restatement), oracle iterative runner, "
-                      f"{workers} single-threaded numpy processes; median {statistics.median(secs):.2f} "
-                      f"s/transform; wall {wall:.1f} s incl. generation"}
+    out = {"value": value, "unit": "transforms/s", "cores": workers,
+           "kind": "port",
+           "sample": f"{nsig} seeded C3 signals (seeds 0..{nsig - 1}, exact gen_signal "
+                     f"restatement, complex128), oracle iterative runner "
+                     f"{'with the filter cached (D13)' if memo else 'as-is (filter built per call)'}, "
+                     f"{workers} single-threaded numpy processes; median "
+                     f"{statistics.median(secs):.2f} s/transform; wall {wall:.1f} s incl. "
+                     f"generation; rate = transforms / (summed transform seconds / workers)"}
+    if want_results:
+        return out, [r[1] for r in res]
+    return out
+
+
+def gpu_parity(sb, cfg, results, dev):
+    """The CPU-baseline signals (exact gen_signal inputs, complex128) through
+    the GPU arm in complex64 (rounded once), against the oracle's results on
+    the unrounded signals: the north_star criterion (identical support,
+    values within 1e-4) plus identical samples_read / iterations / converged."""
+    import numpy as np
+    import torch
+    from oracle import sfft_oracle as O
+    xs = []
+    for seed in range(len(results)):
+        mags = 10 ** np.random.default_rng(seed + 1000).uniform(0, 1, K)
+        xs.append(O.synth(N, K, SNR_DB, seed, magnitudes=mags)[0])
+    X = torch.as_tensor(np.stack(xs)).to(torch.complex64).to(dev)
+    got = sb.run_iterative_batch(X, K, cfg).to_results()
+    same_support, diag, err = 0, 0, 0.0
+    for g, (ent, smp, its, conv) in zip(got, results):
+        e = g.spectrum.entries
+        if set(e) == set(ent):
+            same_support += 1
+            if ent:
+                err = max(err, max(abs(e[f] - c) / abs(c) for f, c in ent.items()))
+        diag += (g.samples_read, g.iterations, g.converged) == (smp, its, conv)
+    return {"signals": len(results), "support_identical": same_support,
+            "diagnostics_identical": diag, "max_rel_err": err, "tol": 1e-4,
+            "inputs": "the cpu_baseline seeds (exact gen_signal), complex64 on the GPU vs "
+                      "complex128 oracle"}
 
 
 def run_reference(args):
@@ -266,10 +313,13 @@ def main():
     conv = sum(r.converged for r in res)
     exact = sum(len(r.spectrum.entries) == K for r in res)
 
-    # roofline of the gather-fold-FFT kernel: algorithmic bytes per item =
-    # Omega gathered complex64 samples + B complex128 bucket values written
+    # roofline of the bucketization (gather-fold + FFT) launches: algorithmic
+    # bytes per item as SURVEY §8(d) defines them, Omega*s + B*s with s = 8
+    # (complex64); the bucket values are stored as complex128 (B*16), which is
+    # also reported
     omega = sb.default_flat_support(N, B)
-    item_bytes = omega * 8 + B * 16
+    item_bytes = omega * 8 + B * 8
+    item_bytes_c128_out = omega * 8 + B * 16
     kern_ms = pm.value
     achieved = (pi.value * item_bytes) / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
     peak, peak_kind = peaks()
@@ -319,14 +369,62 @@ def main():
         torch.cuda.synchronize()
         ems, etot = combine(a0.elapsed_time(a1), Se * args.steps, dev)
         d2h = sum(t.numel() * t.element_size() for t in host)
+        # the streamed results must be the resident batch's, row for row
+        ref_rows = (br.pos[:Se].cpu(), br.coef[:Se].cpu(), br.count[:Se].cpu(),
+                    br.iterations[:Se].cpu(), br.converged[:Se].cpu(),
+                    br.samples_read[:Se].cpu())
+        same = all(torch.equal(a, b) for a, b in zip(host, ref_rows))
         e2e = {"value": etot / (ems * 1e-3), "unit": "transforms/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / args.steps,
-               "path": "run_iterative_stream (pinned host rows, H2D overlapped with compute)"}
+               "path": "run_iterative_stream (pinned host rows, H2D overlapped with compute)",
+               "identical_to_resident": bool(same)}
+        del Xh, Xd
+        torch.cuda.empty_cache()
+
+    # ---- single-signal drop-in latency through the public API (host numpy
+    # signal -> TimeSignal upload -> run_algorithm -> RecoveryResult), the
+    # call a reference user makes after plugin.install()
+    dropin = None
+    if rank == 0 and not args.no_e2e:
+        x1 = X[0].cpu().numpy()
+        lat = []
+        for i in range(6):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r1 = sb.run_algorithm(sb.TimeSignal(x1, dtype="complex64"), K, cfg)
+            lat.append(time.perf_counter() - t0)
+        dropin = {"ms_median": 1e3 * statistics.median(lat[1:]), "samples": len(lat) - 1,
+                  "path": "run_algorithm(TimeSignal(host c64 signal)) -> RecoveryResult, "
+                          "one C3 transform, upload + result conversion included",
+                  "entries": len(r1.spectrum.entries)}
+
+    # ---- complex128 input mode (the reference's dtype), same workload
+    c128 = None
+    if rank == 0 and not args.no_e2e:
+        S2 = min(S, 512)
+        X2 = X[:S2].to(torch.complex128)
+        step2 = lambda: sb.run_iterative_batch(X2, K, cfg, slots=min(args.slots, S2))
+        step2()
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(st)
+        for _ in range(2):
+            step2()
+        b1.record(st)
+        torch.cuda.synchronize()
+        c128 = {"value": 2 * S2 / (b0.elapsed_time(b1) * 1e-3), "unit": "transforms/s",
+                "signals": S2, "note": "same signals widened to complex128 (16-byte gathers)"}
+        del X2
 
     cb = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cb = cpu_baseline(args.cpu_sample)
+        cb, results = cpu_baseline(args.cpu_sample, want_results=True)
+        cbm = cpu_baseline(args.cpu_sample, memo=True)
+        cb["value_filter_cached"] = cbm["value"]
+        cb["sample_filter_cached"] = cbm["sample"]
+        parity = gpu_parity(sb, cfg, results, dev)
 
     if rank == 0:
         line = {
@@ -341,22 +439,19 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": traffic, "traffic_unit": "DRAM bytes per item (ncu)",
-                         "kernel": "k_cluster<float2,FLAT,8,512> (gather+window+fold with strided slot ownership, local radix-8 + one DSMEM push, radix-8 FFT_512)",
-                         "bytes_per_item": item_bytes, "items": pi.value,
+                         "kernel": KERNEL_DESC,
+                         "bytes_per_item": item_bytes,
+                         "bytes_per_item_def": "SURVEY 8(d): Omega*8 gathered + B*8 buckets (c64)",
+                         "frac_c128_outputs": (pi.value * item_bytes_c128_out) /
+                         (kern_ms * 1e-3) / 1e9 / peak if kern_ms > 0 else None,
+                         "items": pi.value,
                          "launches": pl.value, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / ms if ms else None},
-            # the bound the gather-fold actually runs against: one L1TEX wavefront
-            # (a 128-byte line) per random 8-byte sample; ceiling = the marginal
-            # gather rate of the window-support sweep (profiles/r1_gather_bound_microbench.txt)
-            "gather_bound": {"achieved_gathers_per_s": (pi.value * omega) / (kern_ms * 1e-3)
-                             if kern_ms > 0 else None,
-                             "ceiling_gathers_per_s": GATHER_CEILING,
-                             "frac": (pi.value * omega) / (kern_ms * 1e-3) / GATHER_CEILING
-                             if kern_ms > 0 else None,
-                             "ceiling_source": "profiles/r1_gather_bound_microbench.txt (4.96 ps "
-                                               "per gather, k_cluster support sweep)"},
             "cpu_baseline": cb,
+            "parity": parity,
             "e2e": e2e,
+            "dropin_latency": dropin,
+            "c128": c128,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "check": {"converged": conv, "with_k_entries": exact, "signals": S},

@@ -304,6 +304,9 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
   if (NI == 1 && MODE == PROD_FLAT && s_ctx[0].c == 0 && (M / 2) % kClNT == 0 &&
       !strided_off) {
     const ItemCtx c = s_ctx[0];
+    // every CTA of the cluster must have started before any DSMEM access: a
+    // relaxed arrive now, its wait after the fold (overlapped with the gathers)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     // local index j = n1 NJ + jj  ->  slot n1 M + q NJ + jj; pairs (j, j + M/2)
     for (int j = threadIdx.x; j < M / 2; j += kClNT) {
       const int j2 = j + M / 2;
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
       produce_flat2<Tin>(p, c, s0, c, s1, &a[j], &a[j2]);
     }
     __syncthreads();
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     for (int jj = threadIdx.x; jj < NJ; jj += kClNT) {
       const int n2 = q * NJ + jj;
       double2 v[8];
@@ -519,6 +523,136 @@ __global__ void __launch_bounds__(kFrNT) k_fold_rows(Prod p, double2* __restrict
   } else {
     if (s0 < p.B) o[s0] = produce<Tin, PROD_FLAT>(p, c, item, s0);
     if (s1 < p.B) o[s1] = produce<Tin, PROD_FLAT>(p, c, item, s1);
+  }
+}
+
+// ---- permutation runs: the shifted measurements of one (signal, sigma) share
+// their samples.  Item j of a run reads x[sigma (s + rB - tau_j)] for slot s,
+// row r; with tau_j = tau_0 + a_j B + c_j (0 <= c_j < B) and column
+// col = (s - c_j) mod B that is U[col + (r - o_j) B], U[u] = x[sigma (u - tau_0)],
+// o_j = a_j + (col + c_j >= B).  So one thread owns one column: it gathers the
+// column's rows v in [-max o_j, R) ONCE into its private shared-memory column
+// and folds every item of the run from there (virtual slot s_j = col + c_j
+// mod B, taps g[s_j + rB], rows in reference order, no FMA contraction, so
+// bit-identical to the per-item fold).  Items too far back for the window
+// (o_j > wrows - R) are folded by the per-item path, slot = col.  The ladder
+// of a C3 loop iteration (shifts 0,1,8,64,512,4096,32768) gathers 27 rows per
+// column instead of 7 x 19, the polish shifts (0,1,2) 20 instead of 57.
+// Folded slots go to each item's output row; the in-place FFT pass follows.
+constexpr int kRfNT = 256;
+constexpr int kRfMaxBack = 8;  // window reaches at most this many rows back
+constexpr int kRfT = 22;       // tap registers: items of up to kRfT - 1 rows share them
+
+template <typename Tin>
+__global__ void __launch_bounds__(kRfNT, 3)
+    k_run_fold(Prod p, const int32_t* __restrict__ run_first, const int32_t* __restrict__ run_cnt,
+               int wrows, double2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char rf_smem[];
+  Tin* V = reinterpret_cast<Tin*>(rf_smem);  // [wrows][kRfNT], column = thread
+  const int run = blockIdx.y;
+  const int rfirst = run_first[run], rcnt = run_cnt[run];
+  if (p.prof_items && threadIdx.x == 0 && blockIdx.x == 0)
+    atomicAdd(p.prof_items, (unsigned long long)rcnt);
+  // B, Omega < 2^31 (launcher); index arithmetic mod n stays 64-bit
+  const int B = (int)p.B, omega = (int)p.omega;
+  const int64_t n = p.n;
+  const int col = blockIdx.x * kRfNT + threadIdx.x;
+  if (col >= B) return;
+  const int R = (omega + B - 1) / B;  // < kRfT (launcher)
+  const int A = wrows - R;            // largest o_j a window item may have
+  for (int first = rfirst; first < rfirst + rcnt; first += 32) {
+    const int cnt = min(32, rfirst + rcnt - first);
+    uint32_t left = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+    // windows: the first item left is the base (its signal, sigma, tau_h);
+    // every item of the same signal and sigma within A rows behind it joins;
+    // the rest (the ladder's N/16 shift) forms the next window
+    while (left) {
+      const int h = first + __ffs(left) - 1;
+      const int sigh = p.item_sig ? p.item_sig[h] : h;
+      const int64_t sgm = p.item_a[h], tau_h = p.item_b[h];
+      uint32_t win = 0;
+      int maxo = -1, vhi = 0;
+      for (uint32_t m = left; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const int it = first + j;
+        if ((p.item_sig ? p.item_sig[it] : it) != sigh || p.item_a[it] != sgm) continue;
+        const int64_t d = pmod(p.item_b[it] - tau_h, n);
+        const int cj = (int)(d % B);
+        const int64_t o = d / B + (col + cj >= B);
+        if (o > A) continue;
+        const int s = col + cj - ((col + cj >= B) ? B : 0);
+        const int nr = s < omega ? (omega - s + B - 1) / B : 0;
+        win |= 1u << j;
+        maxo = max(maxo, (int)o);
+        vhi = max(vhi, nr - (int)o);
+      }
+      left &= ~win;
+      // gather the column's window rows once, a chunk of loads in flight, raw
+      // samples to shared memory (the column is this thread's own: no barrier)
+      {
+        constexpr int CH = sizeof(Tin) == 8 ? 8 : 4;
+        const Tin* xs = (const Tin*)p.x + (int64_t)sigh * p.xstride;
+        const int64_t step = mulmod(sgm, (int64_t)B % n, n);
+        int64_t idx = mulmod(sgm, pmod((int64_t)col - (int64_t)maxo * B - tau_h, n), n);
+        Tin* vc = V + threadIdx.x;
+        const int nv = vhi + maxo;
+        for (int v = 0; v < nv; v += CH) {
+          Tin t[CH];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            if (v + u < nv) t[u] = __ldcg(xs + idx);
+            idx += step;
+            idx -= (idx >= n) ? n : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (v + u < nv) vc[(v + u) * kRfNT] = t[u];
+        }
+      }
+      // the window's items, grouped by c = shift mod B: the items of one c
+      // read the same taps g[col + c + tB] (t = r - wrap), held in registers
+      uint32_t todo = win;
+      while (todo) {
+        const int c = (int)(pmod(p.item_b[first + __ffs(todo) - 1] - tau_h, n) % B);
+        const int w = (col + c >= B);
+        const int s = col + c - (w ? B : 0);
+        const int nr = s < omega ? (omega - s + B - 1) / B : 0;
+        double T[kRfT];  // T[t + 1] = g[col + c + tB], t = -1 .. kRfT - 2
+        {
+          const double* tp = p.taps + (col + c - B);
+          const int tcnt = (omega - (col + c) + 2 * B - 1) / B;  // valid: t < tcnt
+#pragma unroll
+          for (int t = 0; t < kRfT; ++t)
+            T[t] = (t >= 1 - w && t < tcnt) ? __ldg(tp + t * B) : 0.0;
+        }
+        for (uint32_t m = todo; m; m &= m - 1) {
+          const int j = __ffs(m) - 1;
+          const int it = first + j;
+          const int64_t d = pmod(p.item_b[it] - tau_h, n);
+          if ((int)(d % B) != c) continue;
+          todo &= ~(1u << j);
+          const int o = (int)(d / B) + w;
+          const Tin* vc = V + (maxo - o) * kRfNT + threadIdx.x;  // row r at vc[r NT]
+          double2 acc = cmk(0.0, 0.0);
+          if (w) {
+#pragma unroll
+            for (int r = 0; r < kRfT; ++r)
+              if (r < nr) {
+                const double2 v = to_d2_(vc[r * kRfNT]);
+                acc = cadd_rn(acc, cmk(__dmul_rn(T[r], v.x), __dmul_rn(T[r], v.y)));
+              }
+          } else {
+#pragma unroll
+            for (int r = 0; r + 1 < kRfT; ++r)
+              if (r < nr) {
+                const double2 v = to_d2_(vc[r * kRfNT]);
+                acc = cadd_rn(acc, cmk(__dmul_rn(T[r + 1], v.x), __dmul_rn(T[r + 1], v.y)));
+              }
+          }
+          out[out_row(p, it) * p.B + s] = acc;
+        }
+      }
+    }
   }
 }
 
@@ -871,6 +1005,48 @@ int run_bucketize(int dtype, int mode, const Prod& p0, int64_t nitems, const dou
   rc = run_bucketize_inner(dtype, mode, p, nitems, W, out, ws, ws_bytes, st);
   if (rc) return rc;
   return prof_end(st, ev0);
+}
+
+// Flat bucketizations grouped in permutation runs (items [run_first[r],
+// run_first[r] + run_cnt[r]) share signal and sigma; b' = 0, no gates): the
+// run fold into each item's output row, then the FFT of every row in place.
+// Profiled (when on) as one bucketization launch of nitems items.
+int run_flat_runs(int dtype, const Prod& p0, const int32_t* run_first, const int32_t* run_cnt,
+                  int64_t nruns, int64_t nitems, const double2* W, double2* out, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  if (nruns <= 0 || nitems <= 0) return 0;
+  SFFT_REQUIRE(!p0.item_c && !p0.active && !p0.item_active && p0.item_row,
+               "run fold: needs an ungated item list with output rows and b' = 0");
+  gather_fetch_granularity();
+  BucketProf& bp = bucket_prof();
+  Prod p = p0;
+  p.prof_items = bp.on ? bp.d_items : nullptr;
+  cudaEvent_t ev0{};
+  if (bp.on) {
+    int rc = prof_begin(st, &ev0);
+    if (rc) return rc;
+  }
+  const int R = (int)cdiv_up(p.omega, p.B);
+  if (R >= kRfT || p.B >= (1 << 30) || p.omega >= (1 << 30))  // per-item kernels
+    return run_bucketize(dtype, PROD_FLAT, p0, nitems, W, out, ws, ws_bytes, st);
+  const int wrows = R + (int)std::min<int64_t>(kRfMaxBack, std::max(R - 1, 0));
+  const dim3 g((unsigned)cdiv_up(p.B, kRfNT), (unsigned)nruns);
+  if (dtype == 0) {
+    const size_t sm = (size_t)wrows * kRfNT * sizeof(float2);
+    if (ensure_smem(k_run_fold<float2>, sm)) return -3;
+    k_run_fold<float2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out);
+  } else {
+    const size_t sm = (size_t)wrows * kRfNT * sizeof(double2);
+    if (ensure_smem(k_run_fold<double2>, sm)) return -3;
+    k_run_fold<double2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out);
+  }
+  SFFT_CHECK_LAUNCH("k_run_fold");
+  Prod pl = p;
+  pl.z = out;
+  pl.prof_items = nullptr;
+  int rc = run_bucketize_inner(dtype, PROD_LOAD, pl, nitems, W, out, ws, ws_bytes, st);
+  if (rc) return rc;
+  return bp.on ? prof_end(st, ev0) : 0;
 }
 
 int run_twiddle(double2* W, int64_t B, cudaStream_t st) {

@@ -128,6 +128,11 @@ struct IterArgs {
   int64_t* it2_sigma;
   int64_t* it2_tau;
   int32_t* it2_row;
+  // permutation runs of the compacted list (consecutive items of one signal
+  // and sigma): run_first/run_cnt, rcnt = runs per slot then their offsets
+  int32_t* rcnt;                 // [S + 1]
+  int32_t* run_first;            // [S*(M+C)]
+  int32_t* run_cnt;
 };
 
 __device__ __forceinline__ uint32_t ht_slot(int64_t f, int HT) {
@@ -171,9 +176,16 @@ __global__ void k_cb_admit(IterArgs a) {
   if (S.phase != PH_FREE) return;
   // signals still being copied in (streaming admission) are not taken yet
   const int lim = a.avail ? min(a.Q, *(volatile const int32_t*)a.avail) : a.Q;
-  const int idx = atomicAdd(a.stats + 4, 1);
+  // The queue head never moves past this thread's limit: a CAS loop instead of
+  // add-then-roll-back, so a thread holding an older (smaller) limit cannot undo
+  // an admission made by a thread that already saw the raised limit.
+  int idx = *(volatile int32_t*)(a.stats + 4);
+  while (idx < lim) {
+    const int prev = atomicCAS(a.stats + 4, idx, idx + 1);
+    if (prev == idx) break;
+    idx = prev;
+  }
   if (idx >= lim) {
-    atomicSub(a.stats + 4, 1);
     if (lim >= a.Q) S.phase = PH_IDLE;
     return;
   }
@@ -293,35 +305,45 @@ __global__ void k_cb_plan(IterArgs a) {
     }
     a.role_src[(int64_t)s * a.M + j] = src;
   }
-  int spec = 0;
+  int spec = 0, runs = nm > 0;
   if (first)
     for (int c = 0; c < a.C; ++c) {
       const int pp = S.pidx + 1 + (c < a.M ? 0 : 1 + (c - a.M) / 3);
       spec += pp < a.P;
+      // a new run at each permutation's first shift
+      runs += pp < a.P && (c == 0 || (c >= a.M && (c - a.M) % 3 == 0));
     }
   a.cnt[s] = nm + spec;
+  a.rcnt[s] = runs;
 }
 
 // exclusive scan of cnt[0..S) in place, total in cnt[S] (one CTA)
-__global__ void __launch_bounds__(1024) k_cb_scan(IterArgs a) {
-  __shared__ int red[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
+__device__ void cb_scan_one(int32_t* v, int S, int* red, int* carry, int32_t* total) {
+  if (threadIdx.x == 0) *carry = 0;
   __syncthreads();
-  for (int base = 0; base < a.S; base += 1024) {
+  for (int base = 0; base < S; base += 1024) {
     const int i = base + threadIdx.x;
-    const int v = i < a.S ? a.cnt[i] : 0;
+    const int x = i < S ? v[i] : 0;
     int tot;
-    const int ex = block_exscan<1024>(v, red, &tot);
-    if (i < a.S) a.cnt[i] = carry + ex;
+    const int ex = block_exscan<1024>(x, red, &tot);
+    if (i < S) v[i] = *carry + ex;
     __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
+    if (threadIdx.x == 0) *carry += tot;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    a.cnt[a.S] = carry;
-    a.stats[5] = carry;  // read by the host with the round status
+    v[S] = *carry;
+    *total = *carry;  // read by the host with the round status
   }
+  __syncthreads();
+}
+
+// exclusive scans of the per-slot item and run counts (one CTA)
+__global__ void __launch_bounds__(1024) k_cb_scan(IterArgs a) {
+  __shared__ int red[32];
+  __shared__ int carry;
+  cb_scan_one(a.cnt, a.S, red, &carry, a.stats + 5);
+  cb_scan_one(a.rcnt, a.S, red, &carry, a.stats + 6);
 }
 
 __global__ void k_cb_fill(IterArgs a) {
@@ -329,7 +351,9 @@ __global__ void k_cb_fill(IterArgs a) {
   if (s >= a.S) return;
   const IterState& S = a.st[s];
   int o = a.cnt[s];
+  int ro = a.rcnt[s];
   const int sig = S.sig > 0 ? S.sig : 0;
+  const int o_own = o;
   for (int j = 0; j < S.nsh && j < a.M; ++j) {
     if (a.role_src[(int64_t)s * a.M + j] >= 0) continue;
     a.it2_sig[o] = sig;
@@ -337,6 +361,11 @@ __global__ void k_cb_fill(IterArgs a) {
     a.it2_tau[o] = pmod(a.item_tau[s] + role_shift(a, S, j), a.n);
     a.it2_row[o] = j * a.S + s;
     ++o;
+  }
+  if (o > o_own) {
+    a.run_first[ro] = o_own;
+    a.run_cnt[ro] = o - o_own;
+    ++ro;
   }
   if (!(S.phase == PH_LOOP && S.it == 1)) return;
   int32_t* dp = a.dir_p + (int64_t)s * a.C;
@@ -346,6 +375,12 @@ __global__ void k_cb_fill(IterArgs a) {
     if (pp >= a.P) continue;
     const int64_t d = c < a.M ? a.shifts[c] : (int64_t)((c - a.M) % 3);
     const int64_t row = (int64_t)sig * a.pstride + pp;
+    if (c == 0 || (c >= a.M && (c - a.M) % 3 == 0)) {  // a permutation's first shift
+      a.run_first[ro] = o;
+      a.run_cnt[ro] = 0;
+      ++ro;
+    }
+    a.run_cnt[ro - 1] += 1;
     a.it2_sig[o] = sig;
     a.it2_sigma[o] = a.psig[row];
     a.it2_tau[o] = pmod(pmod(a.ptau[row], a.n) + d, a.n);
@@ -1450,6 +1485,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int64_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 43 it2_sigma + it2_tau
       sizeof(double2) * (size_t)S * kResPre,                    // 44 residual pre-check values
       sizeof(int32_t) * (size_t)S * kResPre,                    // 45 residual pre-check buckets
+      sizeof(int32_t) * (size_t)(S + 1),                        // 46 rcnt
+      sizeof(int32_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 47 run_first + run_cnt
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1641,6 +1678,9 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.it2_row = a.it2_sig + (size_t)S * (M + spec_rows(M));
   a.it2_sigma = (int64_t*)(w + Lo.off[43]);
   a.it2_tau = a.it2_sigma + (size_t)S * (M + spec_rows(M));
+  a.rcnt = (int32_t*)(w + Lo.off[46]);
+  a.run_first = (int32_t*)(w + Lo.off[47]);
+  a.run_cnt = a.run_first + (size_t)S * (M + spec_rows(M));
   double2* rpre = (double2*)(w + Lo.off[44]);
   int32_t* rlist = (int32_t*)(w + Lo.off[45]);
   RealTab rt{};
@@ -1748,12 +1788,20 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     return 0;
   };
   int nit = 0;  // planned items of the coming round (row-cache path)
+  int nrun = 0;  // their permutation runs
+  // permutation-run fold (one gather per sample of a run): c64/c128 flat items
+  // with b' = 0 on the row-cache path, SFFT_RUN_FOLD=1 (A/B measurements;
+  // parity tests run both); default the per-item cluster kernel
+  const bool run_fold_off = !(getenv("SFFT_RUN_FOLD") && atoi(getenv("SFFT_RUN_FOLD")));
   {
     int rc0 = prologue();
     if (rc0) return rc0;
     if (a.C > 0) {
-      SFFT_CUDA(cudaMemcpyAsync(&nit, a.stats + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      int32_t h2[2];
+      SFFT_CUDA(cudaMemcpyAsync(h2, a.stats + 5, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       SFFT_CUDA(cudaStreamSynchronize(st));
+      nit = h2[0];
+      nrun = h2[1];
     }
   }
   for (; round < max_rounds; ++round) {
@@ -1761,7 +1809,11 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     if (a.C > 0) {
       k_cb_copy<<<(unsigned)(S * M), 256, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_cb_copy");
-      if (nit > 0) rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
+      if (nit > 0 && !run_fold_off)
+        rc = run_flat_runs(dtype, pc, a.run_first, a.run_cnt, nrun, nit, W, a.y, bws, bws_bytes,
+                           st);
+      else if (nit > 0)
+        rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
     } else {
       rc = run_bucketize(dtype, PROD_FLAT, p, (int64_t)M * S, W, a.y, bws, bws_bytes, st);
     }
@@ -1852,6 +1904,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     t_max = hs[1];
     h_max = hs[2];
     nit = hs[5];
+    nrun = hs[6];
     if (hs[3] >= Q) break;
   }
   SFFT_REQUIRE(round < max_rounds, "iterative: round limit reached (internal error)");

@@ -228,17 +228,28 @@ def _empty_batch(n, S, k, dev, iterations, converged):
 
 
 class _WS:
+    """Grow-only device scratch handed to the library (caller-owned memory),
+    keyed by (device, current stream, tag): a buffer is only ever used by the
+    launches of the stream it was allocated on, so calls on different streams
+    never share scratch, and the torch caching allocator's stream-ordered reuse
+    keeps an evicted buffer safe.  At most ``cap`` buffers are kept (least
+    recently used evicted), so pooled side streams cannot pin unbounded
+    GB-scale workspaces."""
     buf: dict = {}
+    cap: int = 8
 
     @classmethod
     def get(cls, nbytes, device, tag: str = ""):
         import torch
-        key = str(device) + tag
-        t = cls.buf.get(key)
+        dev = torch.device(device)
+        key = (str(dev), torch.cuda.current_stream(dev).cuda_stream, tag)
+        t = cls.buf.pop(key, None)
         if t is None or t.numel() < nbytes:
-            cls.buf.pop(key, None)
-            t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
-            cls.buf[key] = t
+            t = None  # release before allocating the larger one
+            t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+        cls.buf[key] = t  # most recently used last
+        while len(cls.buf) > cls.cap:
+            cls.buf.pop(next(iter(cls.buf)))
         return t
 
 
@@ -302,7 +313,7 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
     sched = _sched_buffer(S, dev)
     L = lib()
     wsb = L.sfft_iterative_ws_bytes(n, b, nslots, M, cap)
-    ws = _WS.get(wsb, dev, tag=f"it{torch.cuda.current_stream(dev).cuda_stream}")
+    ws = _WS.get(wsb, dev, "iterative")
     import ctypes
     lad = (ctypes.c_int64 * len(ladder))(*ladder) if ladder else None
     dt = 0 if X.dtype == torch.complex64 else 1

@@ -42,7 +42,7 @@ def peeling_batch(xs, k: int, cfg):
     sched = _sched_buffer(S, dev)
     L = lib()
     wsb = L.sfft_peeling_ws_bytes(n, S, fac, m, k)
-    ws = _WS.get(wsb, dev)
+    ws = _WS.get(wsb, dev, "peeling")
     dt = 0 if X.dtype == torch.complex64 else 1
     check(L.sfft_run_peeling(dt, ptr(X), n, X.stride(0), S, fac, m, wst, k, ptr(out_pos),
                              ptr(out_coef), ptr(out_n), ptr(out_it), ptr(out_cv), ptr(out_err),

@@ -41,7 +41,7 @@ def voting_batch(xs, k: int, cfg):
     sched = _sched_buffer(S, dev)
     L = lib()
     wsb = L.sfft_voting_ws_bytes(n, b, S, R, k, bpre)
-    ws = _WS.get(wsb, dev)
+    ws = _WS.get(wsb, dev, "voting")
     gmax = torch.tensor([filt.peak], dtype=torch.float64, device=dev)
     dt = 0 if X.dtype == torch.complex64 else 1
     check(L.sfft_run_voting(dt, ptr(X), n, X.stride(0), S, ptr(filt.taps), filt.support, b,

@@ -211,13 +211,16 @@ def test_iterative_stragglers(sb, case, dtype, tol):
     check_case(sb, rec, arr, dtype, tol)
 
 
+@pytest.mark.parametrize("run_fold", ["1", "0"])
 @pytest.mark.parametrize("slots", [1, 2, 3])
-def test_row_cache_continuous_batching(sb, slots, monkeypatch):
+def test_row_cache_continuous_batching(sb, slots, run_fold, monkeypatch):
     """The measurement row cache (speculative next-loop / polish rows, hits
     copied, misses measured) forced on for C1 with slots refilled as signals
-    finish: every signal gets the reference's result."""
+    finish: every signal gets the reference's result, with the permutation-run
+    fold (k_run_fold) and with the per-item kernel."""
     import torch
     monkeypatch.setenv("SFFT_ROW_CACHE", "1")
+    monkeypatch.setenv("SFFT_RUN_FOLD", run_fold)
     cases = [c for c in CASES if c[0]["name"].startswith("C1")]
     X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).cuda()
     res = sb.run_iterative_batch(X, 16, _cfg(sb, cases[0][0]), slots=slots).to_results()
@@ -230,10 +233,13 @@ def test_row_cache_continuous_batching(sb, slots, monkeypatch):
             (rec["samples_read"], rec["iterations"], rec["converged"]), rec["name"]
 
 
-def test_row_cache_c3_default_gate(sb):
+@pytest.mark.parametrize("run_fold", ["1", "0"])
+def test_row_cache_c3_default_gate(sb, run_fold, monkeypatch):
     """C3 (converging and non-converging signals) through 512 slots, where the
-    row cache is on by default, against the reference golden vectors."""
+    row cache is on by default, against the reference golden vectors (with
+    the permutation-run fold and with the per-item cluster kernel)."""
     import torch
+    monkeypatch.setenv("SFFT_RUN_FOLD", run_fold)
     cases = [c for c in CASES if c[0]["name"].startswith("C3")] + list(STRAG)
     X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).cuda()
     res = sb.run_iterative_batch(X, 256, _cfg(sb, cases[0][0]), slots=512).to_results()
@@ -265,3 +271,41 @@ def test_iterative_four_step_b8192(sb, row_cache, monkeypatch):
         assert err <= 1e-10
         assert (res.samples_read, res.iterations, res.converged) == \
             (want.samples_read, want.iterations, want.converged)
+
+
+def test_run_fold_bit_identical_c3(sb, monkeypatch):
+    """The permutation-run fold gathers each sample of a (signal, sigma) run
+    once and folds every shift from shared memory; it must give bit-identical
+    bucket values, hence identical results, to the per-item cluster kernel
+    (C3 batch incl. non-converging signals, complex64 and complex128)."""
+    import torch
+    cases = [c for c in CASES if c[0]["name"].startswith("C3")] + list(STRAG)
+    cfg = _cfg(sb, cases[0][0])
+    for dt in (torch.complex64, torch.complex128):
+        X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).to(dt).cuda()
+        out = []
+        for on in ("1", "0"):
+            monkeypatch.setenv("SFFT_RUN_FOLD", on)
+            br = sb.run_iterative_batch(X, 256, cfg, slots=512)
+            out.append((br.pos.cpu(), br.coef.cpu(), br.count.cpu(), br.samples_read.cpu(),
+                        br.iterations.cpu()))
+        for u, v in zip(*out):
+            assert torch.equal(u, v)
+
+
+def test_stream_admission_many_slots_chunk1(sb):
+    """Streaming admission with many slots racing for rows that arrive one at a
+    time (chunk=1): every signal is admitted exactly once and its result equals
+    the resident batch's (a queue head that rolled back under a raised limit
+    would run one signal twice and leave another at zeros)."""
+    import torch
+    from oracle import sfft_oracle as O
+    n, k, q = 1 << 14, 8, 96
+    xs = np.stack([O.synth(n, k, 30.0, 900 + j)[0] for j in range(q)])
+    cfg = sb.AlgorithmConfig(framework="iterative", num_buckets=64)
+    want = sb.run_iterative_batch(torch.as_tensor(xs).cuda(), k, cfg, slots=64)
+    got = sb.run_iterative_stream(torch.as_tensor(xs).pin_memory(), k, cfg, slots=64, chunk=1)
+    assert torch.equal(got.count.cpu(), want.count.cpu())
+    assert bool((got.count > 0).all())
+    for f in ("pos", "coef", "samples_read", "iterations", "converged"):
+        assert torch.equal(getattr(got, f).cpu(), getattr(want, f).cpu()), f
