@@ -113,7 +113,7 @@ int sfft_heavy_bitmap(const void* values, int64_t nsets, int64_t B, const double
 size_t sfft_votes_ws_bytes(int64_t n, int64_t nsig, int64_t rounds);
 
 /* A10 vote_tally + A11 select_by_votes (sfft/reconstruct.py:158-194), for
- * nsig independent signals of `rounds` rounds each (rounds <= 64).
+ * nsig independent signals of `rounds` rounds each (rounds <= 255).
  * Position f of signal s scores one per round r whose heavy bitmap
  * bits[s][r] holds f's flat bucket (((sigma*(f-b') mod n) - cs + L/2) mod n)/L.
  * counts_out [nsig][n] (optional) receives the scores (or counts_in supplies
@@ -124,6 +124,19 @@ int sfft_vote_select(int64_t n, int64_t B, int64_t rounds, int64_t nsig, const u
                      const int64_t* counts_in, int64_t* counts_out, int64_t need, int64_t keep,
                      int64_t* cand, int32_t* ncand, void* ws, size_t ws_bytes, void* stream);
 
+/* A10 vote_tally for bucket sets of any kind (sfft/reconstruct.py:158-179,
+ * preimages sfft/bucketize.py:108-118): counts[f] (int64 [n]) = number of
+ * rounds r whose heavy bitmap bits[bit_offset[r] ..] (B_r = nbuckets[r] bits,
+ * as sfft_heavy_bitmap writes it) holds f's bucket under round r's hash view:
+ * m = sigma[r]*(f - bprime[r]) mod n, L = n/B_r, and by kind[r]:
+ *   0 flat / Dirichlet with half offset: ((m - cs[r] + L/2) mod n)/L mod B_r,
+ *   1 spike: m mod B_r,  2 Dirichlet without half offset: ((m - cs[r]) mod n)/L mod B_r.
+ * bprime, kind, center_shift may be NULL (0).  Any number of rounds. */
+int sfft_vote_tally(int64_t n, int64_t rounds, const int64_t* nbuckets, const int64_t* bit_offset,
+                    const uint32_t* bits, const int64_t* sigma, const int64_t* bprime,
+                    const int32_t* kind, const int64_t* center_shift, int64_t* counts,
+                    void* stream);
+
 /* A12 _energy_estimates (sfft/frameworks.py:321-332) for `rounds` bucket sets
  * y[r][B]: est[r][c] = y[r][b]/(G[bL-m]*w^{tau[r] m}), m = sigma[r]*cand[c],
  * (NaN, 0) where |G| < 0.05*(*gmax). */
@@ -132,7 +145,7 @@ int sfft_energy_estimates(const void* y, int64_t B, const void* gtable, const do
                           const int64_t* cand, int64_t ncand, void* est, void* stream);
 
 /* A13 _trimmed_mean (sfft/frameworks.py:335-351) over the rows of est
- * [rounds][ncand] (rounds <= 64). */
+ * [rounds][ncand] (rounds <= 255). */
 int sfft_trimmed_mean(const void* est, int64_t rounds, int64_t ncand, void* out, void* stream);
 
 /* A14 _subtract_flat (sfft/frameworks.py:423-436):

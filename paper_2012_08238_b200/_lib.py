@@ -98,6 +98,8 @@ SIGNATURES.update({
     "sfft_votes_ws_bytes": (sz, [i64, i64, i64]),
     "sfft_vote_select": (C.c_int, [i64, i64, i64, i64, vp, P_i64, P_i64, i64, P_i64, P_i64, i64,
                                    i64, P_i64, P_i32, vp, sz, vp]),
+    "sfft_vote_tally": (C.c_int, [i64, i64, P_i64, P_i64, vp, P_i64, P_i64, P_i32, P_i64, P_i64,
+                                  vp]),
     "sfft_energy_estimates": (C.c_int, [vp, i64, vp, P_f64, i64, i64, P_i64, P_i64, P_i64, i64,
                                         vp, vp]),
     "sfft_trimmed_mean": (C.c_int, [vp, i64, i64, vp, vp]),

@@ -236,14 +236,14 @@ SFFT_API int sfft_vote_select(int64_t n, int64_t B, int64_t rounds, int64_t nsig
                               int64_t center_shift, const int64_t* counts_in, int64_t* counts_out,
                               int64_t need, int64_t keep, int64_t* cand, int32_t* ncand,
                               void* ws, size_t ws_bytes, void* stream) {
-  SFFT_REQUIRE(n > 0 && B > 0 && n % B == 0 && rounds >= 0 && rounds <= 64 && nsig >= 1,
+  SFFT_REQUIRE(n > 0 && B > 0 && n % B == 0 && rounds >= 0 && rounds <= kMaxVoteRounds && nsig >= 1,
                "sfft_vote_select: bad sizes");
   SFFT_REQUIRE(counts_in || (bits && sigma), "sfft_vote_select: need counts or bitmaps");
   SFFT_REQUIRE(need >= 1, "sfft_vote_select: need >= 1");
   SFFT_REQUIRE(!cand || (ncand && keep > 0), "sfft_vote_select: cand needs ncand and keep > 0");
   SFFT_REQUIRE(ws && ws_bytes >= votes_ws_bytes(n, (int)nsig, (int)rounds),
                "sfft_vote_select: workspace too small");
-  VoteRounds vr;
+  VoteRounds vr{};
   vr.bits = bits;
   vr.sigma = sigma;
   vr.bprime = bprime;
@@ -255,6 +255,17 @@ SFFT_API int sfft_vote_select(int64_t n, int64_t B, int64_t rounds, int64_t nsig
   vr.R = (int)rounds;
   return run_votes(vr, (int)nsig, counts_in, counts_out, (int)need, (int)keep, cand, ncand,
                    (int*)ws, cand != nullptr, (cudaStream_t)stream);
+}
+
+SFFT_API int sfft_vote_tally(int64_t n, int64_t rounds, const int64_t* nbuckets,
+                             const int64_t* bit_offset, const uint32_t* bits,
+                             const int64_t* sigma, const int64_t* bprime, const int32_t* kind,
+                             const int64_t* center_shift, int64_t* counts, void* stream) {
+  SFFT_REQUIRE(n > 0 && rounds >= 0 && rounds <= (1 << 30), "sfft_vote_tally: bad sizes");
+  SFFT_REQUIRE(counts && (rounds == 0 || (nbuckets && bit_offset && bits && sigma)),
+               "sfft_vote_tally: null pointer");
+  return run_vote_tally(n, (int)rounds, nbuckets, bit_offset, bits, sigma, bprime, kind,
+                        center_shift, counts, (cudaStream_t)stream);
 }
 
 SFFT_API int sfft_energy_estimates(const void* y, int64_t B, const void* gtable,

@@ -546,7 +546,7 @@ constexpr int kRfT = 22;       // tap registers: items of up to kRfT - 1 rows sh
 template <typename Tin>
 __global__ void __launch_bounds__(kRfNT, 3)
     k_run_fold(Prod p, const int32_t* __restrict__ run_first, const int32_t* __restrict__ run_cnt,
-               int wrows, double2* __restrict__ out) {
+               int wrows, double2* __restrict__ out, int async, int prefetch) {
   extern __shared__ __align__(16) unsigned char rf_smem[];
   Tin* V = reinterpret_cast<Tin*>(rf_smem);  // [wrows][kRfNT], column = thread
   const int run = blockIdx.y;
@@ -560,6 +560,26 @@ __global__ void __launch_bounds__(kRfNT, 3)
   if (col >= B) return;
   const int R = (omega + B - 1) / B;  // < kRfT (launcher)
   const int A = wrows - R;            // largest o_j a window item may have
+  if (prefetch) {
+    // the lead run of a signal (its first in the list; runs are slot-major)
+    // asks L2 for the whole signal in bulk, at streaming efficiency, so the
+    // gathers of all its runs find their lines there
+    const int pr = run + prefetch - 1;
+    if (pr < gridDim.y) {
+      const int f0 = run_first[pr];
+      const int sg0 = p.item_sig ? p.item_sig[f0] : f0;
+      const int sgp = pr == 0 ? -1 : (p.item_sig ? p.item_sig[run_first[pr - 1]] : run_first[pr - 1]);
+      if (sg0 != sgp) {
+        const size_t bytes = (size_t)n * sizeof(Tin);
+        const size_t per = (bytes / (gridDim.x * kRfNT)) & ~(size_t)15;
+        const char* base = (const char*)p.x + (size_t)sg0 * p.xstride * sizeof(Tin) +
+                           (size_t)(blockIdx.x * kRfNT + threadIdx.x) * per;
+        if (per)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base), "r"((uint32_t)per)
+                       : "memory");
+      }
+    }
+  }
   for (int first = rfirst; first < rfirst + rcnt; first += 32) {
     const int cnt = min(32, rfirst + rcnt - first);
     uint32_t left = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
@@ -596,7 +616,25 @@ __global__ void __launch_bounds__(kRfNT, 3)
         int64_t idx = mulmod(sgm, pmod((int64_t)col - (int64_t)maxo * B - tau_h, n), n);
         Tin* vc = V + threadIdx.x;
         const int nv = vhi + maxo;
-        for (int v = 0; v < nv; v += CH) {
+        if (async) {
+          // every row of the window in flight at once, no registers held:
+          // asynchronous copies straight into the thread's column
+          uint32_t sa = (uint32_t)__cvta_generic_to_shared(vc);
+          for (int v = 0; v < nv; ++v) {
+            if (sizeof(Tin) == 8)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(xs + idx)
+                           : "memory");
+            else
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(xs + idx)
+                           : "memory");
+            sa += kRfNT * (uint32_t)sizeof(Tin);
+            idx += step;
+            idx -= (idx >= n) ? n : 0;
+          }
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+        }
+        for (int v = 0; v < (async ? 0 : nv); v += CH) {
           Tin t[CH];
 #pragma unroll
           for (int u = 0; u < CH; ++u) {
@@ -1031,14 +1069,18 @@ int run_flat_runs(int dtype, const Prod& p0, const int32_t* run_first, const int
     return run_bucketize(dtype, PROD_FLAT, p0, nitems, W, out, ws, ws_bytes, st);
   const int wrows = R + (int)std::min<int64_t>(kRfMaxBack, std::max(R - 1, 0));
   const dim3 g((unsigned)cdiv_up(p.B, kRfNT), (unsigned)nruns);
+  // SFFT_RF_SMEM=<bytes>: pad the dynamic shared memory (occupancy experiments)
+  const size_t pad = getenv("SFFT_RF_SMEM") ? (size_t)atoll(getenv("SFFT_RF_SMEM")) : 0;
+  const int async = getenv("SFFT_RF_ASYNC") ? atoi(getenv("SFFT_RF_ASYNC")) : 0;
+  const int prefetch = getenv("SFFT_RF_PREFETCH") ? atoi(getenv("SFFT_RF_PREFETCH")) : 0;
   if (dtype == 0) {
-    const size_t sm = (size_t)wrows * kRfNT * sizeof(float2);
+    const size_t sm = std::max(pad, (size_t)wrows * kRfNT * sizeof(float2));
     if (ensure_smem(k_run_fold<float2>, sm)) return -3;
-    k_run_fold<float2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out);
+    k_run_fold<float2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out, async, prefetch);
   } else {
-    const size_t sm = (size_t)wrows * kRfNT * sizeof(double2);
+    const size_t sm = std::max(pad, (size_t)wrows * kRfNT * sizeof(double2));
     if (ensure_smem(k_run_fold<double2>, sm)) return -3;
-    k_run_fold<double2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out);
+    k_run_fold<double2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out, async, prefetch);
   }
   SFFT_CHECK_LAUNCH("k_run_fold");
   Prod pl = p;

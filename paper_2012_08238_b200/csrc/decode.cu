@@ -221,14 +221,14 @@ __global__ void __launch_bounds__(kVoteNT) k_votes_hist(VoteRounds vr, const int
                                                         int64_t* counts_out, int nchunks,
                                                         int* chist /*[S][nchunks][R+1]*/) {
   extern __shared__ uint32_t sbits[];
-  __shared__ int h[65];
+  __shared__ int h[kMaxVoteRounds + 1];
   const int s = blockIdx.y;
   const int chunk = blockIdx.x;
   const int R = vr.R;
   const int64_t* sig_s = vr.sigma ? vr.sigma + (int64_t)s * R : nullptr;
   const int64_t* bp_s = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
-  const uint32_t* bits_s = sbits;
-  if (!counts_in) {
+  const uint32_t* bits_s = vr.bits_global ? vr.bits + (int64_t)s * R * vr.words : sbits;
+  if (!counts_in && !vr.bits_global) {
     const uint32_t* g = vr.bits + (int64_t)s * R * vr.words;
     for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += kVoteNT) sbits[i] = g[i];
   }
@@ -253,7 +253,7 @@ __global__ void k_votes_scan(int nchunks, int R, int need, int keep, int* chist,
                              int32_t* ncand) {
   const int s = blockIdx.x;
   int* hs = chist + (int64_t)s * nchunks * (R + 1);
-  __shared__ long long tot[65];
+  __shared__ long long tot[kMaxVoteRounds + 1];
   for (int c = threadIdx.x; c <= R; c += blockDim.x) {
     long long run = 0;
     for (int k = 0; k < nchunks; ++k) {
@@ -291,13 +291,14 @@ __global__ void __launch_bounds__(kVoteNT) k_votes_emit(VoteRounds vr, const int
   __shared__ int red[32];
   __shared__ int64_t lpos[kVoteChunk];
   __shared__ uint8_t lcnt[kVoteChunk];
-  __shared__ int run[65];
+  __shared__ int run[kMaxVoteRounds + 1];
   const int s = blockIdx.y;
   const int chunk = blockIdx.x;
   const int R = vr.R;
   const int64_t* sig_s = vr.sigma ? vr.sigma + (int64_t)s * R : nullptr;
   const int64_t* bp_s = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
-  if (!counts_in) {
+  const uint32_t* bits_s = vr.bits_global ? vr.bits + (int64_t)s * R * vr.words : sbits;
+  if (!counts_in && !vr.bits_global) {
     const uint32_t* g = vr.bits + (int64_t)s * R * vr.words;
     for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += kVoteNT) sbits[i] = g[i];
   }
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kVoteNT) k_votes_emit(VoteRounds vr, const int
     int c = 0;
     if (p < vr.n) {
       if (counts_in) c = (int)counts_in[(int64_t)s * vr.n + p];
-      else c = vote_count(vr, sbits, sig_s, bp_s, p);
+      else c = vote_count(vr, bits_s, sig_s, bp_s, p);
     }
     cnts[j] = c;
     mine += (c >= need && c > 0);
@@ -339,6 +340,47 @@ __global__ void __launch_bounds__(kVoteNT) k_votes_emit(VoteRounds vr, const int
     }
   }
   (void)cand_count;
+}
+
+// ---------------------------------------------------------------- general tally
+
+// vote_tally over any bucket sets (sfft/reconstruct.py:158-179): position f
+// scores one in round r iff its bucket under round r's hash view
+// (sfft/bucketize.py:81-90) is heavy.  m = sigma_r (f - b'_r) mod n, L_r = n/B_r:
+//   kind 0 (flat, or Dirichlet with half offset): ((m - cs_r + L_r/2) mod n) / L_r mod B_r
+//   kind 1 (spike):                                m mod B_r
+//   kind 2 (Dirichlet, no half offset):           ((m - cs_r) mod n) / L_r mod B_r
+// This is the reference's preimage scatter evaluated per position (no atomics).
+__global__ void k_vote_tally(int64_t n, int R, const int64_t* __restrict__ Bs,
+                             const int64_t* __restrict__ boff, const uint32_t* __restrict__ bits,
+                             const int64_t* __restrict__ sigma, const int64_t* __restrict__ bprime,
+                             const int32_t* __restrict__ kind, const int64_t* __restrict__ cs,
+                             int64_t* __restrict__ counts) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  int64_t c = 0;
+  for (int r = 0; r < R; ++r) {
+    const int64_t B = Bs[r], L = n / B;
+    const int64_t m = mulmod(pmod(sigma[r], n), pmod(f - (bprime ? bprime[r] : 0), n), n);
+    const int kd = kind ? kind[r] : 0;
+    const int64_t sh = cs ? cs[r] : 0;
+    int64_t b;
+    if (kd == 1) b = m % B;
+    else if (kd == 2) b = (pmod(m - sh, n) / L) % B;
+    else b = (pmod(m - sh + L / 2, n) / L) % B;
+    c += (__ldg(bits + boff[r] + (b >> 5)) >> (b & 31)) & 1u;
+  }
+  counts[f] = c;
+}
+
+int run_vote_tally(int64_t n, int R, const int64_t* Bs, const int64_t* boff, const uint32_t* bits,
+                   const int64_t* sigma, const int64_t* bprime, const int32_t* kind,
+                   const int64_t* cs, int64_t* counts, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_vote_tally<<<(unsigned)cdiv_up(n, 256), 256, 0, st>>>(n, R, Bs, boff, bits, sigma, bprime,
+                                                            kind, cs, counts);
+  SFFT_CHECK_LAUNCH("k_vote_tally");
+  return 0;
 }
 
 // ---------------------------------------------------------------- fast path
@@ -424,12 +466,14 @@ __global__ void __launch_bounds__(256) k_vote_collect(VoteRounds vr, FastVote fv
                                                       int64_t hc, const int32_t* hl,
                                                       const int32_t* nh, const int64_t* sinv,
                                                       int32_t* cnt, unsigned long long* buf) {
-  extern __shared__ uint32_t sb[];
-  __shared__ int64_t ssig[64];
+  extern __shared__ uint32_t sbm[];
+  __shared__ int64_t ssig[kMaxVoteRounds];
   const int s = blockIdx.y;
   const int R = vr.R;
   const uint32_t* gb = vr.bits + (int64_t)s * R * vr.words;
-  for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += blockDim.x) sb[i] = gb[i];
+  const uint32_t* sb = vr.bits_global ? gb : sbm;
+  if (!vr.bits_global)
+    for (int64_t i = threadIdx.x; i < (int64_t)R * vr.words; i += blockDim.x) sbm[i] = gb[i];
   for (int r = threadIdx.x; r < R; r += blockDim.x) ssig[r] = vr.sigma[(int64_t)s * R + r];
   __syncthreads();
   const int64_t* bps = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
@@ -551,7 +595,7 @@ size_t votes_fast_ws_bytes(int S, int R, int64_t hc) {
 int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, int64_t* cand,
                    int32_t* ncand, void* ws, size_t ws_bytes, int* overflow_host,
                    cudaStream_t st) {
-  SFFT_REQUIRE(vr.R >= 1 && vr.R <= 64 && need >= 1, "votes_fast: bad rounds");
+  SFFT_REQUIRE(vr.R >= 1 && vr.R <= kMaxVoteRounds && need >= 1, "votes_fast: bad rounds");
   SFFT_REQUIRE(ws_bytes >= votes_fast_ws_bytes(S, vr.R, hc), "votes_fast: workspace too small");
   char* w = (char*)ws;
   unsigned long long* buf = (unsigned long long*)w;
@@ -571,8 +615,10 @@ int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, 
   FastVote fv;
   fv.nmask = (vr.n & (vr.n - 1)) == 0 ? vr.n - 1 : -1;
   fv.logL = (vr.L & (vr.L - 1)) == 0 ? __builtin_ctzll((unsigned long long)vr.L) : -1;
-  const size_t sm = (size_t)vr.R * vr.words * sizeof(uint32_t);
-  SFFT_REQUIRE(sm <= 200 * 1024, "votes_fast: heavy bitmaps exceed shared memory");
+  // heavy bitmaps in shared memory when they fit, else read from global memory
+  VoteRounds vg = vr;
+  vg.bits_global = (size_t)vr.R * vr.words * sizeof(uint32_t) > 200 * 1024;
+  const size_t sm = vg.bits_global ? 0 : (size_t)vr.R * vr.words * sizeof(uint32_t);
   const int R0 = vr.R - need + 1;
   const bool pre = R0 >= 1 && (double)R0 * hc * vr.L < 0.5 * (double)vr.n;
   if (pre) {
@@ -582,14 +628,14 @@ int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, 
                                    (int)(sm ? sm : 1)));
     const int64_t total = (int64_t)R0 * hc * vr.L;
     const unsigned gx = (unsigned)std::min<int64_t>(cdiv_up(total, 256), 512);
-    k_vote_collect<1><<<dim3(gx, S), 256, sm, st>>>(vr, fv, need, hc, hl, nh, sinv, cnt, buf);
+    k_vote_collect<1><<<dim3(gx, S), 256, sm, st>>>(vg, fv, need, hc, hl, nh, sinv, cnt, buf);
     SFFT_CHECK_LAUNCH("k_vote_collect<pre>");
   } else {
     SFFT_CUDA(cudaFuncSetAttribute(k_vote_collect<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sm ? sm : 1)));
     // >= 16 positions per thread: the per-block bitmap copy is amortised
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv_up(vr.n, 256 * 16), 1024));
-    k_vote_collect<0><<<dim3(gx, S), 256, sm, st>>>(vr, fv, need, hc, hl, nh, sinv, cnt, buf);
+    k_vote_collect<0><<<dim3(gx, S), 256, sm, st>>>(vg, fv, need, hc, hl, nh, sinv, cnt, buf);
     SFFT_CHECK_LAUNCH("k_vote_collect<scan>");
   }
   SFFT_CUDA(cudaFuncSetAttribute(k_vote_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -604,24 +650,24 @@ int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, 
 int run_votes(const VoteRounds& vr, int S, const int64_t* counts_in, int64_t* counts_out,
               int need, int keep, int64_t* cand, int32_t* ncand, int* chist, bool emit,
               cudaStream_t st) {
-  SFFT_REQUIRE(vr.R >= 0 && vr.R <= 64, "votes: rounds must be <= 64");
+  SFFT_REQUIRE(vr.R >= 0 && vr.R <= kMaxVoteRounds, "votes: rounds must be <= 255");
   const int nchunks = (int)cdiv_up(vr.n, kVoteChunk);
-  const size_t sm = counts_in ? 0 : (size_t)vr.R * vr.words * sizeof(uint32_t);
-  SFFT_REQUIRE(sm <= 200 * 1024, "votes: heavy bitmaps exceed shared memory");
+  const size_t static3 = kVoteChunk * (8 + 1) + (kMaxVoteRounds + 1) * 4 + 32 * 4;
+  VoteRounds vg = vr;
+  vg.bits_global = !counts_in && (size_t)vr.R * vr.words * sizeof(uint32_t) + static3 > 220 * 1024;
+  const size_t sm = (counts_in || vg.bits_global) ? 0 : (size_t)vr.R * vr.words * sizeof(uint32_t);
   SFFT_CUDA(cudaFuncSetAttribute(k_votes_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sm ? sm : 1)));
   dim3 g(nchunks, S);
-  k_votes_hist<<<g, kVoteNT, sm, st>>>(vr, counts_in, counts_out, nchunks, chist);
+  k_votes_hist<<<g, kVoteNT, sm, st>>>(vg, counts_in, counts_out, nchunks, chist);
   SFFT_CHECK_LAUNCH("k_votes_hist");
   if (!emit) return 0;
   k_votes_scan<<<S, 64, 0, st>>>(nchunks, vr.R, need, keep, chist, ncand);
   SFFT_CHECK_LAUNCH("k_votes_scan");
   const size_t sm3 = sm;
-  const size_t static3 = kVoteChunk * (8 + 1) + 65 * 4 + 32 * 4;
-  SFFT_REQUIRE(sm3 + static3 <= 220 * 1024, "votes: heavy bitmaps exceed shared memory");
   SFFT_CUDA(cudaFuncSetAttribute(k_votes_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sm3 ? sm3 : 1)));
-  k_votes_emit<<<g, kVoteNT, sm3, st>>>(vr, counts_in, nchunks, chist, need, keep, cand, ncand);
+  k_votes_emit<<<g, kVoteNT, sm3, st>>>(vg, counts_in, nchunks, chist, need, keep, cand, ncand);
   SFFT_CHECK_LAUNCH("k_votes_emit");
   return 0;
 }
@@ -655,7 +701,7 @@ __global__ void k_trimmed_mean(const double2* __restrict__ est, int R, int64_t C
 }
 
 int run_trimmed_mean(const double2* est, int R, int64_t C, double2* out, cudaStream_t st) {
-  SFFT_REQUIRE(R >= 1 && R <= kMaxRounds, "trimmed_mean: 1 <= rounds <= 64");
+  SFFT_REQUIRE(R >= 1 && R <= kMaxRounds, "trimmed_mean: 1 <= rounds <= 255");
   if (C <= 0) return 0;
   k_trimmed_mean<<<(unsigned)cdiv_up(C, 128), 128, 0, st>>>(est, R, C, out);
   SFFT_CHECK_LAUNCH("k_trimmed_mean");

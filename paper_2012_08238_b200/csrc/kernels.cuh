@@ -87,12 +87,17 @@ int run_floor_heavy(const double2* values, int64_t nsets, int64_t B, double mult
 int run_heavy_bitmap(const double2* values, int64_t nsets, int64_t B, const double* thr,
                      int64_t hc, const int32_t* item_sig, const int32_t* active, uint32_t* bits,
                      int32_t* nheavy, cudaStream_t st);
+// Most rounds a vote count covers (scores are stored in 8 bits per position).
+constexpr int kMaxVoteRounds = 255;
+
 struct VoteRounds {
   const uint32_t* bits;   // [S][R][words]
   const int64_t* sigma;   // [S*R]
   const int64_t* bprime;  // [S*R] (null: 0)
   int64_t n, B, L, words, cs;
   int R;
+  int bits_global;        // 1: the bitmaps are read from global memory (too big for
+                          // shared memory); set by the launchers
 };
 // Runner fast path: candidates (score >= need) of every signal in (-score, pos)
 // order, first keep, without materialising per-position scores.  Returns 1 in
@@ -106,6 +111,10 @@ int run_votes(const VoteRounds& vr, int S, const int64_t* counts_in, int64_t* co
               int need, int keep, int64_t* cand, int32_t* ncand, int* chist, bool emit,
               cudaStream_t st);
 size_t votes_ws_bytes(int64_t n, int S, int R);
+// vote_tally over bucket sets of any kind / width / centre shift (stage API)
+int run_vote_tally(int64_t n, int R, const int64_t* Bs, const int64_t* boff, const uint32_t* bits,
+                   const int64_t* sigma, const int64_t* bprime, const int32_t* kind,
+                   const int64_t* cs, int64_t* counts, cudaStream_t st);
 int run_trimmed_mean(const double2* est, int R, int64_t C, double2* out, cudaStream_t st);
 int run_energy_est(const double2* y, int64_t B, const double2* gt, const double* gmax, int64_t n,
                    int R, const int64_t* sigma, const int64_t* tau, const int64_t* cand,

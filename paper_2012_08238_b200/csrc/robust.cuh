@@ -42,11 +42,12 @@ __device__ __forceinline__ double2 np_join(double a, double b) {
   return cmk(a + (0.0 * b - 0.0), 0.0 + b);
 }
 
-constexpr int kMaxRounds = 64;
+constexpr int kMaxRounds = 255;  // = kMaxVoteRounds
 
-// Trimmed mean over the R rows of est (row stride ld) for one column.
-__device__ inline double2 trimmed_mean_col(const double2* est, int64_t ld, int R) {
-  double re[kMaxRounds], im[kMaxRounds], tmp[kMaxRounds], dev[kMaxRounds];
+// Trimmed mean over the R <= MAXR rows of est (row stride ld) for one column.
+template <int MAXR = 64>
+__device__ inline double2 trimmed_mean_col_t(const double2* est, int64_t ld, int R) {
+  double re[MAXR], im[MAXR], tmp[MAXR], dev[MAXR];
   for (int r = 0; r < R; ++r) {
     const double2 v = est[(int64_t)r * ld];
     re[r] = v.x;
@@ -89,6 +90,11 @@ __device__ inline double2 trimmed_mean_col(const double2* est, int64_t ld, int R
   const double mre = cr ? sr / cr : CUDART_NAN;
   const double mim = ci ? si / ci : CUDART_NAN;
   return np_join(mre, mim);
+}
+
+// small per-thread arrays for the usual round counts, the large ones otherwise
+__device__ inline double2 trimmed_mean_col(const double2* est, int64_t ld, int R) {
+  return R <= 64 ? trimmed_mean_col_t<64>(est, ld, R) : trimmed_mean_col_t<kMaxRounds>(est, ld, R);
 }
 
 

@@ -246,7 +246,7 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
                int64_t Bpre, const double2* Wpre, int64_t* out_pos, double2* out_coef,
                int32_t* out_n, int64_t* out_samples, int64_t* out_sched, void* ws,
                size_t ws_bytes, cudaStream_t st) {
-  SFFT_REQUIRE(R >= 1 && R <= 64, "voting: 1 <= rounds <= 64");
+  SFFT_REQUIRE(R >= 1 && R <= kMaxVoteRounds, "voting: 1 <= rounds <= 255");
   const int C = (int)(2 * k);
   SFFT_REQUIRE(C >= 1 && C <= kFusedMaxB, "voting: 2k must be <= 8192");
   SFFT_REQUIRE(ws_bytes >= voting_ws_bytes(n, B, S, R, C, Bpre), "voting: workspace too small");
@@ -301,7 +301,7 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   if (rc) return rc;
   rc = run_floor_heavy(a.y, (int64_t)S * R, B, 3.0, 2 * k, thr, bits, nullptr, st);
   if (rc) return rc;
-  VoteRounds vr;
+  VoteRounds vr{};
   vr.bits = bits;
   vr.sigma = psig;
   vr.bprime = nullptr;

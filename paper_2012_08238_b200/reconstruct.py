@@ -15,7 +15,7 @@ import numpy as np
 
 from ._lib import check, lib, ptr, stream_of
 from .errors import FilterKindMismatch, InvalidParameter
-from .filters import FLAT
+from .filters import FLAT, SPIKE
 
 __all__ = ["VoteTable", "robust_noise_floor", "vote_tally", "select_by_votes",
            "noise_floors", "need_votes", "estimate_freqshift"]
@@ -86,34 +86,58 @@ def need_votes(min_fraction: float, rounds: int) -> int:
 
 def vote_tally(rounds, heavy_count: int) -> VoteTable:
     """Per round, the ``heavy_count`` largest buckets at/above the round's
-    threshold are heavy; each original position whose flat bucket is heavy
-    gains one vote (evaluated per position on the device, no scatter)."""
+    threshold are heavy; each original position whose bucket under that
+    round's hash view is heavy gains one vote (sfft/reconstruct.py:158-179).
+    Bucket sets of any kind (flat, spike, Dirichlet), width and centre shift
+    mix freely; the heavy sets and the per-position scores run on the device
+    (per-position evaluation of the preimage scatter, no atomics)."""
     import torch
     rounds = list(rounds)
     if not rounds:
         return VoteTable(n=1, rounds=0)
     first = rounds[0][0]
-    n, b = first.n, first.num_buckets
-    for bs, _ in rounds:
-        if bs.filter_kind != FLAT:
-            raise FilterKindMismatch(f"device vote_tally supports flat bucket sets, got {bs.filter_kind}")
-    dev = first.values.device
+    n = first.n
+    dev = first.values.device if hasattr(first.values, "device") else None
     R = len(rounds)
-    vals = torch.stack([_dev_values(bs.values) for bs, _ in rounds])
-    thr = torch.as_tensor([float(t) for _, t in rounds], dtype=torch.float64, device=dev)
-    words = (b + 31) // 32
-    bits = torch.zeros((R, words), dtype=torch.int32, device=dev)
+    # heavy bitmaps: one launch per distinct bucket count, each group's rounds
+    # packed contiguously (bit_offset per round)
+    by_b = {}
+    for r, (bs, _) in enumerate(rounds):
+        if bs.n != n:
+            raise InvalidParameter(f"bucket sets of different lengths ({bs.n} != {n})")
+        by_b.setdefault(bs.num_buckets, []).append(r)
+    offs = np.zeros(R, dtype=np.int64)
+    total = 0
+    for b, idx in by_b.items():
+        for r in idx:
+            offs[r] = total
+            total += (b + 31) // 32
+    dev = _dev_values(first.values, dev).device
+    bits = torch.zeros(max(total, 1), dtype=torch.int32, device=dev)
     st = stream_of(dev)
-    check(lib().sfft_heavy_bitmap(ptr(vals), R, b, ptr(thr), int(heavy_count), ptr(bits), None,
-                                  st), "sfft_heavy_bitmap")
-    sig = torch.as_tensor([bs.perm.sigma for bs, _ in rounds], dtype=torch.int64, device=dev)
-    bp = torch.as_tensor([bs.perm.b_prime for bs, _ in rounds], dtype=torch.int64, device=dev)
+    for b, idx in by_b.items():
+        vals = torch.stack([_dev_values(rounds[r][0].values, dev) for r in idx])
+        thr = torch.as_tensor([float(rounds[r][1]) for r in idx], dtype=torch.float64, device=dev)
+        check(lib().sfft_heavy_bitmap(ptr(vals), len(idx), b, ptr(thr), int(heavy_count),
+                                      ptr(bits[int(offs[idx[0]]):]), None, st),
+              "sfft_heavy_bitmap")
+    kinds = []
+    for bs, _ in rounds:
+        if bs.filter_kind == SPIKE:
+            kinds.append(1)
+        elif bs.filter_kind == FLAT or bs.half_offset:
+            kinds.append(0)
+        else:
+            kinds.append(2)
+    i64 = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int64), device=dev)
+    nb = i64([bs.num_buckets for bs, _ in rounds])
+    sig = i64([bs.perm.sigma for bs, _ in rounds])
+    bp = i64([bs.perm.b_prime for bs, _ in rounds])
+    cs = i64([bs.center_shift for bs, _ in rounds])
+    kd = torch.as_tensor(np.asarray(kinds, dtype=np.int32), device=dev)
     counts = torch.empty(n, dtype=torch.int64, device=dev)
-    wsb = lib().sfft_votes_ws_bytes(n, 1, R)
-    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-    check(lib().sfft_vote_select(n, b, R, 1, ptr(bits), ptr(sig), ptr(bp), first.center_shift,
-                                 None, ptr(counts), 1, 0, None, None, ptr(ws), wsb, st),
-          "sfft_vote_select")
+    check(lib().sfft_vote_tally(n, R, ptr(nb), ptr(i64(offs)), ptr(bits), ptr(sig), ptr(bp),
+                                ptr(kd), ptr(cs), ptr(counts), st), "sfft_vote_tally")
     return VoteTable(n=n, rounds=R, counts=counts)
 
 

@@ -22,8 +22,9 @@ def voting_batch(xs, k: int, cfg):
     if cfg.rounds <= 0 or k <= 0:
         return _empty_batch(n, S, max(k, 0), dev, 0, False)
     b = cfg.resolve_buckets(n, k)
-    if cfg.rounds > 64:
-        raise NotImplementedError("device voting supports up to 64 rounds")
+    if cfg.rounds > 255:
+        # scores are kept in 8 bits per position on the device
+        raise NotImplementedError("device voting supports up to 255 rounds")
     filt = make_flat_filter(n, b, device=dev)
     bpre = 0
     if cfg.spike_prestage:
