@@ -28,9 +28,10 @@ SFFT_API int sfft_version(void) { return 1; }
 // Number of kernels this library has launched in this process.
 SFFT_API int64_t sfft_launch_count(void) { return g_launches.load(); }
 
-// Bucketization profiling: CUDA events around every flat/spike bucketization
-// launch (synchronising after each, so only for measurement runs) and a
-// device count of the items each launch actually processed.
+// Bucketization profiling: CUDA events recorded on the launching stream around
+// every flat/spike bucketization launch (no synchronisation; the events are
+// read by sfft_prof_read) and a device count of the items each launch
+// actually processed.
 SFFT_API int sfft_prof_enable(int on) {
   BucketProf& p = bucket_prof();
   if (on && !p.d_items) SFFT_CUDA(cudaMalloc(&p.d_items, sizeof(unsigned long long)));

@@ -15,6 +15,7 @@
 // the slots directly (no z round trip) and whose row pass writes y.
 #include <cooperative_groups.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -526,171 +527,207 @@ __global__ void __launch_bounds__(kFrNT) k_fold_rows(Prod p, double2* __restrict
   }
 }
 
-// ---- permutation runs: the shifted measurements of one (signal, sigma) share
-// their samples.  Item j of a run reads x[sigma (s + rB - tau_j)] for slot s,
-// row r; with tau_j = tau_0 + a_j B + c_j (0 <= c_j < B) and column
-// col = (s - c_j) mod B that is U[col + (r - o_j) B], U[u] = x[sigma (u - tau_0)],
-// o_j = a_j + (col + c_j >= B).  So one thread owns one column: it gathers the
-// column's rows v in [-max o_j, R) ONCE into its private shared-memory column
-// and folds every item of the run from there (virtual slot s_j = col + c_j
-// mod B, taps g[s_j + rB], rows in reference order, no FMA contraction, so
-// bit-identical to the per-item fold).  Items too far back for the window
-// (o_j > wrows - R) are folded by the per-item path, slot = col.  The ladder
-// of a C3 loop iteration (shifts 0,1,8,64,512,4096,32768) gathers 27 rows per
-// column instead of 7 x 19, the polish shifts (0,1,2) 20 instead of 57.
-// Folded slots go to each item's output row; the in-place FFT pass follows.
-constexpr int kRfNT = 256;
-constexpr int kRfMaxBack = 8;  // window reaches at most this many rows back
-constexpr int kRfT = 22;       // tap registers: items of up to kRfT - 1 rows share them
+// ---- item groups: the shifted measurements of one (signal, sigma) share
+// their samples.  Item j reads x[sigma (s + rB - tau_j)] for slot s, row r;
+// with tau_j = tau_h + a_j B + c_j (0 <= c_j < B, tau_h the window head's) and
+// column col = (s - c_j) mod B that is U[col + (r - o_j) B], U[u] =
+// x[sigma (u - tau_h)], o_j = a_j + (col + c_j >= B).  A CTA owns kGfCols
+// columns of a group of up to kGfItems items (whole permutation runs of one
+// slot, packed by the planner): every sample of a window (head + the items
+// within kGfBack rows behind it) is gathered ONCE into shared memory, then
+// warp j folds item j for 32 of the columns from there (virtual slot s_j =
+// col + c_j mod B, taps g[s_j + rB], rows in reference order, no FMA
+// contraction: bit-identical to the per-item fold).  The C3 loop ladder
+// (shifts 0,1,8,...,32768 in one window, N/16 in a second) gathers 27 + 19
+// rows per column instead of 8 x 19; two polish permutations (0,1,2 each)
+// 2 x 20 instead of 6 x 19.  About one slot's groups are in flight at a time,
+// so the granules a slot touches stay in L2 across its windows.  Folded slots
+// go to each item's output row; the in-place FFT pass follows.
+constexpr int kGfCols = 32;    // columns per CTA (one per lane)
+constexpr int kGfNT = 256;     // 8 warps: warp j folds item j
+constexpr int kGfRows = 48;    // window rows held in shared memory at once
+constexpr int kGfBack = 8;     // a window reaches at most this many rows back
+constexpr int kGfTapRegs = 20; // taps of a slot held in registers (rows per slot)
+
+// Per group: its windows (head item, rows gathered before row 0, the batch
+// and first shared-memory row they occupy) and per item the window, rows back
+// a_j and column shift c_j -- formed once per group by k_gf_prep (the 64 CTAs
+// of a group then load it in one round trip).
+struct GfDesc {
+  int32_t nwin, nbatch;
+  int32_t win[kGfItems], a[kGfItems], c[kGfItems];
+  int32_t head[kGfItems], back[kGfItems], row0[kGfItems], batch[kGfItems];
+};
+constexpr int kGfDescWords = (int)(sizeof(GfDesc) / sizeof(int32_t));
+
+__global__ void k_gf_prep(Prod p, const int32_t* __restrict__ gfirst,
+                          const int32_t* __restrict__ gcnt, int64_t ngroups, GfDesc* desc) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  const int first = gfirst[g];
+  const int cnt = min(gcnt[g], kGfItems);
+  const int64_t n = p.n, B = p.B;
+  const int R = (int)((p.omega + B - 1) / B);
+  const int A = min(kGfBack, R - 1);
+  GfDesc d{};
+  int nw = 0;
+  for (int j = 0; j < cnt; ++j) {
+    const int it = first + j;
+    const int sg = p.item_sig ? p.item_sig[it] : it;
+    const int64_t sm = p.item_a[it], tau = p.item_b[it];
+    int w = -1;
+    for (int q = 0; q < nw && w < 0; ++q) {
+      const int h = first + d.head[q];
+      if ((p.item_sig ? p.item_sig[h] : h) != sg || p.item_a[h] != sm) continue;
+      const int64_t dd = pmod(tau - p.item_b[h], n);
+      if (dd / B <= A) {
+        w = q;
+        d.a[j] = (int)(dd / B);
+        d.c[j] = (int)(dd % B);
+      }
+    }
+    if (w < 0) {
+      w = nw++;
+      d.head[w] = j;
+      d.back[w] = 0;
+      d.a[j] = 0;
+      d.c[j] = 0;
+    }
+    d.win[j] = w;
+    d.back[w] = max(d.back[w], d.a[j] + (d.c[j] > 0));
+  }
+  int nb = 0, used = kGfRows + 1;
+  for (int w = 0; w < nw; ++w) {
+    const int rows = R + d.back[w];
+    if (used + rows > kGfRows) {
+      ++nb;
+      used = 0;
+    }
+    d.batch[w] = nb - 1;
+    d.row0[w] = used;
+    used += rows;
+  }
+  d.nwin = nw;
+  d.nbatch = nb;
+  desc[g] = d;
+}
 
 template <typename Tin>
-__global__ void __launch_bounds__(kRfNT, 3)
-    k_run_fold(Prod p, const int32_t* __restrict__ run_first, const int32_t* __restrict__ run_cnt,
-               int wrows, double2* __restrict__ out, int async, int prefetch) {
-  extern __shared__ __align__(16) unsigned char rf_smem[];
-  Tin* V = reinterpret_cast<Tin*>(rf_smem);  // [wrows][kRfNT], column = thread
-  const int run = blockIdx.y;
-  const int rfirst = run_first[run], rcnt = run_cnt[run];
-  if (p.prof_items && threadIdx.x == 0 && blockIdx.x == 0)
-    atomicAdd(p.prof_items, (unsigned long long)rcnt);
-  // B, Omega < 2^31 (launcher); index arithmetic mod n stays 64-bit
+__global__ void __launch_bounds__(kGfNT, 4)
+    k_group_fold(Prod p, const int32_t* __restrict__ gfirst, const int32_t* __restrict__ gcnt,
+                 const GfDesc* __restrict__ desc, double2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char gf_smem[];
+  Tin* V = reinterpret_cast<Tin*>(gf_smem);  // [kGfRows][kGfCols]
+  __shared__ GfDesc sd;
+  __shared__ short s_lo[kGfItems][kGfCols];  // window w, column: rows [-lo, hi) needed
+  __shared__ short s_hi[kGfItems][kGfCols];
+  __shared__ int s_isig[kGfItems];
+  __shared__ int64_t s_isgm[kGfItems], s_itau[kGfItems];
+  const int g = blockIdx.y;
+  const int first = gfirst[g];
+  const int cnt = min(gcnt[g], kGfItems);
   const int B = (int)p.B, omega = (int)p.omega;
   const int64_t n = p.n;
-  const int col = blockIdx.x * kRfNT + threadIdx.x;
-  if (col >= B) return;
-  const int R = (omega + B - 1) / B;  // < kRfT (launcher)
-  const int A = wrows - R;            // largest o_j a window item may have
-  if (prefetch) {
-    // the lead run of a signal (its first in the list; runs are slot-major)
-    // asks L2 for the whole signal in bulk, at streaming efficiency, so the
-    // gathers of all its runs find their lines there
-    const int pr = run + prefetch - 1;
-    if (pr < gridDim.y) {
-      const int f0 = run_first[pr];
-      const int sg0 = p.item_sig ? p.item_sig[f0] : f0;
-      const int sgp = pr == 0 ? -1 : (p.item_sig ? p.item_sig[run_first[pr - 1]] : run_first[pr - 1]);
-      if (sg0 != sgp) {
-        const size_t bytes = (size_t)n * sizeof(Tin);
-        const size_t per = (bytes / (gridDim.x * kRfNT)) & ~(size_t)15;
-        const char* base = (const char*)p.x + (size_t)sg0 * p.xstride * sizeof(Tin) +
-                           (size_t)(blockIdx.x * kRfNT + threadIdx.x) * per;
-        if (per)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base), "r"((uint32_t)per)
+  const int R = (omega + B - 1) / B;
+  const int tail = omega - (R - 1) * B;  // slots s < tail have R rows, the rest R - 1
+  const int col0 = blockIdx.x * kGfCols;
+  if (p.prof_items && threadIdx.x == 0 && blockIdx.x == 0)
+    atomicAdd(p.prof_items, (unsigned long long)cnt);
+  // ---- the group's descriptor and items (one load each, in parallel)
+  if (threadIdx.x < kGfDescWords)
+    reinterpret_cast<int32_t*>(&sd)[threadIdx.x] =
+        reinterpret_cast<const int32_t*>(desc + g)[threadIdx.x];
+  if (threadIdx.x >= 128 && threadIdx.x < 128 + cnt) {
+    const int j = threadIdx.x - 128, it = first + j;
+    s_isig[j] = p.item_sig ? p.item_sig[it] : it;
+    s_isgm[j] = p.item_a[it];
+    s_itau[j] = p.item_b[it];
+  }
+  __syncthreads();
+  const int nw = sd.nwin;
+  // ---- per (window, column): the rows any of its items needs
+  if (threadIdx.x < nw * kGfCols) {
+    const int w = threadIdx.x / kGfCols, c = threadIdx.x % kGfCols;
+    const int gc = col0 + c;
+    int lo = 0, hi = 0;
+    if (gc < B)
+      for (int j = 0; j < cnt; ++j) {
+        if (sd.win[j] != w) continue;
+        const int wrap = gc + sd.c[j] >= B;
+        const int o = sd.a[j] + wrap;
+        const int s = gc + sd.c[j] - (wrap ? B : 0);
+        const int nr = R - (s >= tail);  // rows with s + rB < Omega (s < B <= Omega)
+        if (nr > 0) {
+          lo = max(lo, o);
+          hi = max(hi, nr - o);
+        }
+      }
+    s_lo[w][c] = (short)lo;
+    s_hi[w][c] = (short)hi;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int bt = 0; bt < sd.nbatch; ++bt) {
+    // ---- gather every needed sample of the batch's windows: asynchronous
+    // 8/16-byte copies straight into shared memory, all in flight at once;
+    // thread = (column lane, row phase)
+    for (int w = 0; w < nw; ++w) {
+      if (sd.batch[w] != bt) continue;
+      const int h = sd.head[w];
+      const Tin* xs = (const Tin*)p.x + (int64_t)s_isig[h] * p.xstride;
+      const int64_t sm = s_isgm[h], tau = s_itau[h];
+      const int back = sd.back[w], rows = R + back;
+      const int lo = s_lo[w][lane], hi = s_hi[w][lane];
+      Tin* vw = V + (int64_t)sd.row0[w] * kGfCols + lane;
+      const int64_t base = (int64_t)(col0 + lane) - tau;
+      for (int vr = warp; vr < rows; vr += kGfNT / 32) {
+        const int v = vr - back;
+        if (v < -lo || v >= hi) continue;
+        const int64_t idx = mulmod(sm, pmod(base + (int64_t)v * B, n), n);
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(vw + vr * kGfCols);
+        if (sizeof(Tin) == 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(xs + idx)
+                       : "memory");
+        else
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(xs + idx)
                        : "memory");
       }
     }
-  }
-  for (int first = rfirst; first < rfirst + rcnt; first += 32) {
-    const int cnt = min(32, rfirst + rcnt - first);
-    uint32_t left = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
-    // windows: the first item left is the base (its signal, sigma, tau_h);
-    // every item of the same signal and sigma within A rows behind it joins;
-    // the rest (the ladder's N/16 shift) forms the next window
-    while (left) {
-      const int h = first + __ffs(left) - 1;
-      const int sigh = p.item_sig ? p.item_sig[h] : h;
-      const int64_t sgm = p.item_a[h], tau_h = p.item_b[h];
-      uint32_t win = 0;
-      int maxo = -1, vhi = 0;
-      for (uint32_t m = left; m; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const int it = first + j;
-        if ((p.item_sig ? p.item_sig[it] : it) != sigh || p.item_a[it] != sgm) continue;
-        const int64_t d = pmod(p.item_b[it] - tau_h, n);
-        const int cj = (int)(d % B);
-        const int64_t o = d / B + (col + cj >= B);
-        if (o > A) continue;
-        const int s = col + cj - ((col + cj >= B) ? B : 0);
-        const int nr = s < omega ? (omega - s + B - 1) / B : 0;
-        win |= 1u << j;
-        maxo = max(maxo, (int)o);
-        vhi = max(vhi, nr - (int)o);
-      }
-      left &= ~win;
-      // gather the column's window rows once, a chunk of loads in flight, raw
-      // samples to shared memory (the column is this thread's own: no barrier)
-      {
-        constexpr int CH = sizeof(Tin) == 8 ? 8 : 4;
-        const Tin* xs = (const Tin*)p.x + (int64_t)sigh * p.xstride;
-        const int64_t step = mulmod(sgm, (int64_t)B % n, n);
-        int64_t idx = mulmod(sgm, pmod((int64_t)col - (int64_t)maxo * B - tau_h, n), n);
-        Tin* vc = V + threadIdx.x;
-        const int nv = vhi + maxo;
-        if (async) {
-          // every row of the window in flight at once, no registers held:
-          // asynchronous copies straight into the thread's column
-          uint32_t sa = (uint32_t)__cvta_generic_to_shared(vc);
-          for (int v = 0; v < nv; ++v) {
-            if (sizeof(Tin) == 8)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(xs + idx)
-                           : "memory");
-            else
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(xs + idx)
-                           : "memory");
-            sa += kRfNT * (uint32_t)sizeof(Tin);
-            idx += step;
-            idx -= (idx >= n) ? n : 0;
-          }
-          asm volatile("cp.async.commit_group;\n" ::: "memory");
-          asm volatile("cp.async.wait_all;\n" ::: "memory");
-        }
-        for (int v = 0; v < (async ? 0 : nv); v += CH) {
-          Tin t[CH];
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    // ---- warp j folds item j (of this batch) for its 32 columns; its taps
+    // are requested before the wait, so their L2 round trip overlaps the
+    // gathers' DRAM one
+    const int j = warp;
+    const bool act = j < cnt && sd.batch[sd.win[j]] == bt && col0 + lane < B;
+    int s = 0, nr = 0;
+    const Tin* vc = V;
+    double t[kGfTapRegs];  // every tap of the slot in flight at once (R <= kGfTapRegs)
+    if (act) {
+      const int w = sd.win[j];
+      const int gc = col0 + lane;
+      const int cj = sd.c[j];
+      const int wrap = gc + cj >= B;
+      const int o = sd.a[j] + wrap;
+      s = gc + cj - (wrap ? B : 0);
+      nr = R - (s >= tail);
+      vc = V + (int64_t)(sd.row0[w] + sd.back[w] - o) * kGfCols + lane;  // row r at vc[r C]
+      const double* tg = p.taps + s;
 #pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            if (v + u < nv) t[u] = __ldcg(xs + idx);
-            idx += step;
-            idx -= (idx >= n) ? n : 0;
-          }
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (v + u < nv) vc[(v + u) * kRfNT] = t[u];
-        }
-      }
-      // the window's items, grouped by c = shift mod B: the items of one c
-      // read the same taps g[col + c + tB] (t = r - wrap), held in registers
-      uint32_t todo = win;
-      while (todo) {
-        const int c = (int)(pmod(p.item_b[first + __ffs(todo) - 1] - tau_h, n) % B);
-        const int w = (col + c >= B);
-        const int s = col + c - (w ? B : 0);
-        const int nr = s < omega ? (omega - s + B - 1) / B : 0;
-        double T[kRfT];  // T[t + 1] = g[col + c + tB], t = -1 .. kRfT - 2
-        {
-          const double* tp = p.taps + (col + c - B);
-          const int tcnt = (omega - (col + c) + 2 * B - 1) / B;  // valid: t < tcnt
-#pragma unroll
-          for (int t = 0; t < kRfT; ++t)
-            T[t] = (t >= 1 - w && t < tcnt) ? __ldg(tp + t * B) : 0.0;
-        }
-        for (uint32_t m = todo; m; m &= m - 1) {
-          const int j = __ffs(m) - 1;
-          const int it = first + j;
-          const int64_t d = pmod(p.item_b[it] - tau_h, n);
-          if ((int)(d % B) != c) continue;
-          todo &= ~(1u << j);
-          const int o = (int)(d / B) + w;
-          const Tin* vc = V + (maxo - o) * kRfNT + threadIdx.x;  // row r at vc[r NT]
-          double2 acc = cmk(0.0, 0.0);
-          if (w) {
-#pragma unroll
-            for (int r = 0; r < kRfT; ++r)
-              if (r < nr) {
-                const double2 v = to_d2_(vc[r * kRfNT]);
-                acc = cadd_rn(acc, cmk(__dmul_rn(T[r], v.x), __dmul_rn(T[r], v.y)));
-              }
-          } else {
-#pragma unroll
-            for (int r = 0; r + 1 < kRfT; ++r)
-              if (r < nr) {
-                const double2 v = to_d2_(vc[r * kRfNT]);
-                acc = cadd_rn(acc, cmk(__dmul_rn(T[r + 1], v.x), __dmul_rn(T[r + 1], v.y)));
-              }
-          }
-          out[out_row(p, it) * p.B + s] = acc;
-        }
-      }
+      for (int r = 0; r < kGfTapRegs; ++r) t[r] = r < nr ? __ldg(tg + r * B) : 0.0;
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    if (act) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < kGfTapRegs; ++r)
+        if (r < nr) {
+          const double2 v = to_d2_(vc[r * kGfCols]);
+          acc = cadd_rn(acc, cmk(__dmul_rn(t[r], v.x), __dmul_rn(t[r], v.y)));
+        }
+      out[out_row(p, first + j) * p.B + s] = acc;
+    }
+    if (bt + 1 < sd.nbatch) __syncthreads();  // the next batch reuses the shared memory
   }
 }
 
@@ -1045,16 +1082,108 @@ int run_bucketize(int dtype, int mode, const Prod& p0, int64_t nitems, const dou
   return prof_end(st, ev0);
 }
 
-// Flat bucketizations grouped in permutation runs (items [run_first[r],
-// run_first[r] + run_cnt[r]) share signal and sigma; b' = 0, no gates): the
-// run fold into each item's output row, then the FFT of every row in place.
-// Profiled (when on) as one bucketization launch of nitems items.
-int run_flat_runs(int dtype, const Prod& p0, const int32_t* run_first, const int32_t* run_cnt,
-                  int64_t nruns, int64_t nitems, const double2* W, double2* out, void* ws,
-                  size_t ws_bytes, cudaStream_t st) {
-  if (nruns <= 0 || nitems <= 0) return 0;
+// In-place FFT of folded rows (the group fold's second pass), power-of-two
+// B <= 4096: one CTA per row, the row in shared memory (coalesced in and
+// out), radix-8 DIF stages (the same butterflies and twiddles as fft_pow2, so
+// the values are bit-identical to the cluster path), twiddles read through
+// L1.  Shared-memory index i lives at i + i/8 + i/512: conflict-free for the
+// unit-stride stage loads, the stride-8 last stage and the stride-512
+// digit-reversed read-out.
+constexpr int kFrowNT = 512;
+__device__ __forceinline__ int frow_pad(int i) { return i + (i >> 3) + (i >> 9); }
+
+template <int M>
+__global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict__ item_row,
+                                                     const double2* __restrict__ W,
+                                                     double2* __restrict__ y) {
+  extern __shared__ double2 fr_s[];
+  double2* row = y + (int64_t)item_row[blockIdx.x] * M;
+  for (int k = threadIdx.x; k < M; k += kFrowNT) fr_s[frow_pad(k)] = row[k];
+  __syncthreads();
+  int Mb = M;
+#pragma unroll 1
+  for (int st = 0; st < Pow2<M>::N8; ++st) {
+    const int Mp = Mb >> 3;
+    const int tstr = M / Mb;
+    for (int t = threadIdx.x; t < M / 8; t += kFrowNT) {
+      const int blk = t / Mp, j = t - blk * Mp;
+      const int base = blk * Mb + j;
+      double2 a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = fr_s[frow_pad(base + q * Mp)];
+      dft8_(a);
+      fr_s[frow_pad(base)] = a[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q)
+        fr_s[frow_pad(base + q * Mp)] = j ? cmul(a[q], __ldg(W + j * q * tstr)) : a[q];
+    }
+    __syncthreads();
+    Mb = Mp;
+  }
+  if (Pow2<M>::RL == 4) {
+    for (int t = threadIdx.x; t < M / 4; t += kFrowNT) {
+      double2 x0 = fr_s[frow_pad(4 * t)], x1 = fr_s[frow_pad(4 * t + 1)];
+      double2 x2 = fr_s[frow_pad(4 * t + 2)], x3 = fr_s[frow_pad(4 * t + 3)];
+      dft4_(x0, x1, x2, x3);
+      fr_s[frow_pad(4 * t)] = x0;
+      fr_s[frow_pad(4 * t + 1)] = x1;
+      fr_s[frow_pad(4 * t + 2)] = x2;
+      fr_s[frow_pad(4 * t + 3)] = x3;
+    }
+    __syncthreads();
+  } else if (Pow2<M>::RL == 2) {
+    for (int t = threadIdx.x; t < M / 2; t += kFrowNT) {
+      const double2 u = fr_s[frow_pad(2 * t)], v = fr_s[frow_pad(2 * t + 1)];
+      fr_s[frow_pad(2 * t)] = cadd(u, v);
+      fr_s[frow_pad(2 * t + 1)] = csub(u, v);
+    }
+    __syncthreads();
+  }
+  const double bd = (double)M;
+  for (int k = threadIdx.x; k < M; k += kFrowNT)
+    row[k] = cdivr(fr_s[frow_pad(pow2_pos<M>(k))], bd);
+}
+
+static int launch_fft_rows(const int32_t* item_row, int64_t nitems, int64_t B, const double2* W,
+                           double2* y, cudaStream_t st) {
+  const size_t sm = (size_t)(B + B / 8 + B / 512 + 1) * sizeof(double2);
+  switch (B) {
+    case 4096:
+      SFFT_CUDA(cudaFuncSetAttribute(k_fft_rows<4096>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_fft_rows<4096><<<(unsigned)nitems, kFrowNT, sm, st>>>(item_row, W, y);
+      break;
+    case 2048:
+      if (ensure_smem(k_fft_rows<2048>, sm)) return -3;
+      k_fft_rows<2048><<<(unsigned)nitems, kFrowNT, sm, st>>>(item_row, W, y);
+      break;
+    case 1024:
+      if (ensure_smem(k_fft_rows<1024>, sm)) return -3;
+      k_fft_rows<1024><<<(unsigned)nitems, kFrowNT, sm, st>>>(item_row, W, y);
+      break;
+    default:
+      return 1;  // not handled here
+  }
+  SFFT_CHECK_LAUNCH("k_fft_rows");
+  return 0;
+}
+
+// Flat bucketizations in item groups (items [gfirst[g], gfirst[g] + gcnt[g]),
+// at most kGfItems, whole permutation runs of one slot; b' = 0, no gates):
+// the group fold into each item's output row, then the FFT of every row in
+// place.  Profiled (when on) as one bucketization launch of nitems items.
+size_t flat_groups_desc_bytes(int64_t ngroups) { return (size_t)ngroups * sizeof(GfDesc); }
+
+int run_flat_groups(int dtype, const Prod& p0, const int32_t* gfirst, const int32_t* gcnt,
+                    int64_t ngroups, int64_t nitems, const double2* W, double2* out, void* ws,
+                    size_t ws_bytes, void* desc_ws, cudaStream_t st) {
+  if (ngroups <= 0 || nitems <= 0) return 0;
   SFFT_REQUIRE(!p0.item_c && !p0.active && !p0.item_active && p0.item_row,
-               "run fold: needs an ungated item list with output rows and b' = 0");
+               "group fold: needs an ungated item list with output rows and b' = 0");
+  const int R = (int)cdiv_up(p0.omega, p0.B);
+  if (R + std::min(kGfBack, R - 1) + 1 > kGfRows || R > kGfTapRegs || p0.B >= (1 << 30) ||
+      p0.omega >= (1 << 30))
+    return run_bucketize(dtype, PROD_FLAT, p0, nitems, W, out, ws, ws_bytes, st);
   gather_fetch_granularity();
   BucketProf& bp = bucket_prof();
   Prod p = p0;
@@ -1064,29 +1193,32 @@ int run_flat_runs(int dtype, const Prod& p0, const int32_t* run_first, const int
     int rc = prof_begin(st, &ev0);
     if (rc) return rc;
   }
-  const int R = (int)cdiv_up(p.omega, p.B);
-  if (R >= kRfT || p.B >= (1 << 30) || p.omega >= (1 << 30))  // per-item kernels
-    return run_bucketize(dtype, PROD_FLAT, p0, nitems, W, out, ws, ws_bytes, st);
-  const int wrows = R + (int)std::min<int64_t>(kRfMaxBack, std::max(R - 1, 0));
-  const dim3 g((unsigned)cdiv_up(p.B, kRfNT), (unsigned)nruns);
-  // SFFT_RF_SMEM=<bytes>: pad the dynamic shared memory (occupancy experiments)
-  const size_t pad = getenv("SFFT_RF_SMEM") ? (size_t)atoll(getenv("SFFT_RF_SMEM")) : 0;
-  const int async = getenv("SFFT_RF_ASYNC") ? atoi(getenv("SFFT_RF_ASYNC")) : 0;
-  const int prefetch = getenv("SFFT_RF_PREFETCH") ? atoi(getenv("SFFT_RF_PREFETCH")) : 0;
+  GfDesc* desc = (GfDesc*)desc_ws;
+  k_gf_prep<<<(unsigned)cdiv_up(ngroups, 128), 128, 0, st>>>(p, gfirst, gcnt, ngroups, desc);
+  SFFT_CHECK_LAUNCH("k_gf_prep");
+  const dim3 g((unsigned)cdiv_up(p.B, kGfCols), (unsigned)ngroups);
   if (dtype == 0) {
-    const size_t sm = std::max(pad, (size_t)wrows * kRfNT * sizeof(float2));
-    if (ensure_smem(k_run_fold<float2>, sm)) return -3;
-    k_run_fold<float2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out, async, prefetch);
+    const size_t sm = (size_t)kGfRows * kGfCols * sizeof(float2);
+    SFFT_CUDA(cudaFuncSetAttribute(k_group_fold<float2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_group_fold<float2><<<g, kGfNT, sm, st>>>(p, gfirst, gcnt, desc, out);
   } else {
-    const size_t sm = std::max(pad, (size_t)wrows * kRfNT * sizeof(double2));
-    if (ensure_smem(k_run_fold<double2>, sm)) return -3;
-    k_run_fold<double2><<<g, kRfNT, sm, st>>>(p, run_first, run_cnt, wrows, out, async, prefetch);
+    const size_t sm = (size_t)kGfRows * kGfCols * sizeof(double2);
+    SFFT_CUDA(cudaFuncSetAttribute(k_group_fold<double2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_group_fold<double2><<<g, kGfNT, sm, st>>>(p, gfirst, gcnt, desc, out);
   }
-  SFFT_CHECK_LAUNCH("k_run_fold");
-  Prod pl = p;
-  pl.z = out;
-  pl.prof_items = nullptr;
-  int rc = run_bucketize_inner(dtype, PROD_LOAD, pl, nitems, W, out, ws, ws_bytes, st);
+  SFFT_CHECK_LAUNCH("k_group_fold");
+  // SFFT_GF_FFT=cluster keeps the cluster FFT pass (A/B measurements)
+  const char* fe = getenv("SFFT_GF_FFT");
+  int rc = 1;
+  if (!(fe && !strcmp(fe, "cluster"))) rc = launch_fft_rows(p.item_row, nitems, p.B, W, out, st);
+  if (rc > 0) {
+    Prod pl = p;
+    pl.z = out;
+    pl.prof_items = nullptr;
+    rc = run_bucketize_inner(dtype, PROD_LOAD, pl, nitems, W, out, ws, ws_bytes, st);
+  }
   if (rc) return rc;
   return bp.on ? prof_end(st, ev0) : 0;
 }

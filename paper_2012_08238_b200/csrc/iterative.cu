@@ -285,6 +285,35 @@ __device__ __forceinline__ int64_t role_shift(const IterArgs& a, const IterState
   return (S.phase == PH_LOOP) ? a.shifts[j] : (int64_t)j;
 }
 
+// Greedy packing of a slot's permutation chunks (the items of one
+// permutation, in emission order) into groups of at most kGfItems items: a
+// chunk that does not fit the open group starts a new one; chunks longer than
+// a group are split.  Counting (plan) and emission (fill) share it.
+struct GroupPack {
+  int cur = 0;  // items in the open group
+  int go = 0;   // next group index
+  int32_t* gf = nullptr;
+  int32_t* gc = nullptr;
+  __device__ void chunk(int first_item, int z) {
+    if (cur > 0 && cur + z > kGfItems) cur = 0;
+    while (z > 0) {
+      if (cur == 0) {
+        if (gf) {
+          gf[go] = first_item;
+          gc[go] = 0;
+        }
+        ++go;
+      }
+      const int take = min(z, kGfItems - cur);
+      if (gc) gc[go - 1] += take;
+      cur += take;
+      z -= take;
+      first_item += take;
+      if (cur == kGfItems) cur = 0;
+    }
+  }
+};
+
 __global__ void k_cb_plan(IterArgs a) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= a.S) return;
@@ -305,16 +334,20 @@ __global__ void k_cb_plan(IterArgs a) {
     }
     a.role_src[(int64_t)s * a.M + j] = src;
   }
-  int spec = 0, runs = nm > 0;
-  if (first)
+  int spec = 0;
+  GroupPack gp;
+  if (nm > 0) gp.chunk(0, nm);
+  if (first) {
     for (int c = 0; c < a.C; ++c) {
       const int pp = S.pidx + 1 + (c < a.M ? 0 : 1 + (c - a.M) / 3);
       spec += pp < a.P;
-      // a new run at each permutation's first shift
-      runs += pp < a.P && (c == 0 || (c >= a.M && (c - a.M) % 3 == 0));
     }
+    if (S.pidx + 1 < a.P) gp.chunk(0, a.M);  // the next loop permutation's ladder
+    for (int c = a.M; c < a.C; c += 3)        // polish permutations, 3 shifts each
+      if (S.pidx + 2 + (c - a.M) / 3 < a.P) gp.chunk(0, 3);
+  }
   a.cnt[s] = nm + spec;
-  a.rcnt[s] = runs;
+  a.rcnt[s] = gp.go;
 }
 
 // exclusive scan of cnt[0..S) in place, total in cnt[S] (one CTA)
@@ -351,7 +384,10 @@ __global__ void k_cb_fill(IterArgs a) {
   if (s >= a.S) return;
   const IterState& S = a.st[s];
   int o = a.cnt[s];
-  int ro = a.rcnt[s];
+  GroupPack gp;
+  gp.go = a.rcnt[s];
+  gp.gf = a.run_first;
+  gp.gc = a.run_cnt;
   const int sig = S.sig > 0 ? S.sig : 0;
   const int o_own = o;
   for (int j = 0; j < S.nsh && j < a.M; ++j) {
@@ -362,11 +398,7 @@ __global__ void k_cb_fill(IterArgs a) {
     a.it2_row[o] = j * a.S + s;
     ++o;
   }
-  if (o > o_own) {
-    a.run_first[ro] = o_own;
-    a.run_cnt[ro] = o - o_own;
-    ++ro;
-  }
+  if (o > o_own) gp.chunk(o_own, o - o_own);
   if (!(S.phase == PH_LOOP && S.it == 1)) return;
   int32_t* dp = a.dir_p + (int64_t)s * a.C;
   int64_t* dd = a.dir_d + (int64_t)s * a.C;
@@ -375,12 +407,8 @@ __global__ void k_cb_fill(IterArgs a) {
     if (pp >= a.P) continue;
     const int64_t d = c < a.M ? a.shifts[c] : (int64_t)((c - a.M) % 3);
     const int64_t row = (int64_t)sig * a.pstride + pp;
-    if (c == 0 || (c >= a.M && (c - a.M) % 3 == 0)) {  // a permutation's first shift
-      a.run_first[ro] = o;
-      a.run_cnt[ro] = 0;
-      ++ro;
-    }
-    a.run_cnt[ro - 1] += 1;
+    if (c == 0) gp.chunk(o, a.M);                              // ladder permutation
+    else if (c >= a.M && (c - a.M) % 3 == 0) gp.chunk(o, 3);  // polish permutation
     a.it2_sig[o] = sig;
     a.it2_sigma[o] = a.psig[row];
     a.it2_tau[o] = pmod(pmod(a.ptau[row], a.n) + d, a.n);
@@ -1342,6 +1370,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
   }
   if (t < T) corr[(int64_t)s * a.cap + t] = mine;
   double2 r[3];
+#pragma unroll
   for (int d = 0; d < 3; ++d) r[d] = mine ? a.y[((int64_t)d * a.S + s) * B + bi] : cmk(0, 0);
   for (int u0 = 0; u0 < T; u0 += kPoChunk) {
     __syncthreads();
@@ -1383,6 +1412,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
   }
   if (mine) {
     double2 acc = cmk(0.0, 0.0);
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int64_t ex = pmod(-mulmod(pmod(tau + d, n), m, n), n);
       acc = cadd(acc, cmul(r[d], unit_root(n, ex)));
@@ -1487,6 +1517,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * kResPre,                    // 45 residual pre-check buckets
       sizeof(int32_t) * (size_t)(S + 1),                        // 46 rcnt
       sizeof(int32_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 47 run_first + run_cnt
+      flat_groups_desc_bytes((int64_t)S * (M + spec_rows(M))),  // 48 group descriptors
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1789,10 +1820,12 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   };
   int nit = 0;  // planned items of the coming round (row-cache path)
   int nrun = 0;  // their permutation runs
-  // permutation-run fold (one gather per sample of a run): c64/c128 flat items
-  // with b' = 0 on the row-cache path, SFFT_RUN_FOLD=1 (A/B measurements;
-  // parity tests run both); default the per-item cluster kernel
-  const bool run_fold_off = !(getenv("SFFT_RUN_FOLD") && atoi(getenv("SFFT_RUN_FOLD")));
+  // item-group fold (one gather per sample of a permutation window, the
+  // measurements of a slot's permutations folded from shared memory, then the
+  // row FFTs): c64/c128 flat items with b' = 0 on the row-cache path.
+  // SFFT_RUN_FOLD=0 keeps the per-item cluster kernel (A/B measurements;
+  // the parity tests run both)
+  const bool run_fold_off = getenv("SFFT_RUN_FOLD") && !atoi(getenv("SFFT_RUN_FOLD"));
   {
     int rc0 = prologue();
     if (rc0) return rc0;
@@ -1810,8 +1843,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
       k_cb_copy<<<(unsigned)(S * M), 256, 0, st>>>(a);
       SFFT_CHECK_LAUNCH("k_cb_copy");
       if (nit > 0 && !run_fold_off)
-        rc = run_flat_runs(dtype, pc, a.run_first, a.run_cnt, nrun, nit, W, a.y, bws, bws_bytes,
-                           st);
+        rc = run_flat_groups(dtype, pc, a.run_first, a.run_cnt, nrun, nit, W, a.y, bws,
+                             bws_bytes, w + Lo.off[48], st);
       else if (nit > 0)
         rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
     } else {

@@ -58,11 +58,14 @@ size_t bucketize_ws_bytes(int64_t B, int64_t nitems);
 int run_bucketize(int dtype, int mode, const Prod& p, int64_t nitems, const double2* W,
                   double2* out, void* ws, size_t ws_bytes, cudaStream_t st);
 int run_twiddle(double2* W, int64_t B, cudaStream_t st);
-// permutation runs of flat items (iterative ladder / polish): one gather per
-// sample of a run, then the FFTs in place (bucketize.cu)
-int run_flat_runs(int dtype, const Prod& p, const int32_t* run_first, const int32_t* run_cnt,
-                  int64_t nruns, int64_t nitems, const double2* W, double2* out, void* ws,
-                  size_t ws_bytes, cudaStream_t st);
+constexpr int kGfItems = 8;  // items per group of the group fold (one warp each per column half)
+
+// item groups of flat items (iterative ladder / polish permutations of one
+// slot): one gather per sample of a window, then the FFTs in place (bucketize.cu)
+size_t flat_groups_desc_bytes(int64_t ngroups);  // scratch for the per-group descriptors
+int run_flat_groups(int dtype, const Prod& p, const int32_t* gfirst, const int32_t* gcnt,
+                    int64_t ngroups, int64_t nitems, const double2* W, double2* out, void* ws,
+                    size_t ws_bytes, void* desc_ws, cudaStream_t st);
 // Dirichlet bank (sfft/bucketize.py:181-211): per-offset transforms y [noff][B]
 // (forward FFT of the conjugated fold / B) combined into out [B]
 int run_dirichlet_combine(const double2* y, int64_t noff, const int64_t* offsets, int64_t n,
