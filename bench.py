@@ -51,9 +51,10 @@ def parse():
     return ap.parse_args()
 
 
-KERNEL_DESC = ("bucketization launches of the step: k_run_fold (one gather per sample of a "
-               "(signal, sigma) run, every shift folded from the thread's shared-memory column) "
-               "+ the in-place cluster FFT pass k_cluster<PROD_LOAD,8,512>")
+KERNEL_DESC = ("bucketization launches of the step: k_gf_prep + k_group_fold (item groups of a "
+               "slot's permutations; one gather per sample of a permutation window into shared "
+               "memory, every shift folded from there) + k_fft_rows (in-place radix-8 row FFT); "
+               "later-round misses the same way")
 
 
 def peaks():

@@ -619,8 +619,6 @@ __global__ void __launch_bounds__(kGfNT, 4)
   extern __shared__ __align__(16) unsigned char gf_smem[];
   Tin* V = reinterpret_cast<Tin*>(gf_smem);  // [kGfRows][kGfCols]
   __shared__ GfDesc sd;
-  __shared__ short s_lo[kGfItems][kGfCols];  // window w, column: rows [-lo, hi) needed
-  __shared__ short s_hi[kGfItems][kGfCols];
   __shared__ int s_isig[kGfItems];
   __shared__ int64_t s_isgm[kGfItems], s_itau[kGfItems];
   const int g = blockIdx.y;
@@ -645,27 +643,6 @@ __global__ void __launch_bounds__(kGfNT, 4)
   }
   __syncthreads();
   const int nw = sd.nwin;
-  // ---- per (window, column): the rows any of its items needs
-  if (threadIdx.x < nw * kGfCols) {
-    const int w = threadIdx.x / kGfCols, c = threadIdx.x % kGfCols;
-    const int gc = col0 + c;
-    int lo = 0, hi = 0;
-    if (gc < B)
-      for (int j = 0; j < cnt; ++j) {
-        if (sd.win[j] != w) continue;
-        const int wrap = gc + sd.c[j] >= B;
-        const int o = sd.a[j] + wrap;
-        const int s = gc + sd.c[j] - (wrap ? B : 0);
-        const int nr = R - (s >= tail);  // rows with s + rB < Omega (s < B <= Omega)
-        if (nr > 0) {
-          lo = max(lo, o);
-          hi = max(hi, nr - o);
-        }
-      }
-    s_lo[w][c] = (short)lo;
-    s_hi[w][c] = (short)hi;
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int bt = 0; bt < sd.nbatch; ++bt) {
     // ---- gather every needed sample of the batch's windows: asynchronous
@@ -677,7 +654,23 @@ __global__ void __launch_bounds__(kGfNT, 4)
       const Tin* xs = (const Tin*)p.x + (int64_t)s_isig[h] * p.xstride;
       const int64_t sm = s_isgm[h], tau = s_itau[h];
       const int back = sd.back[w], rows = R + back;
-      const int lo = s_lo[w][lane], hi = s_hi[w][lane];
+      // rows [-lo, hi) any item of the window needs in this lane's column
+      int lo = 0, hi = 0;
+      {
+        const int gc = col0 + lane;
+        if (gc < B)
+          for (int j = 0; j < cnt; ++j) {
+            if (sd.win[j] != w) continue;
+            const int wrap = gc + sd.c[j] >= B;
+            const int o = sd.a[j] + wrap;
+            const int s = gc + sd.c[j] - (wrap ? B : 0);
+            const int nr = R - (s >= tail);  // rows with s + rB < Omega (s < B)
+            if (nr > 0) {
+              lo = max(lo, o);
+              hi = max(hi, nr - o);
+            }
+          }
+      }
       Tin* vw = V + (int64_t)sd.row0[w] * kGfCols + lane;
       const int64_t base = (int64_t)(col0 + lane) - tau;
       for (int vr = warp; vr < rows; vr += kGfNT / 32) {

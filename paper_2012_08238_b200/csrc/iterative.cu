@@ -168,32 +168,47 @@ __device__ __forceinline__ void ht_insert(const IterArgs& a, int s, int64_t f, i
 }
 
 // ------------------------------------------------------------------ rounds
-// Admission: a free slot takes the next queued signal.
-__global__ void k_cb_admit(IterArgs a) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
-  IterState& S = a.st[s];
-  if (S.phase != PH_FREE) return;
-  // signals still being copied in (streaming admission) are not taken yet
-  const int lim = a.avail ? min(a.Q, *(volatile const int32_t*)a.avail) : a.Q;
-  // The queue head never moves past this thread's limit: a CAS loop instead of
-  // add-then-roll-back, so a thread holding an older (smaller) limit cannot undo
-  // an admission made by a thread that already saw the raised limit.
-  int idx = *(volatile int32_t*)(a.stats + 4);
-  while (idx < lim) {
-    const int prev = atomicCAS(a.stats + 4, idx, idx + 1);
-    if (prev == idx) break;
-    idx = prev;
+// Admission: free slots take the next queued signals, in slot order.  One
+// CTA owns the queue head: it reads the streaming limit once, ranks the free
+// slots with a block scan and hands out [head, min(head + free, limit)) --
+// no atomics, so a concurrently raised limit can never make two slots take
+// the same signal or skip one.
+constexpr int kAdmNT = 1024;
+__global__ void __launch_bounds__(kAdmNT) k_cb_admit(IterArgs a) {
+  __shared__ int red[32];
+  __shared__ int s_head, s_lim;
+  // signals still being copied in (streaming admission) are not taken yet;
+  // the limit is read once for the whole launch
+  if (threadIdx.x == 0) {
+    s_head = a.stats[4];
+    s_lim = a.avail ? min(a.Q, *(volatile const int32_t*)a.avail) : a.Q;
   }
-  if (idx >= lim) {
-    if (lim >= a.Q) S.phase = PH_IDLE;
-    return;
+  __syncthreads();
+  const int lim = s_lim;
+  for (int base = 0; base < a.S; base += kAdmNT) {
+    const int s = base + threadIdx.x;
+    const bool fr = s < a.S && a.st[s].phase == PH_FREE;
+    int tot;
+    const int rank = block_exscan<kAdmNT>(fr ? 1 : 0, red, &tot);
+    const int head = s_head;
+    if (fr) {
+      IterState& S = a.st[s];
+      const int idx = head + rank;
+      if (idx < lim) {
+        S = IterState{};
+        S.sig = idx;
+        S.phase = PH_LOOP;
+        S.newslot = 1;
+        a.rec_count[s] = 0;
+      } else if (lim >= a.Q) {
+        S.phase = PH_IDLE;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_head = min(head + tot, max(lim, head));
+    __syncthreads();
   }
-  S = IterState{};
-  S.sig = idx;
-  S.phase = PH_LOOP;
-  S.newslot = 1;
-  a.rec_count[s] = 0;
+  if (threadIdx.x == 0) a.stats[4] = s_head;
 }
 
 __global__ void k_cb_clear(IterArgs a) {
@@ -1797,7 +1812,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   // planning).  It runs at the end of the previous round, so that the host
   // reads the next round's item count with the round's one status read.
   auto prologue = [&]() -> int {
-    k_cb_admit<<<sb, 128, 0, st>>>(a);
+    k_cb_admit<<<1, kAdmNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_cb_admit");
     k_cb_clear<<<dim3(16, S), 256, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_cb_clear");
