@@ -12,7 +12,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfft_b200.so")
+# SFFT_LIB_PATH: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("SFFT_LIB_PATH") or os.path.join(HERE, "libsfft_b200.so")
 
 _lock = threading.Lock()
 _lib = None
