@@ -755,13 +755,13 @@ __global__ void __launch_bounds__(kSubNT, 4) k_subtract(
     const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
     const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
     const int32_t* tcount, int64_t tstride, const int32_t* gate, double2* __restrict__ part,
-    RealTab rt) {
+    RealTab rt, const int32_t* __restrict__ list) {
   __shared__ int32_t s_row[kSubChunk];
   __shared__ int32_t s_q[kSubChunk];
   __shared__ double2 s_a[kSubChunk];     // complex: c w^{tau m}; real: beta = c w^{tau m} w^{-m h} / B
   __shared__ double2 s_al[kSubChunk];    // real: alpha = c w^{tau m} t0 / B
   __shared__ double2 s_alsum;
-  const int item = blockIdx.y;
+  const int item = list ? list[blockIdx.y] : blockIdx.y;
   const int sig = item_sig ? item_sig[item] : item;
   if (gate && !gate[sig]) return;
   const int64_t L = n / B;
@@ -917,8 +917,8 @@ __global__ void __launch_bounds__(kSubNT, 4) k_subtract(
 __global__ void k_sub_reduce(const double2* __restrict__ y, double2* __restrict__ out, int64_t B,
                              int64_t nb, const int32_t* blist, const int32_t* item_sig,
                              const int32_t* gate, const double2* __restrict__ part, int maxTS,
-                             const int32_t* tcount) {
-  const int item = blockIdx.y;
+                             const int32_t* tcount, const int32_t* __restrict__ list) {
+  const int item = list ? list[blockIdx.y] : blockIdx.y;
   const int sig = item_sig ? item_sig[item] : item;
   if (gate && !gate[sig]) return;
   const int TS = sub_splits(tcount[sig], maxTS);
@@ -962,23 +962,25 @@ int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
                        const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
                        int64_t tstride, const int32_t* gate, cudaStream_t st, int TS,
-                       double2* part, const RealTab* rt) {
+                       double2* part, const RealTab* rt, const int32_t* list, int64_t nlist) {
+  // list: the items to process (grid over the list instead of every item)
+  if (list) nitems = nlist;
   if (nitems <= 0 || nb <= 0) return 0;
   if (TS < 1 || !part) TS = 1;
   dim3 g((unsigned)cdiv_up(nb, (int64_t)kSubNT * kSubBPT), (unsigned)nitems, (unsigned)TS);
   if (rt && rt->at) {
     k_subtract<true><<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma,
                                            tau_tot, tpos, tcoef, tcount, tstride, gate, part,
-                                           *rt);
+                                           *rt, list);
   } else {
     k_subtract<false><<<g, kSubNT, 0, st>>>(y, out, B, nb, blist, gt, n, item_sig, sigma,
                                             tau_tot, tpos, tcoef, tcount, tstride, gate, part,
-                                            RealTab{});
+                                            RealTab{}, list);
   }
   SFFT_CHECK_LAUNCH("k_subtract");
   if (TS > 1) {
     dim3 g2((unsigned)cdiv_up(nb, 256), (unsigned)nitems);
-    k_sub_reduce<<<g2, 256, 0, st>>>(y, out, B, nb, blist, item_sig, gate, part, TS, tcount);
+    k_sub_reduce<<<g2, 256, 0, st>>>(y, out, B, nb, blist, item_sig, gate, part, TS, tcount, list);
     SFFT_CHECK_LAUNCH("k_sub_reduce");
   }
   return 0;

@@ -131,6 +131,7 @@ struct IterArgs {
   // permutation runs of the compacted list (consecutive items of one signal
   // and sigma): run_first/run_cnt, rcnt = runs per slot then their offsets
   int32_t* rcnt;                 // [S + 1]
+  int32_t* act_list;             // [S] the round's loop slots (compacted in the prologue)
   int32_t* run_first;            // [S*(M+C)]
   int32_t* run_cnt;
 };
@@ -265,6 +266,28 @@ __global__ void k_cb_step(IterArgs a) {
       S.ngroups = g + 1;
     }
   }
+}
+
+// The round's loop slots, compacted (one CTA, slot order): the per-slot
+// kernels of the loop (subtractions, ladder, location) run over this list
+// instead of every slot, so the late rounds -- a few non-converging signals --
+// do not launch hundreds of thousands of empty CTAs.  Count in stats[7].
+__global__ void __launch_bounds__(kAdmNT) k_act_list(IterArgs a) {
+  __shared__ int red[32];
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int base = 0; base < a.S; base += kAdmNT) {
+    const int s = base + threadIdx.x;
+    const bool on = s < a.S && a.active[s];
+    int tot;
+    const int r = block_exscan<kAdmNT>(on ? 1 : 0, red, &tot);
+    if (on) a.act_list[s_base + r] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.stats[7] = s_base;
 }
 
 // Items are slot-major (i = s*M + j) so that the shifted measurements of one
@@ -735,7 +758,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
   __shared__ double2 t_ph[kLocChunk][kMaxShifts];
   __shared__ double2 t_al[kLocChunk][kMaxShifts];
   __shared__ double2 s_al[kMaxShifts];
-  const int s = blockIdx.y;
+  const int s = a.act_list[blockIdx.y];  // grid over the loop slots of the round
   if (!a.active[s]) return;
   const int nh = a.st[s].nheavy;
   const int h0 = blockIdx.x * kLocNT;
@@ -773,7 +796,7 @@ __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   __shared__ double2 t_ph[kLocChunk][kMaxShifts];
   __shared__ double2 t_al[kLocChunk][kMaxShifts];
   __shared__ double2 s_al[kMaxShifts];
-  const int s = blockIdx.y;
+  const int s = a.act_list[blockIdx.y];  // grid over the loop slots of the round
   if (!a.active[s]) return;
   const IterState& S = a.st[s];
   const int nh = S.nheavy;
@@ -1533,6 +1556,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)(S + 1),                        // 46 rcnt
       sizeof(int32_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 47 run_first + run_cnt
       flat_groups_desc_bytes((int64_t)S * (M + spec_rows(M))),  // 48 group descriptors
+      sizeof(int32_t) * (size_t)S,                              // 49 act_list
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1552,6 +1576,7 @@ size_t iterative_ws_bytes(int64_t n, int64_t B, int S, int M, int cap) {
 
 template <int M>
 static int launch_locate_t(const IterArgs& a, int64_t B, int S, int lts, cudaStream_t st) {
+  if (S <= 0) return 0;  // no loop slot this round
   if (lts) {
     dim3 gp((unsigned)cdiv_up(B, kLocNT), S, lts);
     k_it_ladder_part<M><<<gp, kLocNT, 0, st>>>(a);
@@ -1725,6 +1750,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.it2_sigma = (int64_t*)(w + Lo.off[43]);
   a.it2_tau = a.it2_sigma + (size_t)S * (M + spec_rows(M));
   a.rcnt = (int32_t*)(w + Lo.off[46]);
+  a.act_list = (int32_t*)(w + Lo.off[49]);
   a.run_first = (int32_t*)(w + Lo.off[47]);
   a.run_cnt = a.run_first + (size_t)S * (M + spec_rows(M));
   double2* rpre = (double2*)(w + Lo.off[44]);
@@ -1818,6 +1844,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     SFFT_CHECK_LAUNCH("k_cb_clear");
     k_cb_step<<<sb, 128, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_cb_step");
+    k_act_list<<<1, kAdmNT, 0, st>>>(a);
+    SFFT_CHECK_LAUNCH("k_act_list");
     k_po_epoch<<<dim3(4, S), 256, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_po_epoch");
     if (a.C > 0) {
@@ -1835,6 +1863,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   };
   int nit = 0;  // planned items of the coming round (row-cache path)
   int nrun = 0;  // their permutation runs
+  int n_act = S;  // loop slots of the coming round (k_act_list)
   // item-group fold (one gather per sample of a permutation window, the
   // measurements of a slot's permutations folded from shared memory, then the
   // row FFTs): c64/c128 flat items with b' = 0 on the row-cache path.
@@ -1845,11 +1874,16 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     int rc0 = prologue();
     if (rc0) return rc0;
     if (a.C > 0) {
-      int32_t h2[2];
-      SFFT_CUDA(cudaMemcpyAsync(h2, a.stats + 5, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
+    {
+      int32_t h3[3];
+      SFFT_CUDA(cudaMemcpyAsync(h3, a.stats + 5, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       SFFT_CUDA(cudaStreamSynchronize(st));
-      nit = h2[0];
-      nrun = h2[1];
+      if (a.C > 0) {
+        nit = h3[0];
+        nrun = h3[1];
+      }
+      n_act = h3[2];
     }
   }
   for (; round < max_rounds; ++round) {
@@ -1880,13 +1914,13 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     // ---- loop slots
     rc = run_subtract_gated(a.y, a.y, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.rec_pos, a.rec_coef, a.rec_count, cap, a.active, st,
-                            splits(t_max, 128, kMaxSubSplit), a.part, &rt);
+                            splits(t_max, 128, kMaxSubSplit), a.part, &rt, a.act_list, n_act);
     if (rc) return rc;
     k_it_decide<<<S, kDecNT, dsm, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_decide");
     if (loc == 0) {
       const int lts = t_max > 256 ? splits(t_max, 256, kMaxLadSplit) : 0;
-      rc = launch_locate(a, M, B, S, lts, st);
+      rc = launch_locate(a, M, B, n_act, lts, st);
       if (rc) return rc;
     } else {
       const unsigned hb = (unsigned)cdiv_up(B, kSpH);
@@ -1906,14 +1940,14 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
       SFFT_CHECK_LAUNCH("k_resid_list");
       rc = run_subtract_gated(a.y, rpre, B, kResPre, rlist, S, gt, n, nullptr, a.item_sigma,
                               a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
-                              splits(h_max, 128, kMaxSubSplit), a.part, &rt);
+                              splits(h_max, 128, kMaxSubSplit), a.part, &rt, a.act_list, n_act);
       if (rc) return rc;
       k_resid_pre<<<S, 32, 0, st>>>(a, rpre);
       SFFT_CHECK_LAUNCH("k_resid_pre");
     }
     rc = run_subtract_gated(a.y, a.resid, B, B, nullptr, S, gt, n, nullptr, a.item_sigma,
                             a.item_tau, a.fc_pos, a.fc_coef, a.fc_count, B, a.gate, st,
-                            splits(h_max, 128, kMaxSubSplit), a.part, &rt);
+                            splits(h_max, 128, kMaxSubSplit), a.part, &rt, a.act_list, n_act);
     if (rc) return rc;
     k_it_resid<<<S, kDecNT, 0, st>>>(a);
     SFFT_CHECK_LAUNCH("k_it_resid");
@@ -1953,6 +1987,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     h_max = hs[2];
     nit = hs[5];
     nrun = hs[6];
+    n_act = hs[7];
     if (hs[3] >= Q) break;
   }
   SFFT_REQUIRE(round < max_rounds, "iterative: round limit reached (internal error)");

@@ -145,7 +145,8 @@ int run_subtract_gated(const double2* y, double2* out, int64_t B, int64_t nb,
                        const int32_t* item_sig, const int64_t* sigma, const int64_t* tau_tot,
                        const int64_t* tpos, const double2* tcoef, const int32_t* tcount,
                        int64_t tstride, const int32_t* gate, cudaStream_t st, int TS = 1,
-                       double2* part = nullptr, const RealTab* rt = nullptr);
+                       double2* part = nullptr, const RealTab* rt = nullptr,
+                       const int32_t* list = nullptr, int64_t nlist = -1);
 
 // voting.cu
 size_t voting_ws_bytes(int64_t n, int64_t B, int S, int R, int C, int64_t Bpre);
