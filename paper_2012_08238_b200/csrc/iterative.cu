@@ -136,6 +136,18 @@ struct IterArgs {
   int32_t* run_cnt;
 };
 
+// samples_read memo: every signal draws the same seeded permutation stream, so
+// signals that ran the same schedule (the same read groups: most converging
+// signals) read the same index set.  A finishing slot hashes its group list
+// (two independent 64-bit mixes); the first slot with a key computes the
+// exclusion count, the rest take it.  Entries live for one engine call.
+constexpr int kMemo = 8192;  // power of two
+struct SchedMemo {
+  unsigned long long k1[kMemo], k2[kMemo];
+  long long count[kMemo];
+  int32_t ready[kMemo];
+};
+
 __device__ __forceinline__ uint32_t ht_slot(int64_t f, int HT) {
   return (uint32_t)(((unsigned long long)(f + 1) * 0x9E3779B97F4A7C15ull) >> 40) & (HT - 1);
 }
@@ -1557,6 +1569,7 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       sizeof(int32_t) * (size_t)S * (M + spec_rows(M)) * 2,     // 47 run_first + run_cnt
       flat_groups_desc_bytes((int64_t)S * (M + spec_rows(M))),  // 48 group descriptors
       sizeof(int32_t) * (size_t)S,                              // 49 act_list
+      sizeof(SchedMemo) + sizeof(int32_t) * 2 * (size_t)S,       // 50 samples_read memo, own/ent
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1625,6 +1638,84 @@ __global__ void k_cb_finish(IterArgs a, int32_t* fin, int32_t* rows, int32_t* ng
     out_iters[S.sig] = S.iterations;
     out_conv[S.sig] = S.converged;
   }
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long h, unsigned long long v,
+                                                    unsigned long long m) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  h *= m;
+  return h ^ (h >> 31);
+}
+
+// own[s]: 1 = compute, 0 = not finishing / memo hit; ent[s]: memo entry (-1 none)
+__global__ void k_memo_lookup(const Group* __restrict__ groups, const int32_t* ngroups,
+                              const int32_t* fin, const int32_t* rows, SchedMemo* memo,
+                              int64_t* samples, int32_t* own, int32_t* ent, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  own[s] = 0;
+  ent[s] = -1;
+  if (!fin[s]) return;
+  const int G = min(ngroups[s], kMaxGroups);
+  const Group* gs = groups + (int64_t)s * kMaxGroups;
+  unsigned long long h1 = 0x243F6A8885A308D3ull ^ (unsigned long long)G;
+  unsigned long long h2 = 0x13198A2E03707344ull + (unsigned long long)G;
+  for (int g = 0; g < G; ++g) {
+    const Group& q = gs[g];
+    const unsigned long long f[5] = {(unsigned long long)q.a, (unsigned long long)q.tau,
+                                     (unsigned long long)q.cnt, (unsigned long long)q.kind,
+                                     (unsigned long long)q.nsh};
+    for (int i = 0; i < 5; ++i) {
+      h1 = mix64(h1, f[i], 0xBF58476D1CE4E5B9ull);
+      h2 = mix64(h2, f[i], 0x94D049BB133111EBull);
+    }
+    const int ns = q.kind == 2 ? 1 : min(q.nsh, kMaxShifts);
+    for (int i = 0; i < ns; ++i) {
+      h1 = mix64(h1, (unsigned long long)q.sh[i], 0xBF58476D1CE4E5B9ull);
+      h2 = mix64(h2, (unsigned long long)q.sh[i], 0x94D049BB133111EBull);
+    }
+  }
+  if (h1 == 0) h1 = 1;
+  uint32_t e = (uint32_t)(h1 >> 17) & (kMemo - 1);
+  for (int probe = 0; probe < kMemo; ++probe, e = (e + 1) & (kMemo - 1)) {
+    const unsigned long long old = atomicCAS(&memo->k1[e], 0ull, h1);
+    if (old == 0ull) {  // new key: this slot computes
+      memo->k2[e] = h2;
+      own[s] = 1;
+      ent[s] = (int)e;
+      return;
+    }
+    if (old == h1) {
+      // the same schedule (k2 is written right after the claim of k1; a slot
+      // that cannot confirm it this round computes on its own)
+      const unsigned long long o2 = *(volatile unsigned long long*)&memo->k2[e];
+      if (o2 != h2) break;
+      if (*(volatile int32_t*)&memo->ready[e]) {
+        samples[rows[s]] = memo->count[e];
+      } else {
+        ent[s] = (int)e;  // same round as its owner: copied after the count
+      }
+      return;
+    }
+  }
+  own[s] = 1;  // table full or unconfirmed key: compute without the memo
+}
+
+// after the exclusion count: owners publish, then same-round followers copy
+__global__ void k_memo_publish(const int32_t* own, const int32_t* ent, const int32_t* rows,
+                               SchedMemo* memo, const int64_t* samples, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S || !own[s] || ent[s] < 0) return;
+  memo->count[ent[s]] = samples[rows[s]];
+  __threadfence();
+  memo->ready[ent[s]] = 1;
+}
+
+__global__ void k_memo_copy(const int32_t* fin, const int32_t* own, const int32_t* ent,
+                            const int32_t* rows, const SchedMemo* memo, int64_t* samples, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S || !fin[s] || own[s] || ent[s] < 0) return;
+  samples[rows[s]] = memo->count[ent[s]];
 }
 
 __global__ void k_cb_release(IterArgs a) {
@@ -1751,6 +1842,10 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.it2_tau = a.it2_sigma + (size_t)S * (M + spec_rows(M));
   a.rcnt = (int32_t*)(w + Lo.off[46]);
   a.act_list = (int32_t*)(w + Lo.off[49]);
+  SchedMemo* memo = (SchedMemo*)(w + Lo.off[50]);
+  int32_t* m_own = (int32_t*)(memo + 1);
+  int32_t* m_ent = m_own + S;
+  const bool memo_off = getenv("SFFT_NO_SCHED_MEMO") && atoi(getenv("SFFT_NO_SCHED_MEMO"));
   a.run_first = (int32_t*)(w + Lo.off[47]);
   a.run_cnt = a.run_first + (size_t)S * (M + spec_rows(M));
   double2* rpre = (double2*)(w + Lo.off[44]);
@@ -1785,6 +1880,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   SFFT_CUDA(cudaMemsetAsync(a.st, 0, sizeof(IterState) * S, st));
   SFFT_CUDA(cudaMemsetAsync(a.stats, 0, sizeof(int32_t) * 8, st));
   SFFT_CUDA(cudaMemsetAsync(a.rec_count, 0, sizeof(int32_t) * S, st));
+  SFFT_CUDA(cudaMemsetAsync(memo, 0, sizeof(SchedMemo), st));
 
   Prod p{};
   p.x = x;
@@ -1969,9 +2065,22 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     k_finalize<<<S, kFinNT, dsm, st>>>(a.rec_pos, a.rec_coef, a.rec_count, cap, k, out_pos,
                                         out_coef, out_n, fin, rows);
     SFFT_CHECK_LAUNCH("k_finalize");
-    rc = run_union_count(a.groups, ngroups, S, n, out_samples, fin, rows, st,
-                        (int32_t*)(w + Lo.off[31]));
+    // samples_read: memo hits take the count of an identical schedule; the
+    // first slot of each schedule computes it (SFFT_NO_SCHED_MEMO=1: all compute)
+    if (!memo_off) {
+      k_memo_lookup<<<sb, 128, 0, st>>>(a.groups, ngroups, fin, rows, memo, out_samples, m_own,
+                                        m_ent, S);
+      SFFT_CHECK_LAUNCH("k_memo_lookup");
+    }
+    rc = run_union_count(a.groups, ngroups, S, n, out_samples, memo_off ? fin : m_own, rows, st,
+                         (int32_t*)(w + Lo.off[31]));
     if (rc) return rc;
+    if (!memo_off) {
+      k_memo_publish<<<sb, 128, 0, st>>>(m_own, m_ent, rows, memo, out_samples, S);
+      SFFT_CHECK_LAUNCH("k_memo_publish");
+      k_memo_copy<<<sb, 128, 0, st>>>(fin, m_own, m_ent, rows, memo, out_samples, S);
+      SFFT_CHECK_LAUNCH("k_memo_copy");
+    }
     if (out_sched) {
       k_export_groups<<<S, 64, 0, st>>>(a.groups, ngroups, S, out_sched, fin, rows);
       SFFT_CHECK_LAUNCH("k_export_groups");

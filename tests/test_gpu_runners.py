@@ -309,3 +309,23 @@ def test_stream_admission_many_slots_chunk1(sb):
     assert bool((got.count > 0).all())
     for f in ("pos", "coef", "samples_read", "iterations", "converged"):
         assert torch.equal(getattr(got, f).cpu(), getattr(want, f).cpu()), f
+
+
+def test_samples_read_memo_equals_direct_count(sb, monkeypatch):
+    """samples_read memo (signals with an identical read schedule take the
+    first one's exclusion count) against counting every signal: equal
+    counts on a batch where most signals share schedules (C1-size signals,
+    different seeds; slots refilled over several rounds)."""
+    import torch
+    from oracle import sfft_oracle as O
+    n, k = 1 << 16, 16
+    X = torch.as_tensor(np.stack([O.synth(n, k, 30.0, 300 + j)[0] for j in range(40)])).cuda()
+    cfg = sb.AlgorithmConfig(framework="iterative", num_buckets=256)
+    out = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("SFFT_NO_SCHED_MEMO", off)
+        br = sb.run_iterative_batch(X, k, cfg, slots=16)
+        out.append((br.samples_read.cpu(), br.iterations.cpu(), br.count.cpu()))
+    for u, v in zip(*out):
+        assert torch.equal(u, v)
+    assert len(set(out[0][0].tolist())) < 40  # schedules are shared
