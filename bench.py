@@ -324,11 +324,12 @@ def main():
     kern_ms = pm.value
     achieved = (pi.value * item_bytes) / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
     peak, peak_kind = peaks()
-    # DRAM traffic of the same kernel from the committed ncu --set full capture
-    # (profiles/r1_k_cluster_ncu_raw.json: the co-scheduled first round, "items" bucketizations)
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (profiles/r2_k_group_fold_ncu_raw.json: the C3 first-round group-fold
+    # launch at 512 slots, "items" bucketizations)
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_k_cluster_ncu_raw.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_k_group_fold_ncu_raw.json")) as f:
             raw = json.load(f)
         unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
         rd = float(raw["dram__bytes_read.sum"][0]) * unit[raw["dram__bytes_read.sum"][1]]
@@ -439,7 +440,8 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB per GPU)" % (S * N * 8 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": traffic, "traffic_unit": "DRAM bytes per item (ncu)",
+                         "traffic": traffic,
+                         "traffic_unit": "DRAM read+write bytes per item of k_group_fold (ncu --set full, profiles/r2_k_group_fold_ncu_raw.json)",
                          "kernel": KERNEL_DESC,
                          "bytes_per_item": item_bytes,
                          "bytes_per_item_def": "SURVEY 8(d): Omega*8 gathered + B*8 buckets (c64)",
