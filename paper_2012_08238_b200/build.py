@@ -25,7 +25,21 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, jobs: int = 8) -> str:
+CHECKED_OBJ = os.path.join(HERE, "_build_checked")
+CHECKED_LIB = os.path.join(HERE, "libsfft_b200_checked.so")
+
+
+def build(verbose: bool = False, jobs: int = 8, checked: bool = True) -> str:
+    """The product library, and (checked=True) its bounds-checked twin
+    libsfft_b200_checked.so (-DSFFT_CHECKED: device asserts on the hot
+    kernels' indices; tests/test_gpu_checked.py runs it on small shapes)."""
+    lib = _build(OBJ, LIB, [], verbose, jobs)
+    if checked:
+        _build(CHECKED_OBJ, CHECKED_LIB, ["-DSFFT_CHECKED"], verbose, jobs)
+    return lib
+
+
+def _build(OBJ: str, LIB: str, extra: list, verbose: bool, jobs: int) -> str:
     os.makedirs(OBJ, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh")))
@@ -38,7 +52,7 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
 
     def compile_one(pair):
         src, obj = pair
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

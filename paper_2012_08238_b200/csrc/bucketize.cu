@@ -56,6 +56,7 @@ __device__ __forceinline__ double2 produce(const Prod& p, const ItemCtx& c, int 
   if (MODE == PROD_FLAT) {
     const Tin* xs = (const Tin*)c.xs;
     int64_t idx = mulmod(c.a, pmod(s - c.b, n), n);
+    SFFT_DASSERT(idx >= 0 && idx < n && s >= 0 && s < p.B);
     double2 acc = cmk(0.0, 0.0);
     if (c.c == 0) {
       // rows in order, 4 gathers in flight per step
@@ -332,6 +333,8 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
         v[0] = cadd(u, v[1]);
         v[1] = csub(u, v[1]);
       }
+#pragma unroll
+      SFFT_DASSERT(n2 < M);
 #pragma unroll
       for (int r = 0; r < CL; ++r)
         cl.map_shared_rank(bq, r)[n2] = (n2 * r) ? cmul(v[r], __ldg(W + n2 * r)) : v[r];
@@ -681,6 +684,7 @@ __global__ void __launch_bounds__(kGfNT, SFFT_GF_MINB)
         const int v = vr - back;
         if (v < -lo || v >= hi) continue;
         const int64_t idx = mulmod(sm, pmod(base + (int64_t)v * B, n), n);
+        SFFT_DASSERT(idx >= 0 && idx < n && sd.row0[w] + vr < kGfRows);
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(vw + vr * kGfCols);
         if (sizeof(Tin) == 8)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(xs + idx)
@@ -708,6 +712,8 @@ __global__ void __launch_bounds__(kGfNT, SFFT_GF_MINB)
       s = gc + cj - (wrap ? B : 0);
       nr = R - (s >= tail);
       vc = V + (int64_t)(sd.row0[w] + sd.back[w] - o) * kGfCols + lane;  // row r at vc[r C]
+      SFFT_DASSERT(sd.row0[w] + sd.back[w] - o >= 0 && sd.row0[w] + sd.back[w] - o + nr <= kGfRows);
+      SFFT_DASSERT(s >= 0 && s < B && nr <= kGfTapRegs);
       const double* tg = p.taps + s;
 #pragma unroll
       for (int r = 0; r < kGfTapRegs; ++r) t[r] = r < nr ? __ldg(tg + r * B) : 0.0;
@@ -1102,6 +1108,7 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
     item += gfirst[g_lo];
     if (item >= (g_hi >= 0 ? gfirst[g_hi] : nitems)) return;
   }
+  SFFT_DASSERT(item >= 0 && (gfirst || item < (int)gridDim.x));
   double2* row = y + (int64_t)item_row[item] * M;
   for (int k = threadIdx.x; k < M; k += kFrowNT) fr_s[frow_pad(k)] = row[k];
   __syncthreads();

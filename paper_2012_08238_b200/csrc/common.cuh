@@ -15,6 +15,24 @@
 
 #ifndef SFFT_HD
 #define SFFT_HD __host__ __device__ __forceinline__
+
+// Checked build (-DSFFT_CHECKED, libsfft_b200_checked.so): device-side bounds
+// asserts on the indices of the hot kernels -- the stand-in for
+// compute-sanitizer memcheck where the tool is unavailable.  A failed check
+// prints its location and traps (the launch then fails loudly).
+#ifdef SFFT_CHECKED
+#define SFFT_DASSERT(c)                                                          \
+  do {                                                                           \
+    if (!(c)) {                                                                  \
+      printf("SFFT_DASSERT %s:%d: %s\n", __FILE__, __LINE__, #c);                \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define SFFT_DASSERT(c) \
+  do {                  \
+  } while (0)
+#endif
 #endif
 
 namespace sfft {

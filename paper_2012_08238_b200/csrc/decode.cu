@@ -835,6 +835,7 @@ __global__ void __launch_bounds__(kSubNT, 4) k_subtract(
             for (int u = 0; u < kSubBPT; ++u) {
               int col = bk[u] - s_q[j + v];
               col += (col < 0) ? Bi : 0;
+              SFFT_DASSERT(col >= 0 && col < Bi && s_row[j + v] >= 0 && s_row[j + v] < n / B);
               w[v][u] = __ldg(row + col);
             }
           }

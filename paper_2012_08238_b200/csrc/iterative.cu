@@ -722,6 +722,7 @@ __device__ __forceinline__ void ladder_model_real(const IterArgs& a, int s, int 
         for (int u = 0; u < 4; ++u) {
           int64_t col = b - t_q[tt + u];
           col += (col < 0) ? B : 0;
+          SFFT_DASSERT(col >= 0 && col < B && t_row[tt + u] >= 0 && t_row[tt + u] < L);
           w[u] = __ldg(a.rt.at + t_row[tt + u] * B + col);
         }
 #pragma unroll
