@@ -1102,6 +1102,7 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
                                                      const int32_t* __restrict__ gfirst, int g_lo,
                                                      int g_hi, int nitems) {
   extern __shared__ double2 fr_s[];
+  double2* tw8 = fr_s + frow_pad(M - 1) + 1;  // tw8[e] = W[8 e], e < M/8 (stages >= 2)
   // items [gfirst[g_lo], gfirst[g_hi]) (or all when gfirst is null)
   int item = blockIdx.x;
   if (gfirst) {
@@ -1110,13 +1111,28 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
   }
   SFFT_DASSERT(item >= 0 && (gfirst || item < (int)gridDim.x));
   double2* row = y + (int64_t)item_row[item] * M;
-  for (int k = threadIdx.x; k < M; k += kFrowNT) fr_s[frow_pad(k)] = row[k];
+  for (int e = threadIdx.x; e < M / 8; e += kFrowNT) tw8[e] = __ldg(W + 8 * e);
+  // stage 1 straight from global memory: the 8 inputs of a butterfly and its
+  // twiddles are all requested at once (one round trip), then written to
+  // shared memory already transformed
+  constexpr int Mp1 = M / 8;
+  for (int j = threadIdx.x; j < Mp1; j += kFrowNT) {
+    double2 a[8], w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = row[j + q * Mp1];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) w[q] = __ldg(W + j * q);
+    dft8_(a);
+    fr_s[frow_pad(j)] = a[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) fr_s[frow_pad(j + q * Mp1)] = j ? cmul(a[q], w[q]) : a[q];
+  }
   __syncthreads();
-  int Mb = M;
+  int Mb = Mp1;
 #pragma unroll 1
-  for (int st = 0; st < Pow2<M>::N8; ++st) {
+  for (int st = 1; st < Pow2<M>::N8; ++st) {
     const int Mp = Mb >> 3;
-    const int tstr = M / Mb;
+    const int tstr8 = M / Mb / 8;  // twiddle index j q (M / Mb) = 8 * (j q tstr8)
     for (int t = threadIdx.x; t < M / 8; t += kFrowNT) {
       const int blk = t / Mp, j = t - blk * Mp;
       const int base = blk * Mb + j;
@@ -1127,7 +1143,7 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
       fr_s[frow_pad(base)] = a[0];
 #pragma unroll
       for (int q = 1; q < 8; ++q)
-        fr_s[frow_pad(base + q * Mp)] = j ? cmul(a[q], __ldg(W + j * q * tstr)) : a[q];
+        fr_s[frow_pad(base + q * Mp)] = j ? cmul(a[q], tw8[j * q * tstr8]) : a[q];
     }
     __syncthreads();
     Mb = Mp;
@@ -1159,7 +1175,7 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
 static int launch_fft_rows(const int32_t* item_row, int64_t nitems, int64_t B, const double2* W,
                            double2* y, cudaStream_t st, const int32_t* gfirst = nullptr,
                            int g_lo = 0, int g_hi = -1, int64_t ntot = 0) {
-  const size_t sm = (size_t)(B + B / 8 + B / 512 + 1) * sizeof(double2);
+  const size_t sm = (size_t)(B + B / 8 + B / 512 + 1 + B / 8) * sizeof(double2);
   switch (B) {
     case 4096:
       SFFT_CUDA(cudaFuncSetAttribute(k_fft_rows<4096>,
