@@ -1423,6 +1423,81 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
   double2 r[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) r[d] = mine ? a.y[((int64_t)d * a.S + s) * B + bi] : cmk(0, 0);
+  if (a.rt.at) {
+    // real form of the response (see k_subtract): c G ph = alpha + w^{b L h} beta A,
+    // alpha = c ph t0 / B, beta = c ph w^{-m h} / B; the alpha sums do not
+    // depend on the bucket (one warp forms them per chunk), the inner loop
+    // reads 8 bytes and does 6 FMA per tone pair
+    __shared__ double2 u_be[kPoChunk][3];
+    __shared__ double2 u_al[kPoChunk][3];
+    __shared__ double2 s_al[3];
+    const double t0v = a.rt.taps[0];
+    const double invB = 1.0 / (double)B;
+    const int64_t hh = a.rt.h % n;
+    double2 S3[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) S3[d] = cmk(0.0, 0.0);
+    if (threadIdx.x < 3) s_al[threadIdx.x] = cmk(0.0, 0.0);
+    for (int u0 = 0; u0 < T; u0 += kPoChunk) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < kPoChunk; q += kPoNT) {
+        if (u0 + q >= T) continue;
+        const int64_t mu = mulmod(sigma, pmod(rp[u0 + q], n), n);
+        u_row[q] = (L - mu % L) % L;
+        u_q[q] = (mu + L - 1) / L;
+        const double2 cu = rc[u0 + q];
+        const double2 wmh = unit_root(n, pmod(-mulmod(mu, hh, n), n));
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double2 cp = cmul(cu, unit_root(n, mulmod(pmod(tau + d, n), mu, n)));
+          u_be[q][d] = cscale(cmul(cp, wmh), invB);
+          u_al[q][d] = cscale(cp, t0v * invB);
+        }
+      }
+      __syncthreads();
+      const int un = min(kPoChunk, T - u0);
+      if (threadIdx.x < 3) {
+        double2 z = s_al[threadIdx.x];
+        for (int q = 0; q < un; ++q) z = cadd(z, u_al[q][threadIdx.x]);
+        s_al[threadIdx.x] = z;
+      }
+      if (mine) {
+        int q = 0;
+        for (; q + 8 <= un; q += 8) {
+          double w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            int64_t col = bi - u_q[q + u];
+            col += (col < 0) ? B : 0;
+            w[u] = __ldg(a.rt.at + u_row[q + u] * B + col);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              S3[d].x = fma(u_be[q + u][d].x, w[u], S3[d].x);
+              S3[d].y = fma(u_be[q + u][d].y, w[u], S3[d].y);
+            }
+        }
+        for (; q < un; ++q) {
+          int64_t col = bi - u_q[q];
+          col += (col < 0) ? B : 0;
+          const double w1 = __ldg(a.rt.at + u_row[q] * B + col);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            S3[d].x = fma(u_be[q][d].x, w1, S3[d].x);
+            S3[d].y = fma(u_be[q][d].y, w1, S3[d].y);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (mine) {
+      const double2 pb = unit_root(n, mulmod(mulmod(bi, L, n), hh, n));
+#pragma unroll
+      for (int d = 0; d < 3; ++d) r[d] = csub(csub(r[d], s_al[d]), cmul(pb, S3[d]));
+    }
+  } else {
   for (int u0 = 0; u0 < T; u0 += kPoChunk) {
     __syncthreads();
     for (int q = threadIdx.x; q < kPoChunk; q += kPoNT) {
@@ -1460,6 +1535,7 @@ __global__ void __launch_bounds__(kPoNT) k_po_delta(IterArgs a, const int32_t* o
         for (int d = 0; d < 3; ++d) r[d] = csub(r[d], cmul(cw, u_ph[q][d]));
       }
     }
+  }
   }
   if (mine) {
     double2 acc = cmk(0.0, 0.0);
