@@ -14,6 +14,7 @@
 // FFAST stages) use a four-step split B = B1*B2 whose column pass produces
 // the slots directly (no z round trip) and whose row pass writes y.
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include <cstring>
 #include <mutex>
@@ -22,6 +23,53 @@
 #include "kernels.cuh"
 
 namespace sfft {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TensorMapEncodeFn tensor_map_encoder() {
+  static TensorMapEncodeFn fn = []() -> TensorMapEncodeFn {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return (TensorMapEncodeFn)f;
+  }();
+  return fn;
+}
+
+// The signals as a 3-D tensor of 8-byte words: [signal][row j < L][B eb / 8],
+// boxes of one 128-byte line x up to 256 rows.
+static int stream_tensor_map(const void* x, int64_t xstride, int64_t n, int64_t B, int64_t eb,
+                             CUtensorMap* tm) {
+  TensorMapEncodeFn enc = tensor_map_encoder();
+  SFFT_REQUIRE(enc, "stream fold: cuTensorMapEncodeTiled not available");
+  const int64_t L = n / B;
+  const cuuint64_t dims[3] = {(cuuint64_t)(B * eb / 8), (cuuint64_t)L, (cuuint64_t)1 << 20};
+  const cuuint64_t strides[2] = {(cuuint64_t)(B * eb), (cuuint64_t)(xstride * eb)};
+  const cuuint32_t box[3] = {16, (cuuint32_t)std::min<int64_t>(L, 256), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const char* pe = getenv("SFFT_SF_PROMO");
+  const int promo = pe ? atoi(pe) : 0;
+  const CUtensorMapL2promotion l2 = promo == 64    ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                    : promo == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(x), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("stream fold: cuTensorMapEncodeTiled failed");
+    return -3;
+  }
+  return 0;
+}
 
 struct ItemCtx {
   const void* xs;
@@ -734,6 +782,205 @@ __global__ void __launch_bounds__(kGfNT, SFFT_GF_MINB)
   }
 }
 
+// ---- stream fold (opt-in, SFFT_STREAM_FOLD=1): a slot whose round reads a
+// large part of its signal (the first loop round of the iterative engine with
+// its speculative rows: 31 bucketizations over 7 permutations touch 18 % of
+// the samples and 80 % of the 64-byte granules of a C3 signal) reads the
+// signal ONCE, sequentially, instead of gathering.  With B | n the sample
+// x[sigma (s + rB - tau)] of folded slot s lives in address column
+// c = sigma (s - tau) mod B whatever the row r (sigma B = (sigma mod L) B mod
+// n, L = n/B), and s <-> c is a bijection per item: the signal seen as X[j][c]
+// (j < L rows of B samples), a CTA that holds address columns [c0, c0 + CW)
+// for every j can form, for EVERY item of the slot, the complete folded slot
+// of each of its columns -- rows in reference order from j0 + r (sigma mod L)
+// mod L, taps g[s + rB], no FMA contraction, so bit-identical to the per-item
+// fold.
+//
+// Persistent CTAs (one per SM) walk the (slot, column block) units; a unit is
+// the 128-byte line [c0, c0 + CW) of every signal row.  One producer thread
+// moves it with TMA tile loads (128 B x 256 rows per box) through a 7-box
+// shared-memory ring (full/empty mbarriers; a unit of L = 1024 rows holds 4
+// boxes, 3 more are in flight); the 512 consumer threads are the unit's
+// (item, column) pairs: each reads its taps from the round's permuted tap
+// table (k_sf_taps: T[item][r][c] = g[s_item(c) + rB], so a unit's taps are
+// contiguous instead of one sector per tap; every first-round slot runs the
+// same items, the permutation stream being shared), waits for the unit's
+// boxes, folds from shared memory and writes its slot.
+//
+// Measured (profiles/r2_stream_fold_experiments.md): correct and
+// bit-identical, but not faster than the group fold on this part -- both end
+// at ~4.4 TB/s of mixed DRAM traffic (the scattered 16-byte folded-slot
+// stores cost read-modify-write sectors, the tap table competes with the
+// streamed signal for L2), 9.6 vs 8.6 us per slot -- so the group fold stays
+// the default.
+constexpr int kSfStages = 7;                       // ring of TMA boxes
+constexpr int kSfCons = 512;                       // consumer threads
+constexpr int kSfNT = kSfCons + 32;                // + the producer warp
+constexpr int kSfGranule = 128;                    // bytes per signal row and unit: one line
+constexpr int kSfMaxL = 1024;                      // rows
+constexpr int kSfBoxRows = 256;                    // rows per TMA box (32 KB per stage)
+
+bool stream_fold_ok(int dtype, const void* x, int64_t xstride, int64_t n, int64_t B,
+                    int64_t omega) {
+  const int64_t eb = dtype == 0 ? 8 : 16;
+  if (n <= 0 || B <= 0 || (n & (n - 1)) || (B & (B - 1)) || B > n) return false;
+  const int64_t L = n / B;
+  if (L > kSfMaxL || L < 4 || B * eb < kSfGranule) return false;
+  if (cdiv_up(omega, B) > kGfTapRegs || omega < B) return false;
+  if (((uintptr_t)x % 128) || ((xstride * eb) % 128)) return false;
+  return B < (1 << 30) && omega < (1 << 30) && tensor_map_encoder() != nullptr;
+}
+
+size_t stream_fold_taps_bytes(int64_t B, int64_t nitems) {
+  return sizeof(double) * (size_t)kGfTapRegs * (size_t)B * (size_t)nitems;
+}
+
+// T[i][r][c] = g[s_i(c) + rB] (0 past Omega) for the lead slot's items i
+__global__ void k_sf_taps(Prod p, const int4* __restrict__ dense, int R, double* __restrict__ T) {
+  const int4 dd = __ldg(dense);
+  const int i = blockIdx.y / R, r = blockIdx.y % R;
+  if (i >= dd.z) return;
+  const unsigned B = (unsigned)p.B;
+  const uint64_t sg = (uint64_t)p.item_a[dd.y + i], tau = (uint64_t)p.item_b[dd.y + i];
+  uint64_t inv = sg;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) inv *= 2 - sg * inv;
+  for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < B; c += gridDim.x * blockDim.x) {
+    const unsigned s = (unsigned)((tau + inv * (uint64_t)c) & (B - 1));
+    const int64_t idx = (int64_t)s + (int64_t)r * B;
+    T[((size_t)i * R + r) * B + c] = idx < p.omega ? __ldg(p.taps + idx) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void sf_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(bar), "r"(parity)
+      : "memory");
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(kSfNT, 1)
+    k_stream_fold(const __grid_constant__ CUtensorMap tmap, Prod p, const int4* __restrict__ dense,
+                  int64_t nunits, const double* __restrict__ tperm, double2* __restrict__ out,
+                  int lgB, int mode) {
+  constexpr int CW = kSfGranule / (int)sizeof(Tin);
+  extern __shared__ __align__(128) unsigned char sf_smem[];
+  __shared__ __align__(8) uint64_t sf_full[kSfStages], sf_empty[kSfStages];
+  const unsigned B = (unsigned)p.B, omega = (unsigned)p.omega;
+  const unsigned L = (unsigned)(p.n >> lgB);
+  const int R = (int)((omega + B - 1) / B);
+  const unsigned tail = omega - (unsigned)(R - 1) * B;  // slots s < tail have R rows
+  const unsigned nblk = B / CW;                         // units per slot
+  const unsigned RB = L < (unsigned)kSfBoxRows ? L : (unsigned)kSfBoxRows;  // rows per box
+  const unsigned NB = L / RB;                                               // boxes per unit
+  const unsigned lgRB = 31 - __clz(RB);
+  const unsigned stage_bytes = RB * kSfGranule;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sf_smem);
+  const uint32_t fb = (uint32_t)__cvta_generic_to_shared(sf_full);
+  const uint32_t eb = (uint32_t)__cvta_generic_to_shared(sf_empty);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSfStages; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fb + 8 * i));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(eb + 8 * i), "r"(kSfCons));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= kSfCons) {
+    // ---- producer: box q of the CTA's k-th unit goes to ring position k NB + q
+    if (threadIdx.x == kSfCons) {
+      uint64_t pol;
+      if (mode & 1)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+      unsigned pos = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int4 dd = __ldg(dense + u / nblk);
+        const int cx = (int)((u % nblk) * (kSfGranule / 8));  // in 8-byte words
+        for (unsigned q = 0; q < NB; ++q, ++pos) {
+          const unsigned st = pos % kSfStages;
+          sf_mbar_wait(eb + 8 * st, ((pos / kSfStages) & 1) ^ 1);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                           fb + 8 * st),
+                       "r"(stage_bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
+                  sbase + st * stage_bytes),
+              "l"(&tmap), "r"(cx), "r"((int)(q * RB)), "r"(dd.w), "r"(fb + 8 * st), "l"(pol)
+              : "memory");
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers: thread (item, column) of every unit
+  const int t = threadIdx.x;
+  unsigned pos0 = 0;  // ring position of the unit's first box
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, pos0 += NB) {
+    const int4 dd = __ldg(dense + u / nblk);  // slot, first item, items, signal
+    const int first = dd.y, cnt = dd.z;
+    const unsigned c0 = (unsigned)(u % nblk) * CW;
+    if (p.prof_items && t == 0 && c0 == 0) atomicAdd(p.prof_items, (unsigned long long)cnt);
+    const unsigned st0 = pos0 % kSfStages;
+    const int total = cnt * CW;
+    const int npass = (total + kSfCons - 1) / kSfCons;
+    for (int pass = 0; pass < npass; ++pass) {
+      const int w = pass * kSfCons + t;
+      const bool act = w < total;
+      unsigned s = 0, j = 0, jstep = 0, cc = 0;
+      int nr = 0, item = first;
+      double tp[kGfTapRegs];
+      if (act) {
+        const int i = w / CW;
+        item = first + i;
+        cc = (unsigned)(w % CW);
+        const uint64_t sg = (uint64_t)p.item_a[item], tau = (uint64_t)p.item_b[item];
+        uint64_t inv = sg;  // sigma^-1 mod 2^64 (sigma odd): Newton, 3 -> 96 bits
+#pragma unroll
+        for (int q = 0; q < 5; ++q) inv *= 2 - sg * inv;
+        s = (unsigned)((tau + inv * (uint64_t)(c0 + cc)) & (B - 1));
+        const uint64_t idx0 = (sg * ((uint64_t)s - tau)) & (uint64_t)(p.n - 1);
+        SFFT_DASSERT((unsigned)(idx0 & (B - 1)) == c0 + cc);
+        j = (unsigned)(idx0 >> lgB);
+        jstep = (unsigned)(sg & (L - 1));
+        nr = R - (s >= tail);
+        const double* tg = tperm + (size_t)i * R * B + c0 + cc;
+#pragma unroll
+        for (int r = 0; r < kGfTapRegs; ++r) tp[r] = r < nr ? __ldg(tg + (size_t)r * B) : 0.0;
+      }
+      if (pass == 0)
+        for (unsigned q = 0; q < NB; ++q)
+          sf_mbar_wait(fb + 8 * ((pos0 + q) % kSfStages), ((pos0 + q) / kSfStages) & 1);
+      double2 acc = cmk(0.0, 0.0);
+      if (act) {
+        const unsigned char* vc = sf_smem + cc * sizeof(Tin);
+#pragma unroll
+        for (int r = 0; r < kGfTapRegs; ++r)
+          if (r < nr) {
+            SFFT_DASSERT(j < L);
+            unsigned st = st0 + (j >> lgRB);
+            st -= st >= (unsigned)kSfStages ? (unsigned)kSfStages : 0u;
+            const double2 v = to_d2_(*reinterpret_cast<const Tin*>(
+                vc + st * stage_bytes + (j & (RB - 1)) * kSfGranule));
+            acc = cadd_rn(acc, cmk(__dmul_rn(tp[r], v.x), __dmul_rn(tp[r], v.y)));
+            j = (j + jstep) & (L - 1);
+          }
+      }
+      if (pass == npass - 1)  // done with the unit's boxes: the producer may refill them
+        for (unsigned q = 0; q < NB; ++q)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                           eb + 8 * ((pos0 + q) % kSfStages))
+                       : "memory");
+      if (act) out[out_row(p, item) * p.B + s] = acc;
+    }
+  }
+}
+
 // Fallback for B with a prime factor above 13: slots to HBM, O(B^2) DFT.
 template <typename Tin, int MODE>
 __global__ void __launch_bounds__(256) k_slots(Prod p, double2* __restrict__ z) {
@@ -1205,8 +1452,12 @@ size_t flat_groups_desc_bytes(int64_t ngroups) { return (size_t)ngroups * sizeof
 
 int run_flat_groups(int dtype, const Prod& p0, const int32_t* gfirst, const int32_t* gcnt,
                     int64_t ngroups, int64_t nitems, const double2* W, double2* out, void* ws,
-                    size_t ws_bytes, void* desc_ws, cudaStream_t st) {
-  if (ngroups <= 0 || nitems <= 0) return 0;
+                    size_t ws_bytes, void* desc_ws, cudaStream_t st, const int32_t* dense,
+                    int64_t ndense, void* taps_ws, int max_items) {
+  if ((ngroups <= 0 && ndense <= 0) || nitems <= 0) return 0;
+  SFFT_REQUIRE(ndense <= 0 || (dense &&
+                               stream_fold_ok(dtype, p0.x, p0.xstride, p0.n, p0.B, p0.omega)),
+               "stream fold: streamed slots on a problem it cannot take");
   SFFT_REQUIRE(!p0.item_c && !p0.active && !p0.item_active && p0.item_row,
                "group fold: needs an ungated item list with output rows and b' = 0");
   const int R = (int)cdiv_up(p0.omega, p0.B);
@@ -1223,8 +1474,49 @@ int run_flat_groups(int dtype, const Prod& p0, const int32_t* gfirst, const int3
     if (rc) return rc;
   }
   GfDesc* desc = (GfDesc*)desc_ws;
-  k_gf_prep<<<(unsigned)cdiv_up(ngroups, 128), 128, 0, st>>>(p, gfirst, gcnt, ngroups, desc);
-  SFFT_CHECK_LAUNCH("k_gf_prep");
+  if (ngroups > 0) {
+    k_gf_prep<<<(unsigned)cdiv_up(ngroups, 128), 128, 0, st>>>(p, gfirst, gcnt, ngroups, desc);
+    SFFT_CHECK_LAUNCH("k_gf_prep");
+  }
+  if (ndense > 0) {
+    // streamed slots first: their FFT rows are the bulk of the row pass
+    SFFT_REQUIRE(taps_ws, "stream fold: no tap table scratch");
+    const int64_t L = p.n / p.B;
+    const size_t ssm = (size_t)kSfStages * std::min<int64_t>(L, kSfBoxRows) * kSfGranule;
+    int lgB = 0;
+    while (((int64_t)1 << lgB) < p.B) ++lgB;
+    const int64_t eb = dtype == 0 ? 8 : 16;
+    const int64_t nunits = ndense * (p.B * eb / kSfGranule);
+    CUtensorMap tmap;
+    if (stream_tensor_map(p.x, p.xstride, p.n, p.B, eb, &tmap)) return -3;
+    const int4* dp = reinterpret_cast<const int4*>(dense);
+    double* tperm = (double*)taps_ws;
+    k_sf_taps<<<dim3((unsigned)cdiv_up(p.B, 256), (unsigned)(max_items * R)), 256, 0, st>>>(
+        p, dp, R, tperm);
+    SFFT_CHECK_LAUNCH("k_sf_taps");
+    int dev = 0, sms = 0, per = 0;
+    SFFT_CUDA(cudaGetDevice(&dev));
+    SFFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (dtype == 0) {
+      SFFT_CUDA(cudaFuncSetAttribute(k_stream_fold<float2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+      SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fold<float2>, kSfNT,
+                                                              ssm));
+    } else {
+      SFFT_CUDA(cudaFuncSetAttribute(k_stream_fold<double2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+      SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fold<double2>, kSfNT,
+                                                              ssm));
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(nunits, (int64_t)sms * std::max(per, 1));
+    const char* me = getenv("SFFT_SF_MODE");
+    const int mode = me ? atoi(me) : 1;  // bit 0: evict_first on the streamed lines
+    if (dtype == 0)
+      k_stream_fold<float2><<<grid, kSfNT, ssm, st>>>(tmap, p, dp, nunits, tperm, out, lgB, mode);
+    else
+      k_stream_fold<double2><<<grid, kSfNT, ssm, st>>>(tmap, p, dp, nunits, tperm, out, lgB, mode);
+    SFFT_CHECK_LAUNCH("k_stream_fold");
+  }
   const size_t sm = (size_t)kGfRows * kGfCols * (dtype == 0 ? sizeof(float2) : sizeof(double2));
   if (dtype == 0)
     SFFT_CUDA(cudaFuncSetAttribute(k_group_fold<float2>,
@@ -1246,7 +1538,7 @@ int run_flat_groups(int dtype, const Prod& p0, const int32_t* gfirst, const int3
   const bool rows = !(fe && !strcmp(fe, "cluster")) && (p.B == 4096 || p.B == 2048 || p.B == 1024);
   int rc = 0;
   {
-    if ((rc = fold(0, ngroups, st))) return rc;
+    if (ngroups > 0 && (rc = fold(0, ngroups, st))) return rc;
     rc = rows ? launch_fft_rows(p.item_row, nitems, p.B, W, out, st) : 1;
     if (rc > 0) {
       Prod pl = p;

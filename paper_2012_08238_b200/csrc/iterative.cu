@@ -134,6 +134,12 @@ struct IterArgs {
   int32_t* act_list;             // [S] the round's loop slots (compacted in the prologue)
   int32_t* run_first;            // [S*(M+C)]
   int32_t* run_cnt;
+  // streamed slots: a slot whose round reads a large part of its signal (the
+  // first loop round with its speculative rows) is folded by k_stream_fold
+  // from sequential 64-byte granules instead of per-sample gathers
+  int stream;                    // 1: the stream fold can take this problem
+  int32_t* dcnt;                 // [S + 1] 1 per streamed slot, then exclusive offsets
+  int32_t* dense;                // [S][4] the round's streamed slots: slot, first item, items, signal
 };
 
 // samples_read memo: every signal draws the same seeded permutation stream, so
@@ -397,7 +403,12 @@ __global__ void k_cb_plan(IterArgs a) {
       if (S.pidx + 2 + (c - a.M) / 3 < a.P) gp.chunk(0, 3);
   }
   a.cnt[s] = nm + spec;
-  a.rcnt[s] = gp.go;
+  // streamed when the round's windows add up to a quarter of the signal (by
+  // then most 64-byte granules are touched: reading every granule once,
+  // sequentially, is cheaper than the gathers)
+  const bool dense = a.stream && first && nm == a.M && (int64_t)(nm + spec) * a.omega * 4 >= a.n;
+  a.dcnt[s] = dense;
+  a.rcnt[s] = dense ? 0 : gp.go;
 }
 
 // exclusive scan of cnt[0..S) in place, total in cnt[S] (one CTA)
@@ -427,6 +438,7 @@ __global__ void __launch_bounds__(1024) k_cb_scan(IterArgs a) {
   __shared__ int carry;
   cb_scan_one(a.cnt, a.S, red, &carry, a.stats + 5);
   cb_scan_one(a.rcnt, a.S, red, &carry, a.stats + 6);
+  cb_scan_one(a.dcnt, a.S, red, &carry, a.stats + 0);
 }
 
 __global__ void k_cb_fill(IterArgs a) {
@@ -436,8 +448,15 @@ __global__ void k_cb_fill(IterArgs a) {
   int o = a.cnt[s];
   GroupPack gp;
   gp.go = a.rcnt[s];
-  gp.gf = a.run_first;
-  gp.gc = a.run_cnt;
+  const bool dense = a.dcnt[s + 1] > a.dcnt[s];
+  if (dense) {
+    // no groups: the slot's items go to the stream fold
+    reinterpret_cast<int4*>(a.dense)[a.dcnt[s]] =
+        make_int4(s, a.cnt[s], a.cnt[s + 1] - a.cnt[s], S.sig > 0 ? S.sig : 0);
+  } else {
+    gp.gf = a.run_first;
+    gp.gc = a.run_cnt;
+  }
   const int sig = S.sig > 0 ? S.sig : 0;
   const int o_own = o;
   for (int j = 0; j < S.nsh && j < a.M; ++j) {
@@ -1647,6 +1666,8 @@ static IterLayout iter_layout(int64_t n, int64_t B, int S, int M, int cap) {
       flat_groups_desc_bytes((int64_t)S * (M + spec_rows(M))),  // 48 group descriptors
       sizeof(int32_t) * (size_t)S,                              // 49 act_list
       sizeof(SchedMemo) + sizeof(int32_t) * 2 * (size_t)S,       // 50 samples_read memo, own/ent
+      sizeof(int32_t) * (5 * (size_t)S + 8),                     // 51 dcnt + dense (streamed slots)
+      stream_fold_taps_bytes(B, M + spec_rows(M)),               // 52 stream fold tap table
   };
   const int cnt = sizeof(sizes) / sizeof(sizes[0]);
   static_assert(sizeof(sizes) / sizeof(sizes[0]) <= sizeof(L.off) / sizeof(L.off[0]),
@@ -1919,6 +1940,14 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
   a.it2_tau = a.it2_sigma + (size_t)S * (M + spec_rows(M));
   a.rcnt = (int32_t*)(w + Lo.off[46]);
   a.act_list = (int32_t*)(w + Lo.off[49]);
+  a.dcnt = (int32_t*)(w + Lo.off[51]);
+  a.dense = a.dcnt + ((S + 1 + 3) / 4) * 4;  // 16-byte aligned descriptors
+  // SFFT_STREAM_FOLD=1: first-round slots on the stream fold (measured slower
+  // than the group fold, so opt-in; the parity tests run both)
+  a.stream = (getenv("SFFT_STREAM_FOLD") && atoi(getenv("SFFT_STREAM_FOLD"))) &&
+             !(getenv("SFFT_RUN_FOLD") && !atoi(getenv("SFFT_RUN_FOLD"))) &&
+             pstride == 0 &&  // one shared permutation stream: first-round slots run the same items
+             stream_fold_ok(dtype, x, xstride, n, B, omega);
   SchedMemo* memo = (SchedMemo*)(w + Lo.off[50]);
   int32_t* m_own = (int32_t*)(memo + 1);
   int32_t* m_ent = m_own + S;
@@ -2035,7 +2064,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     return 0;
   };
   int nit = 0;  // planned items of the coming round (row-cache path)
-  int nrun = 0;  // their permutation runs
+  int nrun = 0;  // their permutation runs (slots on the group fold)
+  int ndense = 0;  // slots on the stream fold
   int n_act = S;  // loop slots of the coming round (k_act_list)
   // item-group fold (one gather per sample of a permutation window, the
   // measurements of a slot's permutations folded from shared memory, then the
@@ -2049,14 +2079,15 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     if (a.C > 0) {
     }
     {
-      int32_t h3[3];
-      SFFT_CUDA(cudaMemcpyAsync(h3, a.stats + 5, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      int32_t h8[8];
+      SFFT_CUDA(cudaMemcpyAsync(h8, a.stats, sizeof(h8), cudaMemcpyDeviceToHost, st));
       SFFT_CUDA(cudaStreamSynchronize(st));
       if (a.C > 0) {
-        nit = h3[0];
-        nrun = h3[1];
+        nit = h8[5];
+        nrun = h8[6];
+        ndense = h8[0];
       }
-      n_act = h3[2];
+      n_act = h8[7];
     }
   }
   for (; round < max_rounds; ++round) {
@@ -2066,7 +2097,8 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
       SFFT_CHECK_LAUNCH("k_cb_copy");
       if (nit > 0 && !run_fold_off)
         rc = run_flat_groups(dtype, pc, a.run_first, a.run_cnt, nrun, nit, W, a.y, bws,
-                             bws_bytes, w + Lo.off[48], st);
+                             bws_bytes, w + Lo.off[48], st, a.dense, ndense, w + Lo.off[52],
+                             M + spec_rows(M));
       else if (nit > 0)
         rc = run_bucketize(dtype, PROD_FLAT, pc, nit, W, a.y, bws, bws_bytes, st);
     } else {
@@ -2173,6 +2205,7 @@ int run_iterative(int dtype, const void* x, int64_t n, int64_t xstride, int Q, i
     h_max = hs[2];
     nit = hs[5];
     nrun = hs[6];
+    ndense = hs[0];
     n_act = hs[7];
     if (hs[3] >= Q) break;
   }

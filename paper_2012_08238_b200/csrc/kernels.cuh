@@ -63,9 +63,18 @@ constexpr int kGfItems = 8;  // items per group of the group fold (one warp each
 // item groups of flat items (iterative ladder / polish permutations of one
 // slot): one gather per sample of a window, then the FFTs in place (bucketize.cu)
 size_t flat_groups_desc_bytes(int64_t ngroups);  // scratch for the per-group descriptors
+// dense/ndense: slots folded by the stream fold instead (descriptor i =
+// {slot, first item, items, signal}, 16 bytes each; none of their items is in
+// a group); stream_fold_ok says whether a problem qualifies
 int run_flat_groups(int dtype, const Prod& p, const int32_t* gfirst, const int32_t* gcnt,
                     int64_t ngroups, int64_t nitems, const double2* W, double2* out, void* ws,
-                    size_t ws_bytes, void* desc_ws, cudaStream_t st);
+                    size_t ws_bytes, void* desc_ws, cudaStream_t st,
+                    const int32_t* dense = nullptr, int64_t ndense = 0,
+                    void* taps_ws = nullptr, int max_items = 0);
+// scratch for the stream fold's permuted tap table (max_items items per slot)
+size_t stream_fold_taps_bytes(int64_t B, int64_t nitems);
+bool stream_fold_ok(int dtype, const void* x, int64_t xstride, int64_t n, int64_t B,
+                    int64_t omega);
 // Dirichlet bank (sfft/bucketize.py:181-211): per-offset transforms y [noff][B]
 // (forward FFT of the conjugated fold / B) combined into out [B]
 int run_dirichlet_combine(const double2* y, int64_t noff, const int64_t* offsets, int64_t n,

@@ -51,14 +51,20 @@ def main() -> int:
         sb.TimeSignal(x16, device=dev), 16,
         sb.AlgorithmConfig(framework="iterative", num_buckets=256)))
     xs = torch.as_tensor(np.stack([O.synth(1 << 16, 16, 30.0, 3 + j)[0] for j in range(3)]))
-    for rf in ("0", "1"):
+    for rf, sf in (("0", "1"), ("1", "0"), ("1", "1")):
         os.environ["SFFT_ROW_CACHE"] = "1"
         os.environ["SFFT_RUN_FOLD"] = rf
-        run(f"iterative row cache B=4096 run_fold={rf}", lambda: sb.run_iterative_batch(
-            xs.to(torch.complex64).to(dev), 16,
-            sb.AlgorithmConfig(framework="iterative", num_buckets=4096), slots=2).to_results())
+        os.environ["SFFT_STREAM_FOLD"] = sf
+        run(f"iterative row cache B=4096 run_fold={rf} stream_fold={sf}",
+            lambda: sb.run_iterative_batch(
+                xs.to(torch.complex64).to(dev), 16,
+                sb.AlgorithmConfig(framework="iterative", num_buckets=4096), slots=2).to_results())
+    run("iterative row cache B=256 stream fold c128", lambda: sb.run_iterative_batch(
+        xs.to(dev), 16, sb.AlgorithmConfig(framework="iterative", num_buckets=256),
+        slots=2).to_results())
     os.environ.pop("SFFT_ROW_CACHE", None)
     os.environ.pop("SFFT_RUN_FOLD", None)
+    os.environ.pop("SFFT_STREAM_FOLD", None)
     x14 = O.synth(1 << 14, 8, None, 4)[0]
     run("iterative binary", lambda: sb.run_iterative(
         sb.TimeSignal(x14, device=dev), 8,

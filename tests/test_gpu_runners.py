@@ -274,23 +274,53 @@ def test_iterative_four_step_b8192(sb, row_cache, monkeypatch):
 
 
 def test_run_fold_bit_identical_c3(sb, monkeypatch):
-    """The permutation-run fold gathers each sample of a (signal, sigma) run
-    once and folds every shift from shared memory; it must give bit-identical
-    bucket values, hence identical results, to the per-item cluster kernel
-    (C3 batch incl. non-converging signals, complex64 and complex128)."""
+    """The three gather-folds of the row-cache path must give bit-identical
+    bucket values, hence identical results: the item-group fold (default: each
+    sample of a permutation window gathered once), the stream fold (opt-in: a
+    slot's first round reads every line of its signal once through a TMA ring
+    and folds all of its items from shared memory) and the per-item cluster
+    kernel (C3 batch incl. non-converging signals, complex64 and
+    complex128)."""
     import torch
     cases = [c for c in CASES if c[0]["name"].startswith("C3")] + list(STRAG)
     cfg = _cfg(sb, cases[0][0])
     for dt in (torch.complex64, torch.complex128):
         X = torch.stack([torch.as_tensor(regen_signal(r, a)) for r, a in cases]).to(dt).cuda()
         out = []
-        for on in ("1", "0"):
-            monkeypatch.setenv("SFFT_RUN_FOLD", on)
+        for env in ({}, {"SFFT_STREAM_FOLD": "1"}, {"SFFT_RUN_FOLD": "0"}):
+            for k in ("SFFT_STREAM_FOLD", "SFFT_RUN_FOLD"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
             br = sb.run_iterative_batch(X, 256, cfg, slots=512)
+            out.append((br.pos.cpu(), br.coef.cpu(), br.count.cpu(), br.samples_read.cpu(),
+                        br.iterations.cpu()))
+        for other in out[1:]:
+            for u, v in zip(out[0], other):
+                assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("n,b,k", [(1 << 16, 256, 16), (1 << 18, 1024, 32), (1 << 20, 1024, 64)])
+def test_stream_fold_small_shapes(sb, monkeypatch, n, b, k):
+    """Stream fold against the group fold at other row counts (L = N/B = 256
+    and 1024) and window lengths, row cache forced on, more signals than
+    slots, complex64 and complex128: identical results."""
+    import torch
+    from oracle import sfft_oracle as O
+    xs = np.stack([O.synth(n, k, 30.0, 4100 + j)[0] for j in range(12)])
+    cfg = sb.AlgorithmConfig(framework="iterative", num_buckets=b)
+    monkeypatch.setenv("SFFT_ROW_CACHE", "1")
+    for dt in (torch.complex64, torch.complex128):
+        X = torch.as_tensor(xs).to(dt).cuda()
+        out = []
+        for on in ("1", "0"):
+            monkeypatch.setenv("SFFT_STREAM_FOLD", on)
+            br = sb.run_iterative_batch(X, k, cfg, slots=8)
             out.append((br.pos.cpu(), br.coef.cpu(), br.count.cpu(), br.samples_read.cpu(),
                         br.iterations.cpu()))
         for u, v in zip(*out):
             assert torch.equal(u, v)
+        assert bool((out[0][2] > 0).all())
 
 
 def test_stream_admission_many_slots_chunk1(sb):
