@@ -599,7 +599,8 @@ constexpr int kGfCols = 32;    // columns per CTA (one per lane)
 constexpr int kGfNT = 256;     // 8 warps: warp j folds item j
 constexpr int kGfRows = 48;    // window rows held in shared memory at once
 constexpr int kGfBack = 8;     // a window reaches at most this many rows back
-constexpr int kGfTapRegs = 20; // taps of a slot held in registers (rows per slot)
+constexpr int kGfTapRegs = 20; // most rows per slot (taps of a slot)
+constexpr int kGfTapHalf = 10; // taps in registers at once
 #ifndef SFFT_GF_MINB
 #define SFFT_GF_MINB 5         // CTAs per SM the register budget is set for (4: 64 regs, no spills; 5 measured 7 % faster)
 #endif
@@ -750,7 +751,12 @@ __global__ void __launch_bounds__(kGfNT, SFFT_GF_MINB)
     const bool act = j < cnt && sd.batch[sd.win[j]] == bt && col0 + lane < B;
     int s = 0, nr = 0;
     const Tin* vc = V;
-    double t[kGfTapRegs];  // every tap of the slot in flight at once (R <= kGfTapRegs)
+    // the first kGfTapHalf taps of the slot are requested before the wait, the
+    // rest after the first half is folded: 20 doubles at once do not fit the
+    // 48 registers of 5 CTAs per SM (80 bytes of spills per thread were 6.7 GB
+    // of local-memory traffic per 512-slot launch, 6x the folded-slot stores)
+    double t[kGfTapHalf];
+    const double* tg = p.taps;
     if (act) {
       const int w = sd.win[j];
       const int gc = col0 + lane;
@@ -762,20 +768,27 @@ __global__ void __launch_bounds__(kGfNT, SFFT_GF_MINB)
       vc = V + (int64_t)(sd.row0[w] + sd.back[w] - o) * kGfCols + lane;  // row r at vc[r C]
       SFFT_DASSERT(sd.row0[w] + sd.back[w] - o >= 0 && sd.row0[w] + sd.back[w] - o + nr <= kGfRows);
       SFFT_DASSERT(s >= 0 && s < B && nr <= kGfTapRegs);
-      const double* tg = p.taps + s;
+      tg = p.taps + s;
 #pragma unroll
-      for (int r = 0; r < kGfTapRegs; ++r) t[r] = r < nr ? __ldg(tg + r * B) : 0.0;
+      for (int r = 0; r < kGfTapHalf; ++r) t[r] = r < nr ? __ldg(tg + r * B) : 0.0;
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     if (act) {
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int r = 0; r < kGfTapRegs; ++r)
-        if (r < nr) {
-          const double2 v = to_d2_(vc[r * kGfCols]);
-          acc = cadd_rn(acc, cmk(__dmul_rn(t[r], v.x), __dmul_rn(t[r], v.y)));
+      for (int h = 0; h < kGfTapRegs; h += kGfTapHalf) {
+        if (h > 0) {
+#pragma unroll
+          for (int r = 0; r < kGfTapHalf; ++r) t[r] = h + r < nr ? __ldg(tg + (h + r) * B) : 0.0;
         }
+#pragma unroll
+        for (int r = 0; r < kGfTapHalf; ++r)
+          if (h + r < nr) {
+            const double2 v = to_d2_(vc[(h + r) * kGfCols]);
+            acc = cadd_rn(acc, cmk(__dmul_rn(t[r], v.x), __dmul_rn(t[r], v.y)));
+          }
+      }
       out[out_row(p, first + j) * p.B + s] = acc;
     }
     if (bt + 1 < sd.nbatch) __syncthreads();  // the next batch reuses the shared memory
