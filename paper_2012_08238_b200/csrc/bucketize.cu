@@ -600,7 +600,10 @@ constexpr int kGfNT = 256;     // 8 warps: warp j folds item j
 constexpr int kGfRows = 48;    // window rows held in shared memory at once
 constexpr int kGfBack = 8;     // a window reaches at most this many rows back
 constexpr int kGfTapRegs = 20; // most rows per slot (taps of a slot)
-constexpr int kGfTapHalf = 10; // taps in registers at once
+#ifndef SFFT_GF_HALF
+#define SFFT_GF_HALF 10
+#endif
+constexpr int kGfTapHalf = SFFT_GF_HALF; // taps in registers at once
 #ifndef SFFT_GF_MINB
 #define SFFT_GF_MINB 5         // CTAs per SM the register budget is set for (4: 64 regs, no spills; 5 measured 7 % faster)
 #endif

@@ -749,8 +749,14 @@ __device__ __forceinline__ int sub_splits(int64_t T, int maxTS) {
   return (int)(z < 1 ? 1 : (z > maxTS ? maxTS : z));
 }
 
+#ifndef SFFT_SUB_MINB
+#define SFFT_SUB_MINB 4
+#endif
+#ifndef SFFT_SUB_BATCH
+#define SFFT_SUB_BATCH 8   // tones whose table reads are in flight together (real form)
+#endif
 template <bool REAL>
-__global__ void __launch_bounds__(kSubNT, 4) k_subtract(
+__global__ void __launch_bounds__(kSubNT, SFFT_SUB_MINB) k_subtract(
     const double2* __restrict__ y, double2* __restrict__ out, int64_t B, int64_t nb,
     const int32_t* blist, const double2* __restrict__ gt, int64_t n, const int32_t* item_sig,
     const int64_t* sigma, const int64_t* tau_tot, const int64_t* tpos, const double2* tcoef,
@@ -826,10 +832,10 @@ __global__ void __launch_bounds__(kSubNT, 4) k_subtract(
       if (live[0]) {
         const int tn = (int)((T - t0 < kSubChunk) ? (T - t0) : kSubChunk);
         int j = 0;
-        for (; j + 8 <= tn; j += 8) {
-          double w[8][kSubBPT];
+        for (; j + SFFT_SUB_BATCH <= tn; j += SFFT_SUB_BATCH) {
+          double w[SFFT_SUB_BATCH][kSubBPT];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
+          for (int v = 0; v < SFFT_SUB_BATCH; ++v) {
             const double* row = rt.at + (int64_t)s_row[j + v] * B;
 #pragma unroll
             for (int u = 0; u < kSubBPT; ++u) {
@@ -840,7 +846,7 @@ __global__ void __launch_bounds__(kSubNT, 4) k_subtract(
             }
           }
 #pragma unroll
-          for (int v = 0; v < 8; ++v)
+          for (int v = 0; v < SFFT_SUB_BATCH; ++v)
 #pragma unroll
             for (int u = 0; u < kSubBPT; ++u) {
               acc[u].x = fma(s_a[j + v].x, w[v][u], acc[u].x);
