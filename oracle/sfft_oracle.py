@@ -107,6 +107,7 @@ class FlatWindow:
     support: int
     taps: np.ndarray          # float64[support] (reference stores them as complex)
     response: np.ndarray      # complex128[n], B-normalised transform of the taps
+    center: int = 0           # passband offset in bins (flat_shift)
 
     @property
     def width(self) -> int:
@@ -129,6 +130,17 @@ def flat_window(n: int, b: int, support: int | None = None,
     line = np.zeros(n, dtype=np.complex128)
     line[:w] = taps
     return FlatWindow(n, b, w, taps, np.fft.fft(line) / b)
+
+
+def flat_shift(win: FlatWindow, f0: int) -> FlatWindow:
+    """Passband moved by f0 bins: taps *= w^(-f0 i), response recomputed
+    (sfft/filters.py:190-200).  ``center`` accumulates the offset."""
+    i = np.arange(win.support, dtype=np.int64)
+    taps = win.taps * unit_root(win.n, -f0 * i)
+    line = np.zeros(win.n, dtype=np.complex128)
+    line[:win.support] = taps
+    return FlatWindow(win.n, win.b, win.support, taps, np.fft.fft(line) / win.b,
+                      (win.center + f0) % win.n)
 
 
 # ---------------------------------------------------------------- encode

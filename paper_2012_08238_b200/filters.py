@@ -73,17 +73,29 @@ class WindowFilter:
     center_offset: int = 0
     half_bucket_offset: bool = True
     response: object = None  # Dirichlet: complex128 [N] unnormalised box transform
+    base_taps: object = None  # frequency-shifted flat window: the real taps the kernels use
+                              # (``taps`` then holds taps * w^(-f0 i), as in the reference)
 
     @property
     def device(self):
         return self.taps.device
 
     @property
+    def kernel_taps(self):
+        """The real flat taps (a shifted window's modulation w^(-f0 i) rides on
+        the kernels' per-item phase term)."""
+        return self.taps if self.base_taps is None else self.base_taps
+
+    @property
     def freq_response(self):
         """G over [0, N) in natural order (device tensor)."""
         if self.gtable is None:
             return self.response
-        return self.gtable.transpose(0, 1).reshape(self.n)
+        g = self.gtable.transpose(0, 1).reshape(self.n)
+        if self.kind == FLAT and self.center_offset:
+            import torch
+            g = torch.roll(g, self.center_offset)  # G'[f] = G[f - f0]
+        return g
 
     def bucket_centers(self):
         """Position-space passband centers, one per bucket (sfft/filters.py:92-100)."""
@@ -106,7 +118,7 @@ class WindowFilter:
             base = 0 if self.half_bucket_offset else self.bucket_width // 2
             e = (m - (bucket * self.bucket_width + base)) % self.n
             return self.response[torch.as_tensor(e, device=self.device)]
-        e = (bucket * self.bucket_width - m) % self.n
+        e = (bucket * self.bucket_width - m - self.center_offset) % self.n
         r = torch.as_tensor(e % self.bucket_width, device=self.device)
         j = torch.as_tensor(e // self.bucket_width, device=self.device)
         return self.gtable[r, j]
@@ -176,19 +188,28 @@ def make_dirichlet_bank(n: int, bucket_width: int, num_buckets: int, half_offset
 
 
 def filter_freq_shift(f: WindowFilter, f0: int) -> WindowFilter:
-    """Move a Dirichlet bank's passbands by f0 bins: taps *= w^(-f0 * position),
-    center_offset += f0 (sfft/filters.py:190-200).  The device flat window keeps
-    real taps, so shifting it is not supported here."""
+    """Move the passband centre(s) by f0 bins: taps *= w^(-f0 * position),
+    center_offset += f0 (sfft/filters.py:190-200).  A flat window keeps its
+    real taps for the kernels (``base_taps``): the modulation is the same
+    per-sample phase term a permutation's b' uses, so ``bucketize_flat`` folds
+    the shift into it, and the response is the unshifted table rolled by f0."""
     from dataclasses import replace
-    if f.kind != DIRICHLET:
-        raise NotImplementedError("filter_freq_shift: device path covers Dirichlet banks")
     import numpy as np
     import torch
     from .signal import phase_factor
+    f0 = int(f0)
+    if f.kind == FLAT:
+        off = (f.center_offset + f0) % f.n
+        base = f.kernel_taps
+        pos = np.arange(f.support, dtype=np.int64)
+        taps = base * phase_factor(f.n, -off * pos, device=f.device)
+        return replace(f, taps=taps, base_taps=base, center_offset=off)
+    if f.kind != DIRICHLET:
+        raise NotImplementedError("filter_freq_shift: flat windows and Dirichlet banks")
     pos = np.arange(f.support, dtype=np.int64)
-    taps = f.taps * phase_factor(f.n, -int(f0) * pos, device=f.device)
+    taps = f.taps * phase_factor(f.n, -f0 * pos, device=f.device)
     pad = torch.zeros(f.n, dtype=torch.complex128, device=f.device)
     pad[:f.support] = taps
     resp = torch.fft.fft(pad)
     return replace(f, taps=taps, response=resp, peak=float(resp.abs().max().item()),
-                   center_offset=(f.center_offset + int(f0)) % f.n)
+                   center_offset=(f.center_offset + f0) % f.n)

@@ -318,7 +318,7 @@ def run_iterative_batch(xs, k: int, cfg: AlgorithmConfig, slots: int | None = No
     lad = (ctypes.c_int64 * len(ladder))(*ladder) if ladder else None
     dt = 0 if X.dtype == torch.complex64 else 1
     gmax = torch.tensor([filt.peak], dtype=torch.float64, device=dev)
-    check(L.sfft_run_iterative(dt, ptr(X), n, X.stride(0), S, nslots, ptr(filt.taps),
+    check(L.sfft_run_iterative(dt, ptr(X), n, X.stride(0), S, nslots, ptr(filt.kernel_taps),
                                filt.support, b, ptr(filt.gtable), ptr(gmax),
                                ptr(twiddles(b, dev)), ptr(psig), ptr(ptau), P, 0, k,
                                cfg.max_iterations, lad, len(ladder), 1 if split else 0, br,

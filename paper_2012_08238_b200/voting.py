@@ -45,7 +45,7 @@ def voting_batch(xs, k: int, cfg):
     ws = _WS.get(wsb, dev, "voting")
     gmax = torch.tensor([filt.peak], dtype=torch.float64, device=dev)
     dt = 0 if X.dtype == torch.complex64 else 1
-    check(L.sfft_run_voting(dt, ptr(X), n, X.stride(0), S, ptr(filt.taps), filt.support, b,
+    check(L.sfft_run_voting(dt, ptr(X), n, X.stride(0), S, ptr(filt.kernel_taps), filt.support, b,
                             ptr(filt.gtable), ptr(gmax), ptr(twiddles(b, dev)), ptr(psig),
                             ptr(ptau), R, k, need_votes(cfg.min_vote_fraction, R), bpre,
                             ptr(twiddles(bpre, dev)) if bpre else None, ptr(out_pos),

@@ -42,6 +42,37 @@ def test_flat_golden(sb, dtype, tol):
         off += b
 
 
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-12), ("complex64", 1e-4)])
+def test_flat_freq_shift_golden(sb, dtype, tol):
+    """filter_freq_shift of a flat window (sfft/filters.py:190-200) and flat
+    bucketizations through it, against the reference: modulated taps, rolled
+    response, passband centres, bucket weights, bucket values, centre shift,
+    reads and the hash view (incl. composed shifts, f0 = 0, N and negative)."""
+    from paper_2012_08238_b200.bucketize import hash_view_for
+    z = load_golden("stage_flatshift")
+    for i, row in enumerate(z["meta"]):
+        n, b, ns, s, t, bp, te, center, cshift, access, step = (int(v) for v in row[:11])
+        f = sb.make_flat_filter(n, b)
+        for f0 in row[11:11 + ns]:
+            f = sb.filter_freq_shift(f, int(f0))
+        assert f.center_offset == center
+        assert rel(f.taps.cpu().numpy(), z[f"{i}_taps"]) < 1e-13
+        assert rel(f.freq_response.cpu().numpy()[::step], z[f"{i}_resp"]) < 1e-13
+        assert np.array_equal(f.bucket_centers(), z[f"{i}_centers"])
+        m = (np.arange(40, dtype=np.int64) * 997 + 3) % n
+        got_w = np.stack([f.bucket_weight(bq, m).cpu().numpy() for bq in (0, 1, b - 1)])
+        assert np.abs(got_w - z[f"{i}_weight"]).max() < 1e-13 * np.abs(z[f"{i}_resp"]).max()
+        xs = sb.TimeSignal(stage_signal(20241001 + i, n), dtype=dtype)
+        perm = sb.PermutationParams(n=n, sigma=s, tau=t, b_prime=bp)
+        bs = sb.bucketize_flat(xs, f, perm, te)
+        assert rel(bs.values_host(), z[f"{i}_y"]) < tol, (i, n, b)
+        assert bs.center_shift == cshift and xs.access_count == access
+        hv = hash_view_for(f, perm)
+        assert np.array_equal(np.asarray(hv.bucket_of(m)), z[f"{i}_bucket_of"])
+        assert np.array_equal(hv.preimage(b // 2), z[f"{i}_pre"])
+        assert np.array_equal(np.asarray(bs.hash_map().bucket_of(m)), z[f"{i}_bucket_of"])
+
+
 def test_filter_response_matches_oracle(sb):
     z = load_golden("stage_filter")
     for n, b in [(2048, 16), (3000, 24), (65536, 256)]:

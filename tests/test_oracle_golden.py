@@ -245,3 +245,21 @@ def test_runner_golden_c5_grid(case):
     assert err <= 1e-13, err
     assert (out.samples_read, out.iterations, out.converged) == \
         (rec["samples_read"], rec["iterations"], rec["converged"])
+
+
+def test_flat_shift_golden():
+    """Frequency-shifted flat windows (sfft/filters.py:190-200): the oracle's
+    taps, response and bucket values against the reference's, bit for bit."""
+    z = load_golden("stage_flatshift")
+    for i, row in enumerate(z["meta"]):
+        n, b, ns, s, t, bp, te, center, cshift, access, step = (int(v) for v in row[:11])
+        win = O.flat_window(n, b)
+        for f0 in row[11:11 + ns]:
+            win = O.flat_shift(win, int(f0))
+        assert win.center == center and (-center) % n == cshift
+        assert np.array_equal(win.taps, z[f"{i}_taps"])
+        assert np.array_equal(win.response[::step], z[f"{i}_resp"])
+        acc = O.Access(stage_signal(20241001 + i, n))
+        y = O.flat_buckets(acc, win, s, t, bp, te)
+        assert np.array_equal(y, z[f"{i}_y"])
+        assert acc.count() == access
