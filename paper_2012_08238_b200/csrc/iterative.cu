@@ -632,7 +632,7 @@ template <int M>
 __device__ __forceinline__ void ladder_model(const IterArgs& a, int s, int b, bool live,
                                              int64_t tb, int64_t te, double2* ys,
                                              int64_t (*t_row), int64_t (*t_q), double2* t_c,
-                                             double2 (*t_ph)[kMaxShifts]) {
+                                             double2 (*t_ph)[M]) {
   const int64_t n = a.n, B = a.B, L = a.L;
   const int64_t sigma = a.item_sigma[s];
   const int64_t tau = a.item_tau[s];
@@ -690,8 +690,8 @@ template <int M>
 __device__ __forceinline__ void ladder_model_real(const IterArgs& a, int s, int b, bool live,
                                                   int64_t tb, int64_t te, double2* ys,
                                                   int64_t* t_row, int64_t* t_q,
-                                                  double2 (*t_be)[kMaxShifts],
-                                                  double2 (*t_al)[kMaxShifts], double2* s_al) {
+                                                  double2 (*t_be)[M],
+                                                  double2 (*t_al)[M], double2* s_al) {
   const int64_t n = a.n, B = a.B, L = a.L;
   const int64_t sigma = a.item_sigma[s];
   const int64_t tau = a.item_tau[s];
@@ -783,12 +783,15 @@ __device__ __forceinline__ int lad_splits(int64_t T, int maxTS) {
 
 // Tone-split partial ladder sums for large recovered lists:
 // part[s][z][h][j-1] = -sum_{tones of split z} c w ph_j.
+#ifndef SFFT_LAD_MINB
+#define SFFT_LAD_MINB 4   // 4, 5, 6 CTAs per SM measured equal (128, 96, 80 registers); 8 spills and is 6 % slower
+#endif
 template <int M>
-__global__ void __launch_bounds__(kLocNT) k_it_ladder_part(IterArgs a) {
+__global__ void __launch_bounds__(kLocNT, SFFT_LAD_MINB) k_it_ladder_part(IterArgs a) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
-  __shared__ double2 t_ph[kLocChunk][kMaxShifts];
-  __shared__ double2 t_al[kLocChunk][kMaxShifts];
+  __shared__ double2 t_ph[kLocChunk][M];  // per (tone, shift): sized by the ladder, not kMaxShifts
+  __shared__ double2 t_al[kLocChunk][M];
   __shared__ double2 s_al[kMaxShifts];
   const int s = a.act_list[blockIdx.y];  // grid over the loop slots of the round
   if (!a.active[s]) return;
@@ -825,8 +828,8 @@ template <int M>
 __global__ void __launch_bounds__(kLocNT) k_it_locate(IterArgs a, int maxTS) {
   __shared__ int64_t t_row[kLocChunk], t_q[kLocChunk];
   __shared__ double2 t_c[kLocChunk];
-  __shared__ double2 t_ph[kLocChunk][kMaxShifts];
-  __shared__ double2 t_al[kLocChunk][kMaxShifts];
+  __shared__ double2 t_ph[kLocChunk][M];  // per (tone, shift): sized by the ladder, not kMaxShifts
+  __shared__ double2 t_al[kLocChunk][M];
   __shared__ double2 s_al[kMaxShifts];
   const int s = a.act_list[blockIdx.y];  // grid over the loop slots of the round
   if (!a.active[s]) return;
