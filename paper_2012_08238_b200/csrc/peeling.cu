@@ -169,8 +169,52 @@ __device__ __forceinline__ uint32_t pe_slot(int64_t f, int HT) {
   return (uint32_t)(((unsigned long long)(f + 1) * 0x9E3779B97F4A7C15ull) >> 40) & (HT - 1);
 }
 
+// Bitwise equality of two post-peel bucket states (moments of the stage's
+// shifts, class, and the single-ton's position / coefficient).
+struct PeelState {
+  double2 m[3];
+  Verdict v;
+};
+
+__device__ __forceinline__ bool same_bits(double2 x, double2 y) {
+  return __double_as_longlong(x.x) == __double_as_longlong(y.x) &&
+         __double_as_longlong(x.y) == __double_as_longlong(y.y);
+}
+
+__device__ __forceinline__ bool same_state(const PeelState& x, const PeelState& y, int sh) {
+  bool eq = x.v.kind == y.v.kind;
+  for (int t = 0; t < 3; ++t)
+    if (t < sh) eq = eq && same_bits(x.m[t], y.m[t]);
+  if (eq && x.v.kind == 1) eq = x.v.f == y.v.f && same_bits(x.v.c, y.v.c);
+  return eq;
+}
+
+constexpr int kPeelOldCap = 256;    // queued entries of the cycle's buckets kept for the replay
+constexpr int kPeelSimSteps = 4096; // pops replayed before the attempt is given up
+
 // The sequential peel of one signal, one warp (frameworks.py:669-695).
-__global__ void k_pe_peel(PeelArgs a, int64_t budget) {
+//
+// Exact fast-forward of a two-state cycle.  A signal that exhausts the budget
+// k + sum B_j does so in a loop of period <= 2: the same position f is peeled
+// again and again (a rounding-level residual in one stage's bucket is a
+// "single-ton" c; removing it leaves -c in the other stages' buckets, peeling
+// that restores the first state), 77,479 times for C4's seed 213.  The next
+// state of the buckets of f is a pure function of their moments and of the
+// coefficient of whichever of them is popped, so once
+//   * three consecutive peels had the same f,
+//   * the buckets' state after this peel equals, bit for bit, the state two
+//     peels ago (moments, class, single-ton position and coefficient),
+//   * the queue holds no single-ton entry of any other bucket, and the replay
+//     of its pops (integers only: which stage's entry is taken next, stale
+//     entries skipped as the loop would) always takes an entry whose class is
+//     exactly (f, the coefficient the last two peels used in that state) and
+//     reaches a repeating pattern that never runs dry,
+// every remaining peel is known: the states alternate, recovered[f] receives
+// the two coefficients alternately (the additions are carried out, stopping
+// early once they too repeat), and the budget is reached.  Results, peel
+// count and final classes are bit-identical to running the loop.
+__global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
+  __shared__ int8_t s_old[kPeelOldCap];
   const int s = blockIdx.x;
   const int lane = threadIdx.x;
   int64_t head[2] = {0, 0};
@@ -185,6 +229,15 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget) {
   int32_t* hv = a.ht_val + (int64_t)s * a.HT;
   int nrec = 0;
   int64_t peels = 0;
+  // all stages in one tier (the replay below handles a single live queue)
+  int live_tier = a.sh[0] >= 3 ? 0 : 1;
+  if (!fast_forward) live_tier = -1;
+  for (int j = 1; j < a.nst; ++j)
+    if ((a.sh[j] >= 3 ? 0 : 1) != live_tier) live_tier = -1;
+  PeelState h1{}, h2{};  // this lane's bucket after the previous peel / the one before
+  int64_t f1 = -1, f2 = -1;
+  double2 cprev = cmk(0.0, 0.0);  // coefficient of the previous peel
+  int64_t next_try = 0;
   while (peels < budget) {
     // pop the first still-single entry, verified tier first (all lanes agree);
     // the warp checks 32 queue entries per step instead of one
@@ -231,28 +284,28 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget) {
     ++peels;
     // every stage in its own lane: subtract c w^{t f} from bucket f mod B_j,
     // reclassify; new single-tons are queued in stage order
-    Verdict v{0, 0, cmk(0.0, 0.0)};
-    int64_t gi = 0;
+    PeelState cur{};
+    int64_t gi = -1;
     int tier = 0;
     if (lane < a.nst) {
       const int j = lane;
       const int64_t b = f % a.Bs[j];
-      double2 mv[3];
       for (int t = 0; t < a.sh[j]; ++t) {
         double2* mp = a.meas + a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b;
-        mv[t] = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
-        *mp = mv[t];
+        cur.m[t] = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
+        *mp = cur.m[t];
       }
-      v = classify_one(a, s, j, b, a.err + s, mv);
+      cur.v = classify_one(a, s, j, b, a.err + s, cur.m);
       gi = a.boff[j] + b;
-      kind[gi] = v.kind;
-      cfs[gi] = v.f;
-      ccs[gi] = v.c;
+      kind[gi] = cur.v.kind;
+      cfs[gi] = cur.v.f;
+      ccs[gi] = cur.v.c;
       tier = a.sh[j] >= 3 ? 0 : 1;
     }
+    const bool is_single = lane < a.nst && cur.v.kind == 1;
     for (int tr = 0; tr < 2; ++tr) {
-      const unsigned push = __ballot_sync(0xffffffffu, lane < a.nst && v.kind == 1 && tier == tr);
-      if (lane < a.nst && v.kind == 1 && tier == tr) {
+      const unsigned push = __ballot_sync(0xffffffffu, is_single && tier == tr);
+      if (is_single && tier == tr) {
         const int64_t pos = tail[tr] + __popc(push & ((1u << lane) - 1));
         if (pos < a.qcap) q[tr][pos] = gi;
       }
@@ -260,6 +313,136 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget) {
       tail[tr] = (int32_t)(nt < a.qcap ? nt : a.qcap);
     }
     __syncwarp();
+
+    // ---- two-state cycle: detect, verify, fast-forward (see the header) ----
+    const bool rep = f == f1 && f == f2;
+    bool ok = rep && live_tier >= 0 && peels >= next_try && peels < budget;
+    if (ok) {
+      const bool mine = lane >= a.nst || same_state(cur, h2, (int)a.sh[lane < a.nst ? lane : 0]);
+      ok = __all_sync(0xffffffffu, mine);
+    }
+    // single-ton buckets of the two states; those whose class is exactly the
+    // pair (f, coefficient) the last two peels used may be popped in the replay
+    // (c0: applied to the state two peels ago = this one; c1: to the previous)
+    unsigned pm0 = 0, pm1 = 0, gm0 = 0, gm1 = 0;
+    const double2 c0 = cprev, c1 = c;
+    if (ok) {
+      const bool s1 = lane < a.nst && h1.v.kind == 1;
+      pm0 = __ballot_sync(0xffffffffu, is_single);
+      pm1 = __ballot_sync(0xffffffffu, s1);
+      gm0 = __ballot_sync(0xffffffffu, is_single && cur.v.f == f && same_bits(cur.v.c, c0));
+      gm1 = __ballot_sync(0xffffffffu, s1 && h1.v.f == f && same_bits(h1.v.c, c1));
+      ok = gm0 != 0 && gm1 != 0;
+    }
+    if (ok) {
+      next_try = peels + 32;  // a failed attempt is retried after the queue has moved on
+      // queued entries: the live tier may hold entries of the cycle's buckets
+      // (kept, as stage ids) and stale entries of others (dropped: their class
+      // cannot change any more); a single-ton elsewhere ends the attempt
+      ok = head[1 - live_tier] >= tail[1 - live_tier];
+      int L0 = 0;
+      for (int64_t base = head[live_tier]; ok && base < tail[live_tier]; base += 32) {
+        const int64_t at = base + lane;
+        const int64_t e = at < tail[live_tier] ? q[live_tier][at] : -1;
+        int stage = -1;
+        for (int j = 0; j < a.nst; ++j)
+          if (e == __shfl_sync(0xffffffffu, gi, j)) stage = j;
+        const bool breaker = e >= 0 && stage < 0 && kind[e] == 1;
+        const unsigned keep = __ballot_sync(0xffffffffu, stage >= 0);
+        if (__any_sync(0xffffffffu, breaker) || L0 + __popc(keep) > kPeelOldCap) {
+          ok = false;
+          break;
+        }
+        if (stage >= 0) s_old[L0 + __popc(keep & ((1u << lane) - 1))] = (int8_t)stage;
+        L0 += __popc(keep);
+      }
+      __syncwarp();
+      if (ok) {
+        // integer replay of the pops (warp-uniform): after the kept entries the
+        // queue is the groups pushed by the alternating states, pm1 first
+        const int n0 = __popc(pm0), n1 = __popc(pm1), W = n0 + n1;
+        int64_t ptr = 0, end = L0, lag_prev = -1, off_prev = -1;
+        int qpar = 0;  // parity of the state the next pop sees (0: this peel's)
+        bool steady = false;
+        int64_t simmed = 0;
+        for (int step = 0; step < kPeelSimSteps && peels + simmed < budget; ++step) {
+          const unsigned pm = qpar ? pm1 : pm0;
+          bool found = false;
+          while (ptr < end) {
+            int stage;
+            if (ptr < L0) {
+              stage = s_old[ptr];
+            } else {
+              const int r = (int)((ptr - L0) % W);
+              stage = r < n1 ? __fns(pm1, 0, r + 1) : __fns(pm0, 0, r - n1 + 1);
+            }
+            ++ptr;
+            if ((pm >> stage) & 1u) {
+              found = ((qpar ? gm1 : gm0) >> stage) & 1u;  // another class: not this cycle
+              break;
+            }
+          }
+          if (!found) break;  // dry queue or another single-ton: leave it to the loop
+          ++simmed;
+          qpar ^= 1;
+          end += qpar ? n1 : n0;
+          if (qpar == 0 && ptr >= L0) {
+            const int64_t off = (ptr - L0) % W, lag = end - ptr;
+            if (off == off_prev && lag >= lag_prev) { steady = true; break; }
+            off_prev = off;
+            lag_prev = lag;
+          }
+        }
+        ok = steady || peels + simmed >= budget;
+      }
+      if (ok) {
+        const int64_t R = budget - peels;
+        if (lane == 0) {
+          uint32_t h = pe_slot(f, a.HT);
+          int where = -1;
+          for (int pr = 0; pr < a.HT; ++pr) {
+            const int64_t key = hk[h];
+            if (key == f + 1) { where = hv[h]; break; }
+            if (key == 0) break;
+            h = (h + 1) & (a.HT - 1);
+          }
+          if (where >= 0) {
+            double2 r = rc[where];
+            int64_t i = 0;
+            while (i + 2 <= R) {
+              const double2 r1 = cadd(r, c0);
+              const double2 r2 = cadd(r1, c1);
+              if (same_bits(r2, r)) {  // the additions repeat as well
+                i = R - ((R - i) & 1);
+                break;
+              }
+              r = r2;
+              i += 2;
+            }
+            if (i < R) r = cadd(r, c0);
+            rc[where] = r;
+          }
+          // (f was recorded by the earlier peels; with the table full it never was,
+          // and the loop would not record it either)
+        }
+        if ((R & 1) && lane < a.nst) {  // an odd remainder ends in the other state
+          const int j = lane;
+          const int64_t b = f % a.Bs[j];
+          for (int t = 0; t < a.sh[j]; ++t)
+            a.meas[a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b] = h1.m[t];
+          kind[gi] = h1.v.kind;
+          cfs[gi] = h1.v.f;
+          ccs[gi] = h1.v.c;
+        }
+        peels = budget;
+        break;
+      }
+    }
+    h2 = h1;
+    h1 = cur;
+    f2 = f1;
+    f1 = f;
+    cprev = c;
   }
   if (lane == 0) {
     a.rec_count[s] = nrec;
@@ -460,7 +643,8 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   SFFT_CHECK_LAUNCH("k_pe_classify_all");
   k_pe_queue_init<<<S, 1024, 0, st>>>(a);
   SFFT_CHECK_LAUNCH("k_pe_queue_init");
-  k_pe_peel<<<S, 32, 0, st>>>(a, d.budget);
+  // SFFT_PEEL_NO_FF=1: run every peel of a cycle (A/B measurement and the parity test)
+  k_pe_peel<<<S, 32, 0, st>>>(a, d.budget, getenv("SFFT_PEEL_NO_FF") ? 0 : 1);
   SFFT_CHECK_LAUNCH("k_pe_peel");
   k_pe_stuck<<<S, 256, 0, st>>>(a, out_conv, out_iters);
   SFFT_CHECK_LAUNCH("k_pe_stuck");

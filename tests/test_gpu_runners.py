@@ -359,3 +359,52 @@ def test_samples_read_memo_equals_direct_count(sb, monkeypatch):
     for u, v in zip(*out):
         assert torch.equal(u, v)
     assert len(set(out[0][0].tolist())) < 40  # schedules are shared
+
+
+def _timed(fn):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def test_peeling_cycle_fast_forward(sb, monkeypatch):
+    """C4 seed 213 exhausts the reference's peel budget (k + sum B_j = 77,679
+    peels) in a two-state cycle on one position.  The device fast-forwards the
+    cycle once it has proved it (csrc/peeling.cu, k_pe_peel): same support,
+    peel count and convergence flag as the oracle on the same complex64-rounded
+    input, and bit-identical to the device loop run peel by peel
+    (SFFT_PEEL_NO_FF=1), together with neighbouring seeds that do not cycle."""
+    import torch
+    from oracle import sfft_oracle as O
+    n, k, factors = 3_888_000, 200, (128, 125, 243)
+    seeds = [211, 212, 213, 214]
+    xs = [O.synth(n, k, None, s)[0].astype(np.complex64) for s in seeds]
+    X = torch.stack([torch.as_tensor(x) for x in xs]).cuda()
+    cfg = sb.AlgorithmConfig(framework="peeling", coprime_factors=factors)
+    sb.run_peeling_batch(X, k, cfg)  # warm-up (workspaces)
+    t0 = _timed(lambda: sb.run_peeling_batch(X, k, cfg))
+    rf = sb.run_peeling_batch(X, k, cfg).to_results()
+    monkeypatch.setenv("SFFT_PEEL_NO_FF", "1")
+    t1 = _timed(lambda: sb.run_peeling_batch(X, k, cfg))
+    rs = sb.run_peeling_batch(X, k, cfg).to_results()
+    monkeypatch.delenv("SFFT_PEEL_NO_FF")
+    assert t0 < 0.2 * t1, (t0, t1)  # the cycle was fast-forwarded, not run
+    for a, b in zip(rf, rs):
+        assert a.iterations == b.iterations and a.converged == b.converged
+        assert a.samples_read == b.samples_read
+        assert a.spectrum.entries.keys() == b.spectrum.entries.keys()
+        for f, c in a.spectrum.entries.items():
+            assert np.complex128(c).tobytes() == np.complex128(b.spectrum.entries[f]).tobytes()
+    want = O.peeling(O.Access(xs[2].astype(np.complex128)), k,
+                     O.Cfg(framework="peeling", coprime_factors=factors))
+    got = rf[2]
+    assert got.iterations == want.iterations == k + sum(n // p for p in factors)
+    assert got.converged == want.converged
+    assert set(got.spectrum.entries) == set(want.entries)
+    err = max(abs(got.spectrum.entries[f] - c) / abs(c) for f, c in want.entries.items())
+    assert err <= 1e-10
