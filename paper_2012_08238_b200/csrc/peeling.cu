@@ -213,10 +213,38 @@ constexpr int kPeelSimSteps = 4096; // pops replayed before the attempt is given
 // the two coefficients alternately (the additions are carried out, stopping
 // early once they too repeat), and the budget is reached.  Results, peel
 // count and final classes are bit-identical to running the loop.
+//
+// Windows of independent peels.  The loop is sequential by definition, but a
+// peel only reads and writes the buckets of its own position (one per stage)
+// and its own recovered entry, so consecutive pops whose bucket sets are
+// disjoint — and disjoint from every queue entry passed over on the way —
+// give the same moments, classes, queue order and sums whether they run one
+// after the other or side by side.  Each step the warp walks the verified
+// queue in order, drops stale entries, and accepts up to 32/stages single-tons
+// until an entry or a position touches a bucket of an already accepted peel
+// (that entry stays queued: its class may change); lane p*stages + j then
+// peels stage j of the p-th accepted position, and the pushes are compacted in
+// lane order = the loop's order.  Unverified (two-shift) stages are drawn on
+// one peel at a time, as their pushes to the verified queue take precedence.
+__device__ __forceinline__ int64_t bucket_mod(int64_t f, int64_t B, double invB) {
+  int64_t r = f - __double2ll_rz((double)f * invB) * B;  // f < 2^53
+  if (r < 0) r += B;
+  if (r >= B) r -= B;
+  return r;
+}
+
 __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
   __shared__ int8_t s_old[kPeelOldCap];
   const int s = blockIdx.x;
   const int lane = threadIdx.x;
+  const int nst = a.nst;
+  const int G = 32 / nst;             // peels side by side
+  const int jL = lane % nst;          // this lane's stage
+  const int pL = lane / nst;          // ... and window slot
+  const int64_t BL = a.Bs[jL], boffL = a.boff[jL];
+  const double invBL = 1.0 / (double)BL;
+  const int shL = (int)a.sh[jL];
+  const int tierL = shL >= 3 ? 0 : 1;
   int64_t head[2] = {0, 0};
   int32_t tail[2] = {a.qtail[0][s], a.qtail[1][s]};
   int64_t* q[2] = {a.q[0] + (int64_t)s * a.qcap, a.q[1] + (int64_t)s * a.qcap};
@@ -232,80 +260,125 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
   // all stages in one tier (the replay below handles a single live queue)
   int live_tier = a.sh[0] >= 3 ? 0 : 1;
   if (!fast_forward) live_tier = -1;
-  for (int j = 1; j < a.nst; ++j)
+  for (int j = 1; j < nst; ++j)
     if ((a.sh[j] >= 3 ? 0 : 1) != live_tier) live_tier = -1;
+  const int window = fast_forward == 1 ? G : 1;  // 0 / 2: one peel per step
   PeelState h1{}, h2{};  // this lane's bucket after the previous peel / the one before
   int64_t f1 = -1, f2 = -1;
   double2 cprev = cmk(0.0, 0.0);  // coefficient of the previous peel
   int64_t next_try = 0;
   while (peels < budget) {
-    // pop the first still-single entry, verified tier first (all lanes agree);
-    // the warp checks 32 queue entries per step instead of one
-    int64_t g = -1;
-    for (int tier = 0; tier < 2 && g < 0; ++tier) {
-      while (head[tier] < tail[tier]) {
-        const int64_t at = head[tier] + lane;
-        const int64_t e = at < tail[tier] ? q[tier][at] : -1;
-        const bool single = e >= 0 && kind[e] == 1;
-        const unsigned hit = __ballot_sync(0xffffffffu, single);
-        if (hit) {
-          const int first = __ffs(hit) - 1;
-          g = __shfl_sync(0xffffffffu, e, first);
-          head[tier] += first + 1;
-          break;
+    // ---- the window: accepted peel p lives in lanes p*nst .. p*nst + nst-1
+    int m = 0;
+    int64_t my_gid = -1, my_f = 0;
+    double2 my_c = cmk(0.0, 0.0);
+    for (int tr = 0; tr < 2 && m == 0; ++tr) {
+      const int cap_m = tr == 0 ? window : 1;
+      bool stop = false;
+      while (!stop && head[tr] < tail[tr]) {
+        const int64_t at = head[tr] + lane;
+        const int64_t e = at < tail[tr] ? q[tr][at] : -1;
+        const int kd = e >= 0 ? kind[e] : 0;
+        int64_t fe = 0;
+        double2 ce = cmk(0.0, 0.0);
+        if (kd == 1) {
+          fe = cfs[e];
+          ce = ccs[e];
         }
-        head[tier] = (head[tier] + 32 < tail[tier]) ? head[tier] + 32 : tail[tier];
+        const int64_t left = tail[tr] - head[tr];
+        const int cnt = left < 32 ? (int)left : 32;
+        int used = 0;
+        for (int i = 0; i < cnt; ++i) {
+          const int64_t ei = __shfl_sync(0xffffffffu, e, i);
+          const int kdi = __shfl_sync(0xffffffffu, kd, i);
+          bool clash = my_gid == ei;
+          int64_t fi = 0, gnew = -1;
+          if (kdi == 1) {
+            fi = __shfl_sync(0xffffffffu, fe, i);
+            gnew = boffL + bucket_mod(fi, BL, invBL);
+            clash = clash || my_gid == gnew;
+          }
+          if (__any_sync(0xffffffffu, my_gid >= 0 && clash)) {
+            stop = true;  // it meets an accepted peel's bucket: decided after this step
+            break;
+          }
+          used = i + 1;
+          if (kdi == 1) {
+            const double cx = __shfl_sync(0xffffffffu, ce.x, i);
+            const double cy = __shfl_sync(0xffffffffu, ce.y, i);
+            if (pL == m && pL < G) {
+              my_gid = gnew;
+              my_f = fi;
+              my_c = cmk(cx, cy);
+            }
+            ++m;
+            if (m >= cap_m || peels + m >= budget) {
+              stop = true;
+              break;
+            }
+          }
+        }
+        head[tr] += used;
       }
     }
-    if (g < 0) break;
-    const int64_t f = cfs[g];
-    const double2 c = ccs[g];
-    int grew = 0;
-    if (lane == 0) {
-      uint32_t h = pe_slot(f, a.HT);
-      int where = -1;
+    if (m == 0) break;
+    const bool active = pL < m && pL < G;
+    // ---- recovered[f] += c: the positions of a window differ, so look-ups
+    // are independent; new ones take consecutive indices in window order
+    const bool lead = active && jL == 0;
+    int where = -1;
+    uint32_t hslot = 0;
+    if (lead) {
+      hslot = pe_slot(my_f, a.HT);
       for (int pr = 0; pr < a.HT; ++pr) {
-        const int64_t key = hk[h];
-        if (key == f + 1) { where = hv[h]; break; }
+        const int64_t key = __ldcg(hk + hslot);
+        if (key == my_f + 1) { where = __ldcg(hv + hslot); break; }
         if (key == 0) break;
-        h = (h + 1) & (a.HT - 1);
-      }
-      if (where >= 0) {
-        rc[where] = cadd(rc[where], c);
-      } else if (nrec < a.cap) {
-        hk[h] = f + 1;
-        hv[h] = nrec;
-        rp[nrec] = f;
-        rc[nrec] = c;
-        grew = 1;
+        hslot = (hslot + 1) & (a.HT - 1);
       }
     }
-    nrec += __shfl_sync(0xffffffffu, grew, 0);
-    ++peels;
-    // every stage in its own lane: subtract c w^{t f} from bucket f mod B_j,
-    // reclassify; new single-tons are queued in stage order
+    const unsigned fresh = __ballot_sync(0xffffffffu, lead && where < 0);
+    if (lead) {
+      if (where >= 0) {
+        rc[where] = cadd(rc[where], my_c);
+      } else {
+        const int idx = nrec + __popc(fresh & ((1u << lane) - 1));
+        if (idx < a.cap) {
+          while (atomicCAS((unsigned long long*)(hk + hslot), 0ull,
+                           (unsigned long long)(my_f + 1)) != 0ull)
+            hslot = (hslot + 1) & (a.HT - 1);
+          hv[hslot] = idx;
+          rp[idx] = my_f;
+          rc[idx] = my_c;
+        }
+      }
+    }
+    {
+      const int grown = nrec + __popc(fresh);
+      nrec = grown < a.cap ? grown : a.cap;
+    }
+    peels += m;
+    // ---- every (peel, stage) in its own lane: subtract c w^{t f} from bucket
+    // f mod B_j, reclassify; new single-tons are queued in (peel, stage) order
     PeelState cur{};
-    int64_t gi = -1;
-    int tier = 0;
-    if (lane < a.nst) {
-      const int j = lane;
-      const int64_t b = f % a.Bs[j];
-      for (int t = 0; t < a.sh[j]; ++t) {
+    const int64_t gi = my_gid;
+    if (active) {
+      const int j = jL;
+      const int64_t b = gi - boffL;
+      for (int t = 0; t < shL; ++t) {
         double2* mp = a.meas + a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b;
-        cur.m[t] = csub(*mp, cmul(c, unit_root(a.n, mulmod(t, f % a.n, a.n))));
+        cur.m[t] = csub(*mp, cmul(my_c, unit_root(a.n, mulmod(t, my_f % a.n, a.n))));
         *mp = cur.m[t];
       }
       cur.v = classify_one(a, s, j, b, a.err + s, cur.m);
-      gi = a.boff[j] + b;
       kind[gi] = cur.v.kind;
       cfs[gi] = cur.v.f;
       ccs[gi] = cur.v.c;
-      tier = a.sh[j] >= 3 ? 0 : 1;
     }
-    const bool is_single = lane < a.nst && cur.v.kind == 1;
+    const bool is_single = active && cur.v.kind == 1;
     for (int tr = 0; tr < 2; ++tr) {
-      const unsigned push = __ballot_sync(0xffffffffu, is_single && tier == tr);
-      if (is_single && tier == tr) {
+      const unsigned push = __ballot_sync(0xffffffffu, is_single && tierL == tr);
+      if (is_single && tierL == tr) {
         const int64_t pos = tail[tr] + __popc(push & ((1u << lane) - 1));
         if (pos < a.qcap) q[tr][pos] = gi;
       }
@@ -313,6 +386,12 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
       tail[tr] = (int32_t)(nt < a.qcap ? nt : a.qcap);
     }
     __syncwarp();
+    if (m > 1) {  // the cycle test below follows single peels only
+      f1 = f2 = -1;
+      continue;
+    }
+    const int64_t f = __shfl_sync(0xffffffffu, my_f, 0);
+    const double2 c = cmk(__shfl_sync(0xffffffffu, my_c.x, 0), __shfl_sync(0xffffffffu, my_c.y, 0));
 
     // ---- two-state cycle: detect, verify, fast-forward (see the header) ----
     const bool rep = f == f1 && f == f2;
@@ -401,8 +480,8 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
           uint32_t h = pe_slot(f, a.HT);
           int where = -1;
           for (int pr = 0; pr < a.HT; ++pr) {
-            const int64_t key = hk[h];
-            if (key == f + 1) { where = hv[h]; break; }
+            const int64_t key = __ldcg(hk + h);
+            if (key == f + 1) { where = __ldcg(hv + h); break; }
             if (key == 0) break;
             h = (h + 1) & (a.HT - 1);
           }
@@ -643,8 +722,10 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   SFFT_CHECK_LAUNCH("k_pe_classify_all");
   k_pe_queue_init<<<S, 1024, 0, st>>>(a);
   SFFT_CHECK_LAUNCH("k_pe_queue_init");
-  // SFFT_PEEL_NO_FF=1: run every peel of a cycle (A/B measurement and the parity test)
-  k_pe_peel<<<S, 32, 0, st>>>(a, d.budget, getenv("SFFT_PEEL_NO_FF") ? 0 : 1);
+  // SFFT_PEEL_NO_FF=1: the plain loop, one peel per step and every peel of a cycle
+  // run; SFFT_PEEL_WINDOW=1: cycles fast-forwarded, one peel per step (A/B
+  // measurement and the parity test)
+  k_pe_peel<<<S, 32, 0, st>>>(a, d.budget, getenv("SFFT_PEEL_NO_FF") ? 0 : (getenv("SFFT_PEEL_WINDOW") ? 2 : 1));
   SFFT_CHECK_LAUNCH("k_pe_peel");
   k_pe_stuck<<<S, 256, 0, st>>>(a, out_conv, out_iters);
   SFFT_CHECK_LAUNCH("k_pe_stuck");
