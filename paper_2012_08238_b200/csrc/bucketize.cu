@@ -553,6 +553,174 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
   }
 }
 
+// ---- power-of-two four-step passes (flat B = 2^13 .. 2^18: the config-5 grid)
+// Both passes transform G lines of length M (64..512) per CTA in shared
+// memory, line g at s + g*(M+1): thread t works on line t % G, so the eight
+// threads of a 16-byte shared-memory phase always sit on eight different lines
+// (odd line pitch: no bank conflicts at any butterfly stride) while global
+// loads and stores run along the contiguous axis (G x 16 bytes or a whole
+// line).  Radix-8 register butterflies (dft8_, then one radix-4/2 stage),
+// stage twiddles w_M^e in shared memory, digit reversal by pow2_pos.
+//   pass 1 (columns): DFT_B1 over n1 of z[n1 B2 + n2], times w_B^{n2 k1},
+//                     stored at ws[k1 B2 + n2]
+//   pass 2 (rows):    DFT_B2 over n2 of ws[k1 B2 + n2]; y[k1 + B1 k2] = ./B
+constexpr int kF4NT = 512;
+constexpr int fs_lines(int M) { return M <= 128 ? 32 : (M == 256 ? 16 : 8); }
+
+template <int M, int G>
+__device__ __forceinline__ void fs_lines_fft(double2* __restrict__ s,
+                                             const double2* __restrict__ tw) {
+  constexpr int NB = kF4NT / G;  // butterflies of a line side by side
+  const int g = threadIdx.x % G, bi = threadIdx.x / G;
+  double2* line = s + g * (M + 1);
+  int Mb = M;
+#pragma unroll
+  for (int st = 0; st < Pow2<M>::N8; ++st) {
+    const int Mp = Mb >> 3;
+    const int tstr = M / Mb;
+    for (int tt = bi; tt < M / 8; tt += NB) {
+      const int blk = tt / Mp, j = tt - blk * Mp;
+      double2* x = line + blk * Mb + j;
+      double2 a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = x[q * Mp];
+      dft8_(a);
+      x[0] = a[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) x[q * Mp] = j ? cmul(a[q], tw[j * q * tstr]) : a[q];
+    }
+    __syncthreads();
+    Mb = Mp;
+  }
+  if (Pow2<M>::RL == 4) {
+    for (int tt = bi; tt < M / 4; tt += NB) {
+      double2* x = line + 4 * tt;
+      dft4_(x[0], x[1], x[2], x[3]);
+    }
+    __syncthreads();
+  } else if (Pow2<M>::RL == 2) {
+    for (int tt = bi; tt < M / 2; tt += NB) {
+      double2* x = line + 2 * tt;
+      const double2 u = x[0], v = x[1];
+      x[0] = cadd(u, v);
+      x[1] = csub(u, v);
+    }
+    __syncthreads();
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kF4NT) k_fs_cols(Prod p, int B2, const double2* __restrict__ W,
+                                                   double2* __restrict__ ws) {
+  constexpr int G = fs_lines(M);
+  extern __shared__ double2 fs_s[];
+  double2* tw = fs_s + G * (M + 1);
+  const int item = blockIdx.y;
+  const int sig = p.item_sig ? p.item_sig[item] : item;
+  if ((p.active && !p.active[sig]) || (p.item_active && !p.item_active[item])) return;
+  const int B = M * B2;
+  const int c0 = blockIdx.x * G;
+  const double2* in = p.z + out_row(p, item) * (int64_t)B;
+  for (int e = threadIdx.x; e < M; e += kF4NT) tw[e] = __ldg(W + (int64_t)e * B2);
+  for (int t = threadIdx.x; t < G * M; t += kF4NT) {
+    const int g = t % G, n1 = t / G;
+    fs_s[g * (M + 1) + n1] = in[(int64_t)n1 * B2 + c0 + g];
+  }
+  __syncthreads();
+  fs_lines_fft<M, G>(fs_s, tw);
+  double2* o = ws + (int64_t)item * B;
+  for (int t = threadIdx.x; t < G * M; t += kF4NT) {
+    const int g = t % G, k1 = t / G;
+    const int n2 = c0 + g;
+    const double2 v = fs_s[g * (M + 1) + pow2_pos<M>(k1)];
+    const int e = n2 * k1;  // < B
+    o[(int64_t)k1 * B2 + n2] = e ? cmul(v, __ldg(W + e)) : v;
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kF4NT) k_fs_rows(Prod p, int B1, const double2* __restrict__ W,
+                                                   const double2* __restrict__ ws,
+                                                   double2* __restrict__ out) {
+  constexpr int G = fs_lines(M);
+  extern __shared__ double2 fs_s[];
+  double2* tw = fs_s + G * (M + 1);
+  const int item = blockIdx.y;
+  const int sig = p.item_sig ? p.item_sig[item] : item;
+  if ((p.active && !p.active[sig]) || (p.item_active && !p.item_active[item])) return;
+  const int B = M * B1;
+  const int r0 = blockIdx.x * G;
+  const double2* in = ws + (int64_t)item * B + (int64_t)r0 * M;
+  for (int e = threadIdx.x; e < M; e += kF4NT) tw[e] = __ldg(W + (int64_t)e * B1);
+  for (int t = threadIdx.x; t < G * M; t += kF4NT) {
+    const int g = t / M, n2 = t - g * M;
+    fs_s[g * (M + 1) + n2] = in[t];
+  }
+  __syncthreads();
+  fs_lines_fft<M, G>(fs_s, tw);
+  double2* o = out + out_row(p, item) * (int64_t)B;
+  const double bd = (double)B;
+  for (int t = threadIdx.x; t < G * M; t += kF4NT) {
+    const int g = t % G, k2 = t / G;
+    o[r0 + g + (int64_t)B1 * k2] = cdivr(fs_s[g * (M + 1) + pow2_pos<M>(k2)], bd);
+  }
+}
+
+template <int M>
+static int launch_fs_cols(const Prod& p, int64_t nitems, int64_t B2, const double2* W, double2* ws,
+                          cudaStream_t st) {
+  constexpr int G = fs_lines(M);
+  const size_t sm = (size_t)(G * (M + 1) + M) * sizeof(double2);
+  SFFT_CUDA(cudaFuncSetAttribute(k_fs_cols<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+  k_fs_cols<M><<<dim3((unsigned)(B2 / G), (unsigned)nitems), kF4NT, sm, st>>>(p, (int)B2, W, ws);
+  SFFT_CHECK_LAUNCH("k_fs_cols");
+  return 0;
+}
+
+template <int M>
+static int launch_fs_rows(const Prod& p, int64_t nitems, int64_t B1, const double2* W,
+                          const double2* ws, double2* out, cudaStream_t st) {
+  constexpr int G = fs_lines(M);
+  const size_t sm = (size_t)(G * (M + 1) + M) * sizeof(double2);
+  SFFT_CUDA(cudaFuncSetAttribute(k_fs_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+  k_fs_rows<M><<<dim3((unsigned)(B1 / G), (unsigned)nitems), kF4NT, sm, st>>>(p, (int)B1, W, ws,
+                                                                             out);
+  SFFT_CHECK_LAUNCH("k_fs_rows");
+  return 0;
+}
+
+// B = B1*B2 with B1 = 2^floor(lg/2); both in 64..512 for B = 2^12 .. 2^18.
+static bool fs_pow2_split(int64_t B, int64_t* B1, int64_t* B2) {
+  if (B < 4096 || B > (1 << 18) || (B & (B - 1))) return false;
+  int lg = 0;
+  while (((int64_t)1 << lg) < B) ++lg;
+  *B1 = (int64_t)1 << (lg / 2);
+  *B2 = B / *B1;
+  return true;
+}
+
+// The two passes over rows already in natural order at p.z (row of item i =
+// out_row(p, i)); ws holds the intermediate, results land in out's rows.
+static int run_fs_pow2(const Prod& p, int64_t nitems, int64_t B1, int64_t B2, const double2* W,
+                       double2* ws, double2* out, cudaStream_t st) {
+  int rc;
+  switch (B1) {
+    case 64: rc = launch_fs_cols<64>(p, nitems, B2, W, ws, st); break;
+    case 128: rc = launch_fs_cols<128>(p, nitems, B2, W, ws, st); break;
+    case 256: rc = launch_fs_cols<256>(p, nitems, B2, W, ws, st); break;
+    default: rc = launch_fs_cols<512>(p, nitems, B2, W, ws, st); break;
+  }
+  if (rc) return rc;
+  switch (B2) {
+    case 64: return launch_fs_rows<64>(p, nitems, B1, W, ws, out, st);
+    case 128: return launch_fs_rows<128>(p, nitems, B1, W, ws, out, st);
+    case 256: return launch_fs_rows<256>(p, nitems, B1, W, ws, out, st);
+    default: return launch_fs_rows<512>(p, nitems, B1, W, ws, out, st);
+  }
+}
+
 // Four-step flat path, fold pass: the folded slots of every item, two per
 // thread (8 gathers in flight, rows in reference order), written to the item's
 // output row, which the column pass then reads coalesced (PROD_LOAD) before the
@@ -1142,12 +1310,30 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
                "bucketize: workspace too small for the four-step path");
   double2* z = (double2*)ws;
   int64_t B1, B2;
+  // power-of-two B >= 8192 (flat fold pass or rows already folded): the
+  // line-per-thread radix-8 passes; SFFT_NO_FS_POW2=1 keeps the generic ones
+  static const bool fs_pow2_on = !getenv("SFFT_NO_FS_POW2");
+  if (fs_pow2_on && (MODE == PROD_FLAT || MODE == PROD_LOAD) && B >= 8192 &&
+      fs_pow2_split(B, &B1, &B2)) {
+    Prod pz = p;
+    if (MODE == PROD_FLAT) {
+      dim3 gf((unsigned)cdiv_up(B, 2 * kFrNT), (unsigned)nitems);
+      k_fold_rows<Tin><<<gf, kFrNT, 0, st>>>(p, out);
+      SFFT_CHECK_LAUNCH("k_fold_rows");
+      pz.z = out;
+      pz.prof_items = nullptr;
+    }
+    return run_fs_pow2(pz, nitems, B1, B2, W, z, out, st);
+  }
   if (split_plan(B, &B1, &B2)) {
     FftPlan P1, P2;
     make_plan(B1, &P1);
     make_plan(B2, &P2);
-    const int CG = (int)std::max<int64_t>(1, std::min<int64_t>(B2, kFusedMaxB / (B1 + 1)));
-    const int RG = (int)std::max<int64_t>(1, std::min<int64_t>(B1, kFusedMaxB / (B2 + 1)));
+    // columns / rows per CTA: SFFT_FS_CAP shared-memory entries per CTA
+    static const int64_t fs_cap =
+        getenv("SFFT_FS_CAP") ? std::max<int64_t>(256, atoll(getenv("SFFT_FS_CAP"))) : kFusedMaxB;
+    const int CG = (int)std::max<int64_t>(1, std::min<int64_t>(B2, fs_cap / (B1 + 1)));
+    const int RG = (int)std::max<int64_t>(1, std::min<int64_t>(B1, fs_cap / (B2 + 1)));
     const size_t smc = (size_t)CG * (B1 + 1) * sizeof(double2);
     const size_t smr = (size_t)RG * (B2 + 1) * sizeof(double2);
     if (ensure_smem(k_cols<Tin, MODE>, smc)) return -3;

@@ -279,9 +279,9 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
         const int64_t at = head[tr] + lane;
         const int64_t e = at < tail[tr] ? q[tr][at] : -1;
         const int kd = e >= 0 ? kind[e] : 0;
-        int64_t fe = 0;
+        int64_t fe = 0;  // requested with the class, not after it: one round trip less
         double2 ce = cmk(0.0, 0.0);
-        if (kd == 1) {
+        if (e >= 0) {
           fe = cfs[e];
           ce = ccs[e];
         }
@@ -323,6 +323,15 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
     }
     if (m == 0) break;
     const bool active = pL < m && pL < G;
+    // the buckets' moments are requested before the recovered-table look-up
+    // below, so the two round trips overlap
+    double2 mold[3] = {cmk(0.0, 0.0), cmk(0.0, 0.0), cmk(0.0, 0.0)};
+    double2* mp0 = a.meas + a.moff[jL] + (int64_t)s * BL + (my_gid - boffL);
+    if (active) {
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        if (t < shL) mold[t] = mp0[(int64_t)t * a.S * BL];
+    }
     // ---- recovered[f] += c: the positions of a window differ, so look-ups
     // are independent; new ones take consecutive indices in window order
     const bool lead = active && jL == 0;
@@ -365,10 +374,12 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
     if (active) {
       const int j = jL;
       const int64_t b = gi - boffL;
-      for (int t = 0; t < shL; ++t) {
-        double2* mp = a.meas + a.moff[j] + ((int64_t)t * a.S + s) * a.Bs[j] + b;
-        cur.m[t] = csub(*mp, cmul(my_c, unit_root(a.n, mulmod(t, my_f % a.n, a.n))));
-        *mp = cur.m[t];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        if (t < shL) {
+          cur.m[t] = csub(mold[t], cmul(my_c, unit_root(a.n, mulmod(t, my_f % a.n, a.n))));
+          mp0[(int64_t)t * a.S * BL] = cur.m[t];
+        }
       }
       cur.v = classify_one(a, s, j, b, a.err + s, cur.m);
       kind[gi] = cur.v.kind;
