@@ -503,6 +503,9 @@ __global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2
     sm[g * seg + n1] = (n2 < B2) ? produce<Tin, MODE>(p, c, item, (int64_t)n1 * B2 + n2)
                                  : cmk(0.0, 0.0);
   }
+  // digit-reversed positions once per CTA (behind the CG segments)
+  int* pos = (int*)(sm + CG * seg);
+  for (int k = threadIdx.x; k < B1; k += kNT) pos[k] = fft_pos(k, P1);
   __syncthreads();
   fft_dif(sm, CG, seg, P1, W, B, threadIdx.x, kNT);
   double2* o = ws + (int64_t)item * B;
@@ -510,8 +513,8 @@ __global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2
     const int g = t % CG, k1 = t / CG;
     const int n2 = c0 + g;
     if (n2 >= B2) continue;
-    const double2 v = sm[g * seg + fft_pos(k1, P1)];
-    const int64_t e = ((int64_t)n2 * k1) % B;
+    const double2 v = sm[g * seg + pos[k1]];
+    const int e = n2 * k1;  // n2 < B2, k1 < B1: below B, no reduction needed
     o[(int64_t)k1 * B2 + n2] = e ? cmul(v, __ldg(W + e)) : v;
   }
 }
@@ -539,6 +542,8 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
     const int k1 = r0 + g;
     sm[g * seg + n2] = (k1 < B1) ? in[(int64_t)k1 * B2 + n2] : cmk(0.0, 0.0);
   }
+  int* pos = (int*)(sm + RG * seg);
+  for (int k = threadIdx.x; k < B2; k += kNT) pos[k] = fft_pos(k, P2);
   __syncthreads();
   fft_dif(sm, RG, seg, P2, W, B, threadIdx.x, kNT);
   const int64_t row = item_row ? item_row[item]
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
     const int g = t % RG, k2 = t / RG;
     const int k1 = r0 + g;
     if (k1 >= B1) continue;
-    o[k1 + (int64_t)B1 * k2] = cdivr(sm[g * seg + fft_pos(k2, P2)], bd);
+    o[k1 + (int64_t)B1 * k2] = cdivr(sm[g * seg + pos[k2]], bd);
   }
 }
 
@@ -1334,8 +1339,8 @@ static int run_bucketize_t(const Prod& p, int64_t nitems, const double2* W, doub
         getenv("SFFT_FS_CAP") ? std::max<int64_t>(256, atoll(getenv("SFFT_FS_CAP"))) : kFusedMaxB;
     const int CG = (int)std::max<int64_t>(1, std::min<int64_t>(B2, fs_cap / (B1 + 1)));
     const int RG = (int)std::max<int64_t>(1, std::min<int64_t>(B1, fs_cap / (B2 + 1)));
-    const size_t smc = (size_t)CG * (B1 + 1) * sizeof(double2);
-    const size_t smr = (size_t)RG * (B2 + 1) * sizeof(double2);
+    const size_t smc = (size_t)CG * (B1 + 1) * sizeof(double2) + (size_t)B1 * sizeof(int);
+    const size_t smr = (size_t)RG * (B2 + 1) * sizeof(double2) + (size_t)B2 * sizeof(int);
     if (ensure_smem(k_cols<Tin, MODE>, smc)) return -3;
     if (ensure_smem(k_rows, smr)) return -3;
     dim3 gc((unsigned)cdiv_up(B2, CG), (unsigned)nitems);
