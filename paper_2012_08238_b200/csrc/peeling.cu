@@ -580,6 +580,11 @@ __global__ void k_pe_groups(PeelArgs a, Group* groups, int32_t* ngroups) {
   ngroups[s] = ng;
 }
 
+__global__ void k_pe_samples(int64_t* samples, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > 0 && s < S) samples[s] = samples[0];
+}
+
 struct PeelLayout {
   size_t off[24];
   size_t total;
@@ -748,8 +753,15 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
   SFFT_CHECK_LAUNCH("k_finalize");
   k_pe_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(a, groups, ngroups);
   SFFT_CHECK_LAUNCH("k_pe_groups");
-  int rc = run_union_count(groups, ngroups, S, n, out_samples, nullptr, nullptr, st);
-  if (rc) return rc;
+  // every signal reads the same samples (the stages' strides and shifts do not
+  // depend on the data): the union is counted once, by 64 CTAs, and copied
+  k_zero_rows<<<1, 128, 0, st>>>(out_samples, 1, nullptr, nullptr);
+  SFFT_CHECK_LAUNCH("k_zero_rows");
+  k_union_excl<<<dim3(64, 1), kUxNT, 0, st>>>(groups, ngroups, kMaxGroups, n, nullptr, nullptr,
+                                              (unsigned long long*)out_samples);
+  SFFT_CHECK_LAUNCH("k_union_excl");
+  k_pe_samples<<<(unsigned)cdiv_up(S, 256), 256, 0, st>>>(out_samples, S);
+  SFFT_CHECK_LAUNCH("k_pe_samples");
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(groups, ngroups, S, out_sched);
     SFFT_CHECK_LAUNCH("k_export_groups");
