@@ -479,7 +479,58 @@ __global__ void __launch_bounds__(256) k_vote_collect(VoteRounds vr, FastVote fv
   const int64_t* bps = vr.bprime ? vr.bprime + (int64_t)s * R : nullptr;
   const bool fast32 = MODE == 0 && fv.nmask >= 0 && fv.logL >= 0 && !bps && vr.cs == 0 &&
                       vr.n <= (int64_t(1) << 32) && vr.words <= 64 * 1024;
-  if (fast32) {
+  if (fast32 && vr.words <= 32 && R <= 32) {
+    // B <= 1024: lane w keeps word w of every round's heavy bitmap in a
+    // register and a look-up is one shuffle — no shared-memory bank conflicts
+    // (32 random words over 32 banks serialise ~3.5x).  Two positions per
+    // thread; the warp leaves the round loop once none of its 64 positions can
+    // still reach `need` (a candidate keeps its warp in the loop to the last
+    // round, so its count is complete).
+    const uint32_t mask = (uint32_t)fv.nmask, half = (uint32_t)(vr.L >> 1);
+    const int lg = fv.logL;
+    const int words = (int)vr.words;
+    const int lane = threadIdx.x & 31;
+    uint32_t w[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) w[r] = (r < R && lane < words) ? sb[r * words + lane] : 0u;
+    // t = (sigma f + L/2) mod N: word = t >> (lg + 5), bit = (t >> lg) & 31
+    // (the funnel shift takes its count mod 32)
+    constexpr int P = 4;  // positions per thread
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * P;
+    for (int64_t f0 = (int64_t)blockIdx.x * blockDim.x * P; f0 < vr.n; f0 += step) {
+      uint32_t u[P];
+      int c[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        u[q] = (uint32_t)(f0 + threadIdx.x + (int64_t)q * blockDim.x);
+        c[q] = 0;
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r >= R) break;
+        const uint32_t sg = (uint32_t)ssig[r];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const uint32_t t = (sg * u[q] + half) & mask;
+          const uint32_t wv = __shfl_sync(0xffffffffu, w[r], t >> (lg + 5));
+          c[q] += __funnelshift_r(wv, 0u, t >> lg) & 1u;
+        }
+        if (r & 1) {  // every second round is often enough
+          const int left = R - 1 - r;
+          int best = c[0];
+#pragma unroll
+          for (int q = 1; q < P; ++q) best = max(best, c[q]);
+          if (!__any_sync(0xffffffffu, best + left >= need)) break;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const int64_t f = f0 + threadIdx.x + (int64_t)q * blockDim.x;
+        vappend(f < vr.n && c[q] >= need,
+                ((unsigned long long)(R - c[q]) << 40) | (unsigned long long)f, s, cnt, buf);
+      }
+    }
+  } else if (fast32) {
     // power-of-two N: bucket of f in round r is ((sigma_r f mod 2^32 & (N-1)) + L/2 & (N-1)) >> log2 L
     const uint32_t mask = (uint32_t)fv.nmask, half = (uint32_t)(vr.L >> 1);
     const int lg = fv.logL;

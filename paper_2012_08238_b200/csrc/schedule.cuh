@@ -344,14 +344,17 @@ static __global__ void k_union_gate(int S, const int32_t* gate, const int32_t* f
 }
 
 // Scratch for run_union_count's fallback gate: 2 ints per slot.
-inline size_t union_scratch_bytes(int S) { return sizeof(int32_t) * 2 * (size_t)S; }
+// (a third int per slot is the caller's: the voting runner keeps its
+// shared-schedule gate there)
+inline size_t union_scratch_bytes(int S) { return sizeof(int32_t) * 3 * (size_t)S; }
 
 inline int run_union_count(const Group* groups, const int32_t* ngroups, int S, int64_t n,
                           int64_t* samples, const int32_t* gate, const int32_t* rows,
-                          cudaStream_t st, int32_t* scratch = nullptr) {
+                          cudaStream_t st, int32_t* scratch = nullptr, int ctas_min = 1) {
   k_zero_rows<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(samples, S, gate, rows);
   SFFT_CHECK_LAUNCH("k_zero_rows");
-  const unsigned ctas = (unsigned)std::min<int64_t>(8, std::max<int64_t>(1, n >> 20));
+  const unsigned ctas = (unsigned)std::max<int64_t>(
+      ctas_min, std::min<int64_t>(8, std::max<int64_t>(1, n >> 20)));
   const bool p2 = (n & (n - 1)) == 0 && n <= (int64_t(1) << 31) && scratch;
   const int32_t* g2 = gate;
   if (p2) {

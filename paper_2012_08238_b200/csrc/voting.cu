@@ -157,6 +157,23 @@ __global__ void k_vo_prefilter(VoteArgs a, const uint32_t* pbits, int64_t Bpre) 
   if (threadIdx.x == 0) a.ncand[s] = tot;
 }
 
+// gate[s] = 1 for signal 0 and for every signal whose (sigma, tau) rows differ
+// from signal 0's; the others take signal 0's samples_read.
+__global__ void k_vo_same(const int64_t* __restrict__ psig, const int64_t* __restrict__ ptau,
+                          int S, int R, int32_t* gate) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  bool diff = false;
+  for (int r = 0; r < R; ++r)
+    diff |= psig[(int64_t)s * R + r] != psig[r] || ptau[(int64_t)s * R + r] != ptau[r];
+  gate[s] = (s == 0 || diff) ? 1 : 0;
+}
+
+__global__ void k_vo_samples(int64_t* samples, const int32_t* gate, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S && !gate[s]) samples[s] = samples[0];
+}
+
 __global__ void k_vo_groups(Group* groups, int32_t* ngroups, const int64_t* psig,
                             const int64_t* ptau, int S, int R, int64_t omega, int64_t pre_L,
                             int64_t pre_B) {
@@ -362,9 +379,17 @@ int run_voting(int dtype, const void* x, int64_t n, int64_t xstride, int S, cons
   k_vo_groups<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(groups, ngroups, psig, ptau, S, R, omega,
                                                          pre_L, Bpre);
   SFFT_CHECK_LAUNCH("k_vo_groups");
-  rc = run_union_count(groups, ngroups, S, n, out_samples, nullptr, nullptr, st,
-                      (int32_t*)(w + Lo.off[21]));
+  // signals that share signal 0's permutations read the same samples (the
+  // batched runner draws one seeded stream for the whole batch): those are
+  // counted once, by more CTAs, and copied
+  int32_t* same_gate = (int32_t*)(w + Lo.off[21]) + 2 * (size_t)S;
+  k_vo_same<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(psig, ptau, S, R, same_gate);
+  SFFT_CHECK_LAUNCH("k_vo_same");
+  rc = run_union_count(groups, ngroups, S, n, out_samples, same_gate, nullptr, st,
+                      (int32_t*)(w + Lo.off[21]), 32);
   if (rc) return rc;
+  k_vo_samples<<<(unsigned)cdiv_up(S, 128), 128, 0, st>>>(out_samples, same_gate, S);
+  SFFT_CHECK_LAUNCH("k_vo_samples");
   if (out_sched) {
     k_export_groups<<<S, 64, 0, st>>>(groups, ngroups, S, out_sched);
     SFFT_CHECK_LAUNCH("k_export_groups");
