@@ -458,6 +458,100 @@ __device__ __forceinline__ void vappend(bool take, unsigned long long key, int s
   }
 }
 
+// Bit-sliced vote scan (power-of-two N and B, no b' and no centre shift: the
+// runners' case).  sigma (f0 + j L) = sigma f0 + (sigma j mod B) L, so the
+// bucket of position f0 + j L in round r is (b_r(f0) + sigma_r j) mod B: with
+// the round's heavy bitmap permuted once, P_r[i] = heavy_r[(sigma_r i) mod B],
+// the B positions {f0 + j L} hit exactly the bits of P_r rotated by
+// c_r = sigma_r^-1 b_r(f0) mod B.  A warp takes 1024 of them at a time (one
+// 32-bit word per lane), rotates each round's vector out of shared memory
+// (two conflict-free loads and a funnel shift) and adds it into bit-sliced
+// counters (two logic ops per slice): ~25 instructions per round for 1024
+// positions instead of a multiply, a shuffle and a test per position and
+// round.  Positions whose counter reaches `need` (a sliced comparison) are
+// appended with their exact count, as the scan does.
+template <int NS>
+__global__ void __launch_bounds__(256) k_vote_sliced(VoteRounds vr, FastVote fv, int need,
+                                                     int32_t* cnt, unsigned long long* buf) {
+  extern __shared__ uint32_t vsp[];  // [R][W] permuted bitmaps
+  __shared__ uint32_t vsig[kMaxVoteRounds], vinv[kMaxVoteRounds];
+  const int s = blockIdx.y;
+  const int R = vr.R;
+  const int W = (int)vr.words;
+  const uint32_t Bm = (uint32_t)vr.B - 1u;
+  const uint32_t* gb = vr.bits + (int64_t)s * R * W;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    const uint32_t sg = (uint32_t)vr.sigma[(int64_t)s * R + r];
+    uint32_t x = sg;  // Newton: inverse of an odd number mod 2^32
+    for (int it = 0; it < 5; ++it) x *= 2u - sg * x;
+    vsig[r] = sg;
+    vinv[r] = x;
+  }
+  __syncthreads();
+  for (int wi = threadIdx.x; wi < R * W; wi += blockDim.x) {
+    const int r = wi / W, k = wi - r * W;
+    const uint32_t sg = vsig[r];
+    const uint32_t* bw = gb + (int64_t)r * W;
+    uint32_t word = 0;
+    for (int t = 0; t < 32; ++t) {
+      const uint32_t src = (sg * (uint32_t)(32 * k + t)) & Bm;
+      word |= ((__ldg(bw + (src >> 5)) >> (src & 31)) & 1u) << t;
+    }
+    vsp[wi] = word;
+  }
+  __syncthreads();
+  const uint32_t nmask = (uint32_t)fv.nmask, half = (uint32_t)(vr.L >> 1);
+  const int lg = fv.logL;
+  const int lane = threadIdx.x & 31;
+  const int nchunk = W >= 32 ? W / 32 : 1;
+  const int64_t items = vr.L * nchunk;
+  const int wpb = blockDim.x >> 5;
+  for (int64_t item = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); item < items;
+       item += (int64_t)gridDim.x * wpb) {
+    const uint32_t f0 = (uint32_t)(item / nchunk);
+    const int k = (int)(item % nchunk) * 32 + lane;  // this lane's word of the vector
+    uint32_t sl[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) sl[i] = 0u;
+    for (int r = 0; r < R; ++r) {
+      const uint32_t b0 = ((((vsig[r] * f0) & nmask) + half) & nmask) >> lg;
+      const uint32_t c = (vinv[r] * b0) & Bm;
+      const int cw = (int)(c >> 5);
+      const uint32_t* pr = vsp + r * W;
+      const uint32_t lo = pr[(k + cw) & (W - 1)], hi = pr[(k + cw + 1) & (W - 1)];
+      uint32_t carry = lane < W ? __funnelshift_r(lo, hi, c & 31u) : 0u;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        const uint32_t t = sl[i] & carry;
+        sl[i] ^= carry;
+        carry = t;
+      }
+    }
+    uint32_t gt = 0u, eq = ~0u;
+#pragma unroll
+    for (int i = NS - 1; i >= 0; --i) {
+      const uint32_t nb = ((need >> i) & 1) ? ~0u : 0u;
+      gt |= eq & sl[i] & ~nb;
+      eq &= ~(sl[i] ^ nb);
+    }
+    uint32_t ge = gt | eq;
+    while (__any_sync(0xffffffffu, ge != 0u)) {
+      const bool take = ge != 0u;
+      unsigned long long key = 0ull;
+      if (take) {
+        const int t = __ffs(ge) - 1;
+        ge &= ge - 1u;
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < NS; ++i) c |= (int)((sl[i] >> t) & 1u) << i;
+        const int64_t f = (int64_t)f0 + (int64_t)(32 * k + t) * vr.L;
+        key = ((unsigned long long)(R - c) << 40) | (unsigned long long)f;
+      }
+      vappend(take, key, s, cnt, buf);
+    }
+  }
+}
+
 // mode 0: every position; mode 1: preimages of the heavy buckets of rounds
 // 0..R-need (every position with >= need votes is heavy in one of them),
 // each position counted from its first heavy round only.
@@ -672,7 +766,29 @@ int run_votes_fast(const VoteRounds& vr, int S, int need, int keep, int64_t hc, 
   const size_t sm = vg.bits_global ? 0 : (size_t)vr.R * vr.words * sizeof(uint32_t);
   const int R0 = vr.R - need + 1;
   const bool pre = R0 >= 1 && (double)R0 * hc * vr.L < 0.5 * (double)vr.n;
-  if (pre) {
+  // SFFT_NO_VOTE_SLICED=1 keeps the per-position scans (A/B and the parity test)
+  const bool sliced = !getenv("SFFT_NO_VOTE_SLICED") && fv.nmask >= 0 && fv.logL >= 0 &&
+                      !vr.bprime && vr.cs == 0 && vr.n <= (int64_t(1) << 32) && vr.B >= 32 &&
+                      (vr.B & (vr.B - 1)) == 0 && vr.words * 32 == vr.B && sm > 0 && need >= 1 &&
+                      need <= vr.R;
+  if (sliced) {
+    const int64_t items = vr.L * std::max<int64_t>(1, vr.words / 32);
+    // a CTA permutes the R bitmaps once (~0.04 R B instructions per thread): give
+    // each warp enough 1024-position items (>= B/128) to amortise that
+    const int64_t per_warp = std::max<int64_t>(16, vr.B / 128);
+    const unsigned gx =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(items / (8 * per_warp), 64));
+    if (vr.R <= 31) {
+      SFFT_CUDA(cudaFuncSetAttribute(k_vote_sliced<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm));
+      k_vote_sliced<5><<<dim3(gx, S), 256, sm, st>>>(vg, fv, need, cnt, buf);
+    } else {
+      SFFT_CUDA(cudaFuncSetAttribute(k_vote_sliced<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm));
+      k_vote_sliced<8><<<dim3(gx, S), 256, sm, st>>>(vg, fv, need, cnt, buf);
+    }
+    SFFT_CHECK_LAUNCH("k_vote_sliced");
+  } else if (pre) {
     k_vote_lists<<<dim3(vr.R, S), 256, 0, st>>>(vr, hc, hl, nh, sinv);
     SFFT_CHECK_LAUNCH("k_vote_lists");
     SFFT_CUDA(cudaFuncSetAttribute(k_vote_collect<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,

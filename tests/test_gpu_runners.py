@@ -408,3 +408,27 @@ def test_peeling_cycle_fast_forward(sb, monkeypatch):
     assert set(got.spectrum.entries) == set(want.entries)
     err = max(abs(got.spectrum.entries[f] - c) / abs(c) for f, c in want.entries.items())
     assert err <= 1e-10
+
+
+@pytest.mark.parametrize("n,b,k,rounds", [(1 << 18, 512, 32, 12), (1 << 18, 2048, 32, 40),
+                                          (1 << 14, 32, 4, 10), (1 << 20, 1 << 13, 50, 10)])
+def test_voting_sliced_scan_identical(sb, monkeypatch, n, b, k, rounds):
+    """The bit-sliced vote scan (k_vote_sliced: permuted heavy bitmaps rotated
+    per family of positions f0 + j L, bit-sliced counters) selects exactly the
+    candidates of the per-position scans (SFFT_NO_VOTE_SLICED=1): identical
+    positions, coefficients (bit for bit) and diagnostics."""
+    import torch
+    from oracle import sfft_oracle as O
+    xs = [O.synth(n, k, 25.0, 900 + s)[0].astype(np.complex64) for s in range(3)]
+    X = torch.stack([torch.as_tensor(x) for x in xs]).cuda()
+    cfg = sb.AlgorithmConfig(framework="voting", num_buckets=b, rounds=rounds)
+    ra = sb.run_voting_batch(X, k, cfg).to_results()
+    monkeypatch.setenv("SFFT_NO_VOTE_SLICED", "1")
+    rb = sb.run_voting_batch(X, k, cfg).to_results()
+    monkeypatch.delenv("SFFT_NO_VOTE_SLICED")
+    for a, c in zip(ra, rb):
+        assert a.samples_read == c.samples_read and a.iterations == c.iterations
+        assert list(a.spectrum.entries) == list(c.spectrum.entries)
+        for f, v in a.spectrum.entries.items():
+            assert np.complex128(v).tobytes() == np.complex128(c.spectrum.entries[f]).tobytes()
+    assert any(r.spectrum.entries for r in ra)
