@@ -60,6 +60,28 @@ struct Verdict {
   double2 c;
 };
 
+// Exact stand-ins for the 64-bit '%' and fmod of the classification, which sit
+// on the peel loop's critical path (one warp runs a dependent chain; a 64-bit
+// modulo is ~130 instructions): their arguments are within one or two periods
+// here, so conditional adds give the same values.
+//   w^{t f} for t < 3, 0 <= f < n
+__device__ __forceinline__ double2 unit_root_tf(int64_t n, int t, int64_t f) {
+  int64_t e = (int64_t)t * f;  // < 3 n
+  e -= (e >= n) ? n : 0;
+  e -= (e >= n) ? n : 0;
+  const double th = (-6.283185307179586 * (double)e) / (double)n;  // as unit_root
+  double s, c;
+  sincos(th, &s, &c);
+  return cmk(c, s);
+}
+//   fmod(x, nd) for |x| < 2 nd (x - nd is exact there: Sterbenz)
+__device__ __forceinline__ double fmod_near(double x, double nd) {
+  if (fabs(x) >= 2.0 * nd) return fmod(x, nd);
+  if (x >= nd) return x - nd;
+  if (x <= -nd) return x + nd;
+  return x;
+}
+
 // classify_bucket with a_max = 1 (sfft/reconstruct.py:412-440) after the
 // peeling pre-check (sfft/frameworks.py:653-658), one thread.  The
 // candidates {b + B i} are evenly spaced, so the nearest one under circular
@@ -92,15 +114,22 @@ __device__ Verdict classify_one(const PeelArgs& a, int s, int j, int64_t b, int3
   }
   const double nd = (double)n;
   const double2 r = cdiv(m[1], m[0]);
-  double raw = fmod(atan2(r.y, r.x) * (-nd / (2.0 * 3.141592653589793)), nd);
+  double raw = fmod_near(atan2(r.y, r.x) * (-nd / (2.0 * 3.141592653589793)), nd);
   if (raw != 0.0 && raw < 0.0) raw += nd;
   if (raw == 0.0) raw = 0.0;
   const int64_t i0 = (int64_t)floor((raw - (double)b) / (double)B);
   double bd = CUDART_INF;
   int64_t bc = 0x7fffffffffffffffll;
   for (int64_t di = -1; di <= 2; ++di) {
-    const int64_t cnd = pmod(b + B * pmod(i0 + di, L), n);
-    double d = fmod(((double)cnd - raw) + nd / 2.0, nd);
+    int64_t iw = i0 + di;  // in [-2, L + 2]: one wrap at most when L >= 8
+    if (L < 8) {
+      iw = pmod(iw, L);
+    } else {
+      iw += (iw < 0) ? L : 0;
+      iw -= (iw >= L) ? L : 0;
+    }
+    const int64_t cnd = b + B * iw;  // <= (B - 1) + B (L - 1) = n - 1
+    double d = fmod_near(((double)cnd - raw) + nd / 2.0, nd);
     if (d != 0.0 && d < 0.0) d += nd;
     d = fabs(d - nd / 2.0);
     if (d < bd || (d == bd && cnd < bc)) {
@@ -113,7 +142,7 @@ __device__ Verdict classify_one(const PeelArgs& a, int s, int j, int64_t b, int3
   double mx = 0.0;
   double2 sum = cmk(0.0, 0.0);
   for (int t = 0; t < ns; ++t) {
-    const double2 car = unit_root(n, mulmod(t, f, n));
+    const double2 car = unit_root_tf(n, t, f);
     mx = fmax(mx, cabs_(csub(m[t], cmul(m[0], car))));
     sum = cadd(sum, cmul(m[t], cconj(car)));
   }
@@ -377,7 +406,7 @@ __global__ void k_pe_peel(PeelArgs a, int64_t budget, int fast_forward) {
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         if (t < shL) {
-          cur.m[t] = csub(mold[t], cmul(my_c, unit_root(a.n, mulmod(t, my_f % a.n, a.n))));
+          cur.m[t] = csub(mold[t], cmul(my_c, unit_root_tf(a.n, t, my_f)));
           mp0[(int64_t)t * a.S * BL] = cur.m[t];
         }
       }
