@@ -77,6 +77,47 @@ __device__ __forceinline__ void bfly(double2* __restrict__ s, int base, int Mp, 
       s[base + 2 * Mp] = b2;
       s[base + 3 * Mp] = b3;
     }
+  } else if constexpr (R == 3) {
+    // X0 = a0 + t, X1/X2 = (a0 - t/2) -/+ i sin(2 pi/3) (a1 - a2), t = a1 + a2
+    constexpr double s3 = 0.86602540378443864676;
+    const double2 t = cadd(a[1], a[2]), d = csub(a[1], a[2]);
+    const double2 m = cmk(a[0].x - 0.5 * t.x, a[0].y - 0.5 * t.y);
+    const double2 x1 = cmk(m.x + s3 * d.y, m.y - s3 * d.x);
+    const double2 x2 = cmk(m.x - s3 * d.y, m.y + s3 * d.x);
+    s[base] = cadd(a[0], t);
+    if (j) {
+      s[base + Mp] = cmul(x1, __ldg(W + j * ws));
+      s[base + 2 * Mp] = cmul(x2, __ldg(W + 2 * j * ws));
+    } else {
+      s[base + Mp] = x1;
+      s[base + 2 * Mp] = x2;
+    }
+  } else if constexpr (R == 5) {
+    // t1 = a1 + a4, t2 = a2 + a3, d1 = a1 - a4, d2 = a2 - a3;
+    // X1/X4 = (a0 + c1 t1 + c2 t2) -/+ i (s1 d1 + s2 d2),
+    // X2/X3 = (a0 + c2 t1 + c1 t2) -/+ i (s2 d1 - s1 d2)
+    constexpr double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+    constexpr double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;
+    const double2 t1 = cadd(a[1], a[4]), t2 = cadd(a[2], a[3]);
+    const double2 d1 = csub(a[1], a[4]), d2 = csub(a[2], a[3]);
+    const double2 m1 = cmk(a[0].x + c1 * t1.x + c2 * t2.x, a[0].y + c1 * t1.y + c2 * t2.y);
+    const double2 m2 = cmk(a[0].x + c2 * t1.x + c1 * t2.x, a[0].y + c2 * t1.y + c1 * t2.y);
+    const double2 n1 = cmk(s1 * d1.x + s2 * d2.x, s1 * d1.y + s2 * d2.y);
+    const double2 n2 = cmk(s2 * d1.x - s1 * d2.x, s2 * d1.y - s1 * d2.y);
+    const double2 x1 = cmk(m1.x + n1.y, m1.y - n1.x), x4 = cmk(m1.x - n1.y, m1.y + n1.x);
+    const double2 x2 = cmk(m2.x + n2.y, m2.y - n2.x), x3 = cmk(m2.x - n2.y, m2.y + n2.x);
+    s[base] = cadd(a[0], cadd(t1, t2));
+    if (j) {
+      s[base + Mp] = cmul(x1, __ldg(W + j * ws));
+      s[base + 2 * Mp] = cmul(x2, __ldg(W + 2 * j * ws));
+      s[base + 3 * Mp] = cmul(x3, __ldg(W + 3 * j * ws));
+      s[base + 4 * Mp] = cmul(x4, __ldg(W + 4 * j * ws));
+    } else {
+      s[base + Mp] = x1;
+      s[base + 2 * Mp] = x2;
+      s[base + 3 * Mp] = x3;
+      s[base + 4 * Mp] = x4;
+    }
   } else {
     // generic odd radix: all inputs are in registers, so each output can be
     // formed and stored in turn (no second register array)
