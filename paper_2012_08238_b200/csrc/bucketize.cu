@@ -497,11 +497,49 @@ __global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2
   const int c0 = blockIdx.x * CG;
   const int seg = B1 + 1;
   const int B = (int)p.B;
-  for (int t = threadIdx.x; t < CG * B1; t += kNT) {
-    const int g = t % CG, n1 = t / CG;
-    const int n2 = c0 + g;
-    sm[g * seg + n1] = (n2 < B2) ? produce<Tin, MODE>(p, c, item, (int64_t)n1 * B2 + n2)
-                                 : cmk(0.0, 0.0);
+  if (MODE == PROD_SPIKE) {
+    // strided samples x[(L s - a) mod n], s = n1 B2 + n2 < B so L s < n: the
+    // index needs one conditional add, not a 64-bit modulo per sample, and
+    // (g, n1) advance incrementally; four gathers are in flight per thread
+    // before the first is stored (the kernel is bound by their latency)
+    const Tin* xs = (const Tin*)c.xs;
+    const int64_t n = p.n, Ls = n / p.B, am = pmod(c.a, n);
+    const int dg = kNT % CG, dn = kNT / CG;
+    int g = threadIdx.x % CG, n1 = threadIdx.x / CG;
+    for (int t = threadIdx.x; t < CG * B1; t += 4 * kNT) {
+      double2 v[4];
+      int at[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        at[u] = -1;
+        v[u] = cmk(0.0, 0.0);
+        if (t + u * kNT < CG * B1) {
+          at[u] = g * seg + n1;
+          const int n2 = c0 + g;
+          if (n2 < B2) {
+            int64_t idx = Ls * ((int64_t)n1 * B2 + n2) - am;
+            idx += (idx < 0) ? n : 0;
+            v[u] = Sample<Tin>::load(xs, idx);
+          }
+        }
+        g += dg;
+        n1 += dn;
+        if (g >= CG) {
+          g -= CG;
+          ++n1;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (at[u] >= 0) sm[at[u]] = v[u];
+    }
+  } else {
+    for (int t = threadIdx.x; t < CG * B1; t += kNT) {
+      const int g = t % CG, n1 = t / CG;
+      const int n2 = c0 + g;
+      sm[g * seg + n1] = (n2 < B2) ? produce<Tin, MODE>(p, c, item, (int64_t)n1 * B2 + n2)
+                                   : cmk(0.0, 0.0);
+    }
   }
   // digit-reversed positions once per CTA (behind the CG segments)
   int* pos = (int*)(sm + CG * seg);
@@ -509,13 +547,23 @@ __global__ void __launch_bounds__(kNT) k_cols(Prod p, FftPlan P1, int B1, int B2
   __syncthreads();
   fft_dif(sm, CG, seg, P1, W, B, threadIdx.x, kNT);
   double2* o = ws + (int64_t)item * B;
-  for (int t = threadIdx.x; t < CG * B1; t += kNT) {
-    const int g = t % CG, k1 = t / CG;
-    const int n2 = c0 + g;
-    if (n2 >= B2) continue;
-    const double2 v = sm[g * seg + pos[k1]];
-    const int e = n2 * k1;  // n2 < B2, k1 < B1: below B, no reduction needed
-    o[(int64_t)k1 * B2 + n2] = e ? cmul(v, __ldg(W + e)) : v;
+  {
+    const int dg = kNT % CG, dk = kNT / CG;  // (g, k1) of t = k1 CG + g, advanced by kNT
+    int g = threadIdx.x % CG, k1 = threadIdx.x / CG;
+    for (int t = threadIdx.x; t < CG * B1; t += kNT) {
+      const int n2 = c0 + g;
+      if (n2 < B2) {
+        const double2 v = sm[g * seg + pos[k1]];
+        const int e = n2 * k1;  // n2 < B2, k1 < B1: below B, no reduction needed
+        o[(int64_t)k1 * B2 + n2] = e ? cmul(v, __ldg(W + e)) : v;
+      }
+      g += dg;
+      k1 += dk;
+      if (g >= CG) {
+        g -= CG;
+        ++k1;
+      }
+    }
   }
 }
 
@@ -537,10 +585,19 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
   const int seg = B2 + 1;
   const int B = B1 * B2;
   const double2* in = ws + (int64_t)item * B;
-  for (int t = threadIdx.x; t < RG * B2; t += kNT) {
-    const int g = t / B2, n2 = t - g * B2;
-    const int k1 = r0 + g;
-    sm[g * seg + n2] = (k1 < B1) ? in[(int64_t)k1 * B2 + n2] : cmk(0.0, 0.0);
+  {
+    const int dn = kNT % B2, dg = kNT / B2;  // (g, n2) of t = g B2 + n2, advanced by kNT
+    int g = threadIdx.x / B2, n2 = threadIdx.x % B2;
+    for (int t = threadIdx.x; t < RG * B2; t += kNT) {
+      const int k1 = r0 + g;
+      sm[g * seg + n2] = (k1 < B1) ? in[(int64_t)k1 * B2 + n2] : cmk(0.0, 0.0);
+      n2 += dn;
+      g += dg;
+      if (n2 >= B2) {
+        n2 -= B2;
+        ++g;
+      }
+    }
   }
   int* pos = (int*)(sm + RG * seg);
   for (int k = threadIdx.x; k < B2; k += kNT) pos[k] = fft_pos(k, P2);
@@ -550,11 +607,19 @@ __global__ void __launch_bounds__(kNT) k_rows(const double2* __restrict__ ws, Ff
                                  : (out_M > 0 ? (item % out_M) * out_S + item / out_M : item);
   double2* o = out + row * B;
   const double bd = (double)B;
-  for (int t = threadIdx.x; t < RG * B2; t += kNT) {
-    const int g = t % RG, k2 = t / RG;
-    const int k1 = r0 + g;
-    if (k1 >= B1) continue;
-    o[k1 + (int64_t)B1 * k2] = cdivr(sm[g * seg + pos[k2]], bd);
+  {
+    const int dg = kNT % RG, dk = kNT / RG;  // (g, k2) of t = k2 RG + g, advanced by kNT
+    int g = threadIdx.x % RG, k2 = threadIdx.x / RG;
+    for (int t = threadIdx.x; t < RG * B2; t += kNT) {
+      const int k1 = r0 + g;
+      if (k1 < B1) o[k1 + (int64_t)B1 * k2] = cdivr(sm[g * seg + pos[k2]], bd);
+      g += dg;
+      k2 += dk;
+      if (g >= RG) {
+        g -= RG;
+        ++k2;
+      }
+    }
   }
 }
 
