@@ -432,3 +432,36 @@ def test_voting_sliced_scan_identical(sb, monkeypatch, n, b, k, rounds):
         for f, v in a.spectrum.entries.items():
             assert np.complex128(v).tobytes() == np.complex128(c.spectrum.entries[f]).tobytes()
     assert any(r.spectrum.entries for r in ra)
+
+
+@pytest.mark.parametrize("factors", [(3, 5, 7, 11), (3, 4, 5, 7, 11), (5, 7, 8, 9, 11, 13), (3, 25, 49)])
+def test_peeling_windows_match_plain_loop(sb, monkeypatch, factors):
+    """Windows of independent peels and the cycle fast-forward against the plain
+    one-peel-per-step loop (SFFT_PEEL_NO_FF=1) on small co-prime lengths with
+    two-shift (unverified) stages, exact and noisy inputs, sparse and crowded:
+    results, peel counts and flags bit for bit."""
+    import torch
+    from oracle import sfft_oracle as O
+    n = int(np.prod(factors))
+    xs, ks = [], []
+    for seed in range(24):
+        k = [2, 5, 11, 23][seed % 4]
+        snr = [None, 40.0, 15.0][seed % 3]
+        xs.append(O.synth(n, min(k, n // 4), snr, 7000 + seed)[0])
+        ks.append(min(k, n // 4))
+    cfg = sb.AlgorithmConfig(framework="peeling", coprime_factors=factors)
+    for dtype in (np.complex128, np.complex64):
+        for k in sorted(set(ks)):
+            sel = [x.astype(dtype) for x, kk in zip(xs, ks) if kk == k]
+            X = torch.stack([torch.as_tensor(x) for x in sel]).cuda()
+            ra = sb.run_peeling_batch(X, k, cfg).to_results()
+            monkeypatch.setenv("SFFT_PEEL_NO_FF", "1")
+            rb = sb.run_peeling_batch(X, k, cfg).to_results()
+            monkeypatch.delenv("SFFT_PEEL_NO_FF")
+            for a, b in zip(ra, rb):
+                assert (a.iterations, a.converged, a.samples_read) == \
+                    (b.iterations, b.converged, b.samples_read)
+                assert list(a.spectrum.entries) == list(b.spectrum.entries)
+                for f, v in a.spectrum.entries.items():
+                    assert np.complex128(v).tobytes() == \
+                        np.complex128(b.spectrum.entries[f]).tobytes()
