@@ -588,8 +588,10 @@ __global__ void k_pe_stuck(PeelArgs a, int32_t* conv, int32_t* iters) {
 __global__ void k_pe_items(int S, int ns, int32_t* item_sig, int64_t* tau) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S * ns) return;
-  item_sig[i] = i % S;
-  tau[i] = i / S;
+  // signal-major: the shifts 0..ns-1 of a signal are neighbouring items, so
+  // they run together and share the 32-byte sectors their samples sit in
+  item_sig[i] = i / ns;
+  tau[i] = i % ns;
 }
 
 __global__ void k_pe_groups(PeelArgs a, Group* groups, int32_t* ngroups) {
@@ -754,6 +756,8 @@ int run_peeling(int dtype, const void* x, int64_t n, int64_t xstride, int S,
     p.B = a.Bs[j];
     p.item_sig = item_sig;
     p.item_a = item_tau;
+    p.out_M = ns;  // item s*ns + t writes row t*S + s of meas_j [ns][S][B_j]
+    p.out_S = S;
     int rc = run_bucketize(dtype, PROD_SPIKE, p, (int64_t)S * ns, Wst[j], a.meas + a.moff[j], bws,
                            (size_t)d.bws, st);
     if (rc) return rc;
