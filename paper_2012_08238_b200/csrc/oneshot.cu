@@ -467,8 +467,10 @@ __global__ void k_os_items(int S, int nsh, const int64_t* shifts, int32_t* item_
                            int64_t* item_tau) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)S * nsh) return;
-  item_sig[i] = (int32_t)(i % S);
-  item_tau[i] = shifts[i / S];
+  // signal-major: a signal's shifts are neighbouring items (shifts 0, 1, 2, ...
+  // read neighbouring samples: shared 32-byte sectors)
+  item_sig[i] = (int32_t)(i / nsh);
+  item_tau[i] = shifts[i % nsh];
 }
 
 __global__ void k_os_groups(int S, int nsh, int64_t n, int64_t B, const int64_t* shifts,
@@ -590,6 +592,8 @@ int run_oneshot(int dtype, const void* x, int64_t n, int64_t xstride, int S, int
   p.B = B;
   p.item_sig = item_sig;
   p.item_a = item_tau;
+  p.out_M = nsh;  // item s*nsh + t writes row t*S + s
+  p.out_S = S;
   int rc = run_bucketize(dtype, PROD_SPIKE, p, nitems, W, (double2*)a.meas, bws,
                          bucketize_ws_bytes(B, nitems), st);
   if (rc) return rc;
