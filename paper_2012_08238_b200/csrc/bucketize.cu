@@ -1633,7 +1633,23 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
   }
   SFFT_DASSERT(item >= 0 && (gfirst || item < (int)gridDim.x));
   double2* row = y + (int64_t)item_row[item] * M;
-  for (int e = threadIdx.x; e < M / 8; e += kFrowNT) tw8[e] = __ldg(W + 8 * e);
+  // stage twiddles laid out [stage][q][j] (j contiguous): thread j of a warp
+  // reads consecutive entries for every q.  The flat table tw8[j q 8^(st-1)]
+  // made the eight j of the Mp = 8 stage hit one bank group for every q (8-way
+  // conflicts on 7 loads per butterfly; ncu: L1/TEX 91 % busy, DRAM 38 %).
+  // Same table values, so the results are unchanged bit for bit.
+  {
+    int off = 0, Mbs = M / 8;
+    for (int st = 1; st < Pow2<M>::N8; ++st) {
+      const int Mps = Mbs >> 3;
+      for (int e = threadIdx.x; e < 7 * Mps; e += kFrowNT) {
+        const int q = e / Mps + 1, j = e - (q - 1) * Mps;
+        tw8[off + e] = __ldg(W + (int64_t)j * q * (M / Mbs));
+      }
+      off += 7 * Mps;
+      Mbs = Mps;
+    }
+  }
   // stage 1 straight from global memory: the 8 inputs of a butterfly and its
   // twiddles are all requested at once (one round trip), then written to
   // shared memory already transformed
@@ -1651,10 +1667,11 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
   }
   __syncthreads();
   int Mb = Mp1;
+  int toff = 0;
 #pragma unroll 1
   for (int st = 1; st < Pow2<M>::N8; ++st) {
     const int Mp = Mb >> 3;
-    const int tstr8 = M / Mb / 8;  // twiddle index j q (M / Mb) = 8 * (j q tstr8)
+    const double2* tws = tw8 + toff;  // tws[(q - 1) Mp + j] = w_M^{j q (M / Mb)}
     for (int t = threadIdx.x; t < M / 8; t += kFrowNT) {
       const int blk = t / Mp, j = t - blk * Mp;
       const int base = blk * Mb + j;
@@ -1665,9 +1682,10 @@ __global__ void __launch_bounds__(kFrowNT) k_fft_rows(const int32_t* __restrict_
       fr_s[frow_pad(base)] = a[0];
 #pragma unroll
       for (int q = 1; q < 8; ++q)
-        fr_s[frow_pad(base + q * Mp)] = j ? cmul(a[q], tw8[j * q * tstr8]) : a[q];
+        fr_s[frow_pad(base + q * Mp)] = j ? cmul(a[q], tws[(q - 1) * Mp + j]) : a[q];
     }
     __syncthreads();
+    toff += 7 * Mp;
     Mb = Mp;
   }
   if (Pow2<M>::RL == 4) {
