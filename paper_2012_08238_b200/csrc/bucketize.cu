@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
   const int B = CL * M;
   double2* a = sm;               // [NI][M] folded slots of this CTA
   double2* bq = sm + NI * M;     // [NI][M] sub-transform inputs
-  double2* tw = bq + NI * M;     // [M] w_M^e
+  double2* tw = bq + NI * M;     // [< M] stage twiddles of fft_pow2
   if (threadIdx.x < NI) {
     const int64_t it = item0 + threadIdx.x;
     const bool in = it < nitems;
@@ -339,7 +339,19 @@ __global__ void __launch_bounds__(kClNT, cluster_min_blocks<Tin, MODE>())
     s_ctx[threadIdx.x] = c;
     s_live[threadIdx.x] = in && !c.skip;
   }
-  for (int e = threadIdx.x; e < M; e += kClNT) tw[e] = __ldg(W + (int64_t)e * CL);
+  // stage twiddles of fft_pow2 laid out [stage][q][j] (see fft.cuh): w_M^e = W[e CL]
+  {
+    int off = 0, Mbs = M;
+    for (int st = 0; st < Pow2<M>::N8; ++st) {
+      const int Mps = Mbs >> 3;
+      for (int e = threadIdx.x; e < 7 * Mps; e += kClNT) {
+        const int q = e / Mps + 1, j = e - (q - 1) * Mps;
+        tw[off + e] = __ldg(W + (int64_t)j * q * (M / Mbs) * CL);
+      }
+      off += 7 * Mps;
+      Mbs = Mps;
+    }
+  }
   __syncthreads();
   int nl = 0;
 #pragma unroll

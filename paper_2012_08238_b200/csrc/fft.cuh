@@ -173,8 +173,8 @@ __device__ __forceinline__ void fft_dif(double2* s, int G, int seg, const FftPla
 // ---------------------------------------------------------------- pow2 FFT
 // Radix-8 register butterflies for power-of-two lengths M = 2^LG (then one
 // radix-2/4 stage when LG % 3 != 0), NI segments of length M at s + i*M,
-// every butterfly of a stage on its own thread.  Twiddles tw[e] = w_M^e
-// (shared memory).  Output k of a segment lands at pow2_pos<M>(k).
+// every butterfly of a stage on its own thread.  Output k of a segment lands
+// at pow2_pos<M>(k).
 __device__ __forceinline__ void dft4_(double2& x0, double2& x1, double2& x2, double2& x3) {
   const double2 t0 = cadd(x0, x2), t1 = csub(x0, x2);
   const double2 t2 = cadd(x1, x3), d = csub(x1, x3);
@@ -231,13 +231,16 @@ __device__ __forceinline__ int pow2_pos(int k) {
   return pos;
 }
 
+// tw: the stage twiddles laid out [stage][q][j], tw[off_st + (q - 1) Mp + j] =
+// w_M^{j q (M / Mb)} with Mb = M / 8^st, Mp = Mb / 8 (fewer than M entries in
+// all): the threads of a warp read consecutive j for every q, where a flat
+// table w_M^e made the few j of a late stage collide on one bank group.
 template <int M, int NI, int NT>
 __device__ __forceinline__ void fft_pow2(double2* __restrict__ s, const double2* __restrict__ tw) {
   int Mb = M;
 #pragma unroll 1
   for (int st = 0; st < Pow2<M>::N8; ++st) {
     const int Mp = Mb >> 3;
-    const int tstr = M / Mb;
 #pragma unroll 1
     for (int t = threadIdx.x; t < NI * (M / 8); t += NT) {
       const int seg = t / (M / 8), tt = t - seg * (M / 8);
@@ -249,9 +252,10 @@ __device__ __forceinline__ void fft_pow2(double2* __restrict__ s, const double2*
       dft8_(a);
       x[0] = a[0];
 #pragma unroll
-      for (int q = 1; q < 8; ++q) x[q * Mp] = j ? cmul(a[q], tw[j * q * tstr]) : a[q];
+      for (int q = 1; q < 8; ++q) x[q * Mp] = j ? cmul(a[q], tw[(q - 1) * Mp + j]) : a[q];
     }
     __syncthreads();
+    tw += 7 * Mp;
     Mb = Mp;
   }
   if (Pow2<M>::RL == 4) {
